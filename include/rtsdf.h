@@ -1,0 +1,213 @@
+/*
+ * rtsdf.h -- C ABI of the B200-native RTSDF hot path (librtsdf.so).
+ *
+ * The reference (`sdfshadow`, Python + numba, /root/reference/pkg/src/sdfshadow)
+ * has no FFI: every public op is a Python validator around ONE numba kernel
+ * called with raw arrays plus scalar dims/spacings.  Each entry point below
+ * replaces exactly one of those kernel calls; the file:line it replaces is
+ * cited on each declaration.  The Python host package
+ * (paper_2210_06160_b200/) binds these with ctypes, keeping the reference's
+ * function names, argument meaning and exception types.
+ *
+ * Conventions
+ *   - All array arguments are DEVICE pointers unless marked (host).  The caller
+ *     owns every buffer; workspace sizes are queried with *_ws_bytes.
+ *   - `stream` is a cudaStream_t passed as void*; every call is asynchronous on
+ *     it, deterministic, and free of order-dependent atomics.
+ *   - Grids are C-order (nx, ny, nz), z fastest, like the reference arrays.
+ *   - Seeds inside the library are PACKED int32: (i << 20) | (j << 10) | k,
+ *     EMPTY = -1.  Numeric order == lexicographic (i, j, k) order.  Each dim
+ *     must be <= 1024.  rtsdf_seeds_packed_to_linear converts to the
+ *     reference's linear index (jfa.py:31,53).
+ *   - Return value: 0 on success, else an RTSDF_ERR_* code; no exceptions or
+ *     exits cross the ABI.  rtsdf_last_error() gives a message (thread-local).
+ */
+#ifndef RTSDF_H
+#define RTSDF_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+    RTSDF_OK = 0,
+    RTSDF_ERR_INVALID = 1,   /* bad argument (maps to ValueError)            */
+    RTSDF_ERR_CUDA = 2,      /* CUDA launch / runtime failure (RuntimeError) */
+    RTSDF_ERR_DIMS = 3,      /* unsupported grid dims (> 1024 per axis)      */
+    RTSDF_ERR_WORKSPACE = 4  /* workspace too small                          */
+};
+
+const char* rtsdf_version(void);
+const char* rtsdf_last_error(void);
+/* number of kernel launches issued by this library since load (diagnostics) */
+int64_t rtsdf_launch_count(void);
+
+/* ---------------------------------------------------------------- voxelize */
+/* Replaces voxel.py:179 (_voxelize_kernel call) + the OOB check voxel.py:168-175
+ * + jfa.py:98 (jfa_init's np.where).  Conservative closed-box 13-axis SAT in
+ * fp64 without FMA.  occ (nullable) is zeroed then set to 1 per occupied cell;
+ * seed_packed (nullable) is set to EMPTY then self-seeded per occupied cell.
+ * counters (device, int64[2]) receive [0] = triangles outside [lo, hi],
+ * [1] = occupied-cell writes (> 0 iff any cell occupied).  bad_flags (nullable,
+ * uint8[n_tris]) receives 1 for each out-of-bounds triangle.               */
+size_t rtsdf_voxelize_ws_bytes(int64_t n_tris);
+int rtsdf_voxelize(const double* verts, int64_t n_verts, const int32_t* tris, int64_t n_tris,
+                   const double* lo /*host[3]*/, const double* hi /*host[3]*/, int nx, int ny,
+                   int nz, uint8_t* occ, int32_t* seed_packed, int64_t* counters,
+                   uint8_t* bad_flags, void* ws, size_t ws_bytes, void* stream);
+
+/* --------------------------------------------------------------------- JFA */
+/* Replaces jfa.py:98 (jfa_init): seed = packed(c) if occ[c] else EMPTY;
+ * count (device int64, nullable) += occupied cells.                         */
+int rtsdf_jfa_init(const uint8_t* occ, int nx, int ny, int nz, int32_t* seed_packed,
+                   int64_t* count, void* stream);
+
+/* Replaces jfa.py:180 (_jfa_step_kernel call): one 27-tap pass at `offset`.
+ * Adopt iff fp64 d2 (jfa.py:72-76, left to right, no FMA) is smaller, or equal
+ * and the seed is lexicographically smaller (jfa.py:116-124).  (wx, wy, wz) > 0
+ * asserts hx^2 : hy^2 : hz^2 == wx : wy : wz EXACTLY (host-checked with exact
+ * rationals); the kernel then orders candidates by the integer
+ * q = wx dx^2 + wy dy^2 + wz dz^2 and evaluates fp64 d2 only on integer ties.
+ * (0, 0, 0) = general fp64 path.                                            */
+int rtsdf_jfa_step(const int32_t* src, int32_t* dst, int nx, int ny, int nz, int offset,
+                   double hx, double hy, double hz, int wx, int wy, int wz, void* stream);
+
+/* Slab form for z-slab (outer-axis) sharding across GPUs: this rank owns global
+ * planes [x0, x0 + nxl) of an nx-plane grid in `local`; halo_lo holds global
+ * planes [lo_first, lo_first + n_lo) and halo_hi [hi_first, hi_first + n_hi)
+ * (received from other ranks).  Output: dst (nxl planes).  Every plane a
+ * cell needs must be present; the host schedules the exchange.              */
+int rtsdf_jfa_step_slab(const int32_t* local, const int32_t* halo_lo, const int32_t* halo_hi,
+                        int32_t* dst, int nx, int x0, int nxl, int lo_first, int n_lo,
+                        int hi_first, int n_hi, int ny, int nz, int offset, double hx,
+                        double hy, double hz, int wx, int wy, int wz, void* stream);
+
+/* Replaces jfa.py:140-145 (jfa_run's pass loop): runs the whole schedule
+ * n/2 .. 1 ping-ponging between buf_a (holding the init seeds) and buf_b.
+ * *which (host) = 0 if the result is in buf_a, 1 if in buf_b.               */
+int rtsdf_jfa_run(int32_t* buf_a, int32_t* buf_b, int nx, int ny, int nz, double hx, double hy,
+                  double hz, int wx, int wy, int wz, int* which, void* stream);
+
+/* Replaces jfa.py:224 (_seed_distance_kernel): out = f32(sqrt(d2_fp64) - beta).
+ * empty_count (device int64, nullable) += EMPTY cells (NoSeedsError check,
+ * jfa.py:176-177).  x0/nx_global: slab offset (0 / nx for a whole grid).    */
+int rtsdf_seeds_to_sdf(const int32_t* seed_packed, float* out, int nx, int ny, int nz,
+                       double hx, double hy, double hz, double beta, int64_t* empty_count,
+                       void* stream);
+int rtsdf_seeds_packed_to_linear(const int32_t* packed, int32_t* linear, int nx, int ny, int nz,
+                                 void* stream);
+int rtsdf_seeds_linear_to_packed(const int32_t* linear, int32_t* packed, int nx, int ny, int nz,
+                                 void* stream);
+
+/* ---------------------------------------------------- resample, mask, band */
+/* Replaces raysample.py:114 (_coarse_at_fine_kernel) and the band-exit reset
+ * raysample.py:288-295.  Per fine texel: v = fp64 trilinear of coarse at
+ * clo + (i + 0.5) fh (field.py:95-128); mask = v <= d (fp64).
+ *   c_fine (nullable): f32(v) for every texel;
+ *   out_unmasked (nullable): f32(v) where !mask (raysample.py:290), untouched
+ *                            where masked (the sampler writes those);
+ *   mask_new (nullable) u8; block_counts (nullable, int32[n_blocks]) masked
+ *   count per RS_CELLS_PER_BLOCK chunk for rtsdf_compact_mask;
+ *   mask_old + run_min/front/back (nullable): reset where mask_old & !mask. */
+int64_t rtsdf_mask_blocks(int64_t n_cells);
+int rtsdf_resample_mask(const float* coarse, int cnx, int cny, int cnz,
+                        const double* clo /*host[3]*/, const double* ch /*host[3]*/, int fnx,
+                        int fny, int fnz, const double* fh /*host[3]*/, double d, float* c_fine,
+                        float* out_unmasked, uint8_t* mask_new, int32_t* block_counts,
+                        const uint8_t* mask_old, float* run_min, int32_t* front, int32_t* back,
+                        void* stream);
+/* Replaces raysample.py:266 (np.flatnonzero): ascending int64 indices of
+ * mask != 0; *count (device int64) = M.  Needs block_counts from
+ * rtsdf_resample_mask (or NULL to recount).                                 */
+size_t rtsdf_compact_ws_bytes(int64_t n_cells);
+int rtsdf_compact_mask(const uint8_t* mask, int64_t n_cells, int32_t* block_counts,
+                       int64_t* idx, int64_t* count, void* ws, size_t ws_bytes, void* stream);
+
+/* --------------------------------------------------------------------- BVH */
+/* Replaces geometry.py:202-267 (build_bvh), on the host (plain C++, same
+ * median split on the longest node-bbox axis, stable order, leaf <= 4) so the
+ * tree -- and therefore traversal order and pruning -- is the reference's.
+ * All pointers HOST.  node arrays sized >= 2*T-1.  Returns node count (< 0 on
+ * error).                                                                   */
+int64_t rtsdf_bvh_build_host(const double* tri_lo, const double* tri_hi, int64_t n_tris,
+                             double* node_lo, double* node_hi, int32_t* node_left,
+                             int32_t* node_right, int32_t* order);
+/* Pack the flat BVH (device SoA as in BvhIndex, geometry.py:186-195) into the
+ * device traversal layout: nodes (64 B each) and triangles (128 B each).    */
+size_t rtsdf_bvh_packed_bytes(int64_t n_nodes, int64_t n_tris);
+int rtsdf_bvh_pack(const double* node_lo, const double* node_hi, const int32_t* node_left,
+                   const int32_t* node_right, const int32_t* order, const double* tri_a,
+                   const double* tri_e1, const double* tri_e2, const double* tri_n,
+                   int64_t n_nodes, int64_t n_tris, void* packed, void* stream);
+
+/* Replaces geometry.py:395-410 (ray_query) for a batch of rays.            */
+int rtsdf_ray_query(const void* bvh_packed, int64_t n_nodes, const double* origins,
+                    const double* dirs, int64_t n, double t_max, double* out_t, int32_t* out_id,
+                    int32_t* out_facing, void* stream);
+
+/* ---------------------------------------------- ray-sampled refine + Eq. 1 */
+/* Replaces raysample.py:277-299 (_sample_masked_kernel + band reset +
+ * _update_masked_kernel) fused: one warp per masked texel idx[n], one lane
+ * per ray (x <= 32 per round, looped), warp-reduced min/front/back -- no
+ * atomics.  M is read from device memory (*count from rtsdf_compact_mask)
+ * so no host sync is needed; m_cap bounds the grid.
+ *   dirs (nullable): host-supplied table dirs[(n*x + r)*3 + c] (parity mode);
+ *                    NULL = on-device SplitMix64 stream (rng.py:30-53).
+ *   samp_min/front/back (nullable): per-texel frame results.
+ *   update (prev != NULL): Eq. 1 combine + sign into out for masked texels,
+ *     with c recomputed by the same trilinear as rtsdf_resample_mask; prev
+ *     and out may alias (in-place).                                        */
+typedef struct {
+    const float* coarse;
+    int cnx, cny, cnz;
+    double clo[3], ch[3];
+    int fnx, fny, fnz;
+    double fh[3];
+} rtsdf_resample_desc;
+
+int rtsdf_sample_update(const void* bvh_packed, int64_t n_nodes, const int64_t* idx,
+                        const int64_t* count, int64_t m_cap, const rtsdf_resample_desc* rs,
+                        int x, uint64_t seed, int64_t frame, double t_max, const double* dirs,
+                        double* samp_min, int32_t* samp_front, int32_t* samp_back,
+                        const float* prev, const uint8_t* mask_old, float* run_min,
+                        int32_t* front, int32_t* back, double alpha, float* out, void* stream);
+
+/* ------------------------------------------------------------- soft shadow */
+/* Replaces render.py:167 (_occlusion_kernel): per covered pixel fp64 sphere
+ * trace with the triangulated cone term (raymarch.py:83-147).               */
+int rtsdf_occlusion(const float* field, int nx, int ny, int nz, const double* lo /*host[3]*/,
+                    const double* h /*host[3]*/, const double* g_pos, const double* g_nrm,
+                    const uint8_t* g_cov, int height, int width, const double* light /*host[3]*/,
+                    double eps, int max_iter, double max_step, double t_max, double k,
+                    double jitter, double offset, int draws, uint64_t seed, double* out,
+                    void* stream);
+/* Replaces raymarch.py:128 (_march from sphere_trace) for a batch.          */
+int rtsdf_sphere_trace(const float* field, int nx, int ny, int nz, const double* lo,
+                       const double* h, const double* origins, const double* dirs, int64_t n,
+                       double eps, int max_iter, double max_step, double t_max,
+                       const double* t0 /*nullable*/, double k, int32_t* status, double* t,
+                       int32_t* iters, double* min_term, void* stream);
+/* Replaces field.py:354-360 (_sample_many).                                */
+int rtsdf_trilinear_many(const float* field, int nx, int ny, int nz, const double* lo,
+                         const double* h, const double* pts, int64_t n, double* out,
+                         void* stream);
+/* Replaces render.py:123 (_gbuffer_kernel).  cam (host[12]) = pos, fwd,
+ * right, up.                                                                */
+int rtsdf_gbuffer(const void* bvh_packed, int64_t n_nodes, const double* normals_orig,
+                  const float* albedo_orig, const double* cam, double half_w, double half_h,
+                  int width, int height, double* out_pos, double* out_nrm, float* out_alb,
+                  uint8_t* out_cov, void* stream);
+/* Replaces render.py:186-192 (compose).                                    */
+int rtsdf_compose(const double* g_nrm, const float* g_alb, const uint8_t* g_cov,
+                  const double* occ, int height, int width, const double* light /*host[3]*/,
+                  const double* background /*host[3]*/, float* out_rgb, void* stream);
+/* Replaces field.py:373 (apply_bias): out = data - f32(bias) in f32.       */
+int rtsdf_apply_bias(const float* data, int64_t n, float bias, float* out, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RTSDF_H */

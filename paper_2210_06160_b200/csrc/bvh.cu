@@ -1,0 +1,176 @@
+// bvh.cu -- K5: BVH build (host), device packing, batched closest-hit queries.
+//
+// Build: geometry.py:202-267 restated in C++: median split on the longest
+// NODE-bbox axis by triangle-bbox centroid, stable order, leaf <= 4, preorder
+// node numbering.  Building the reference's own tree (instead of an LBVH)
+// keeps traversal order and best-t pruning identical, so closest hits,
+// facing and tie-breaks match the reference bit for bit even in the fp64
+// corner cases where a different tree could prune differently.  The build is
+// per scene view (static scenes build once, scenes.py:383-390); C++ makes the
+// 1.31 M-triangle C4 mesh ~100x faster than the reference's recursive Python.
+#include <algorithm>
+#include <cmath>
+#include <numeric>
+#include <vector>
+
+#include "common.cuh"
+
+namespace rtsdf {
+
+struct HostBuild {
+    const double* tri_lo;
+    const double* tri_hi;
+    std::vector<double> cen;
+    double* node_lo;
+    double* node_hi;
+    int32_t* left;
+    int32_t* right;
+    int32_t* order;
+    int64_t n_nodes = 0;
+    int64_t n_out = 0;
+    std::vector<double> keys;
+    std::vector<int64_t> perm;
+
+    int64_t build(int64_t* idx, int64_t n) {
+        int64_t me = n_nodes++;
+        double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+        for (int64_t q = 0; q < n; ++q)
+            for (int a = 0; a < 3; ++a) {
+                double l = tri_lo[3 * idx[q] + a], h = tri_hi[3 * idx[q] + a];
+                if (l < lo[a]) lo[a] = l;
+                if (h > hi[a]) hi[a] = h;
+            }
+        for (int a = 0; a < 3; ++a) {
+            node_lo[3 * me + a] = lo[a];
+            node_hi[3 * me + a] = hi[a];
+        }
+        if (n <= 4) {
+            int64_t start = n_out;
+            for (int64_t q = 0; q < n; ++q) order[n_out++] = (int32_t)idx[q];
+            left[me] = (int32_t)(-(start + 1));
+            right[me] = (int32_t)n;
+            return me;
+        }
+        double ext[3] = {hi[0] - lo[0], hi[1] - lo[1], hi[2] - lo[2]};
+        int axis = 0;  // np.argmax: first maximum wins
+        if (ext[1] > ext[axis]) axis = 1;
+        if (ext[2] > ext[axis]) axis = 2;
+        // np.argsort(kind="stable") of the centroid keys, then gather
+        std::vector<std::pair<double, int64_t>> kv((size_t)n);
+        for (int64_t q = 0; q < n; ++q) kv[q] = {cen[3 * idx[q] + axis], idx[q]};
+        std::stable_sort(kv.begin(), kv.end(),
+                         [](const std::pair<double, int64_t>& a, const std::pair<double, int64_t>& b) {
+                             return a.first < b.first;
+                         });
+        for (int64_t q = 0; q < n; ++q) idx[q] = kv[q].second;
+        std::vector<std::pair<double, int64_t>>().swap(kv);
+        int64_t half = n / 2;
+        int64_t l = build(idx, half);
+        int64_t r = build(idx + half, n - half);
+        left[me] = (int32_t)l;
+        right[me] = (int32_t)r;
+        return me;
+    }
+};
+
+__global__ void bvh_pack_kernel(const double* __restrict__ node_lo, const double* __restrict__ node_hi,
+                                const int32_t* __restrict__ node_left,
+                                const int32_t* __restrict__ node_right,
+                                const int32_t* __restrict__ order, const double* __restrict__ tri_a,
+                                const double* __restrict__ tri_e1, const double* __restrict__ tri_e2,
+                                const double* __restrict__ tri_n, int64_t n_nodes, int64_t n_tris,
+                                BvhNode* __restrict__ nodes, BvhTri* __restrict__ tris) {
+    int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (q < n_nodes) {
+        BvhNode nd;
+        for (int a = 0; a < 3; ++a) {
+            nd.lo[a] = node_lo[3 * q + a];
+            nd.hi[a] = node_hi[3 * q + a];
+        }
+        nd.left = node_left[q];
+        nd.right = node_right[q];
+        nodes[q] = nd;
+    }
+    if (q < n_tris) {
+        BvhTri t;
+        for (int a = 0; a < 3; ++a) {
+            t.a[a] = tri_a[3 * q + a];
+            t.e1[a] = tri_e1[3 * q + a];
+            t.e2[a] = tri_e2[3 * q + a];
+            t.n[a] = tri_n[3 * q + a];
+        }
+        t.orig = order[q];
+        for (int p = 0; p < 7; ++p) t.pad[p] = 0;
+        tris[q] = t;
+    }
+}
+
+__global__ void ray_query_kernel(BvhView b, const double* __restrict__ orig,
+                                 const double* __restrict__ dirs, int64_t n, double t_max,
+                                 double* __restrict__ out_t, int32_t* __restrict__ out_id,
+                                 int32_t* __restrict__ out_facing) {
+    int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (q >= n) return;
+    int32_t id;
+    int facing;
+    double t = bvh_ray(b, orig[3 * q], orig[3 * q + 1], orig[3 * q + 2], dirs[3 * q],
+                       dirs[3 * q + 1], dirs[3 * q + 2], t_max, id, facing);
+    out_t[q] = t;
+    out_id[q] = id;
+    out_facing[q] = facing;
+}
+
+}  // namespace rtsdf
+
+using namespace rtsdf;
+
+extern "C" int64_t rtsdf_bvh_build_host(const double* tri_lo, const double* tri_hi,
+                                        int64_t n_tris, double* node_lo, double* node_hi,
+                                        int32_t* node_left, int32_t* node_right, int32_t* order) {
+    if (n_tris < 1) {
+        set_error("bvh_build: empty mesh");
+        return -1;
+    }
+    HostBuild b;
+    b.tri_lo = tri_lo;
+    b.tri_hi = tri_hi;
+    b.cen.resize((size_t)(3 * n_tris));
+    for (int64_t q = 0; q < 3 * n_tris; ++q) b.cen[q] = (tri_lo[q] + tri_hi[q]) * 0.5;  // geometry.py:211
+    b.node_lo = node_lo;
+    b.node_hi = node_hi;
+    b.left = node_left;
+    b.right = node_right;
+    b.order = order;
+    std::vector<int64_t> idx((size_t)n_tris);
+    std::iota(idx.begin(), idx.end(), (int64_t)0);
+    b.build(idx.data(), n_tris);
+    return b.n_nodes;
+}
+
+extern "C" size_t rtsdf_bvh_packed_bytes(int64_t n_nodes, int64_t n_tris) {
+    return (size_t)n_nodes * sizeof(BvhNode) + (size_t)n_tris * sizeof(BvhTri);
+}
+
+extern "C" int rtsdf_bvh_pack(const double* node_lo, const double* node_hi,
+                              const int32_t* node_left, const int32_t* node_right,
+                              const int32_t* order, const double* tri_a, const double* tri_e1,
+                              const double* tri_e2, const double* tri_n, int64_t n_nodes,
+                              int64_t n_tris, void* packed, void* stream) {
+    BvhView v = bvh_view(packed, n_nodes);
+    int64_t n = n_nodes > n_tris ? n_nodes : n_tris;
+    bvh_pack_kernel<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+        node_lo, node_hi, node_left, node_right, order, tri_a, tri_e1, tri_e2, tri_n, n_nodes,
+        n_tris, (BvhNode*)v.nodes, (BvhTri*)v.tris);
+    count_launch();
+    return check_launch("bvh_pack");
+}
+
+extern "C" int rtsdf_ray_query(const void* packed, int64_t n_nodes, const double* origins,
+                               const double* dirs, int64_t n, double t_max, double* out_t,
+                               int32_t* out_id, int32_t* out_facing, void* stream) {
+    if (n <= 0) return RTSDF_OK;
+    ray_query_kernel<<<(unsigned)((n + 127) / 128), 128, 0, (cudaStream_t)stream>>>(
+        bvh_view(packed, n_nodes), origins, dirs, n, t_max, out_t, out_id, out_facing);
+    count_launch();
+    return check_launch("ray_query");
+}

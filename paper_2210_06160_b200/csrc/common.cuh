@@ -1,0 +1,274 @@
+// common.cuh -- shared device helpers for librtsdf (sm_100a).
+//
+// Every fp64 expression that must be bit-identical to the reference is
+// compiled with --fmad=false (see _build.py) and written in the reference's
+// left-to-right order; comments cite the reference line each helper restates.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/rtsdf.h"
+
+#define RTSDF_EMPTY (-1)
+#define RTSDF_MAX_DIM 1024
+
+namespace rtsdf {
+
+// ---- error plumbing (api.cu) ------------------------------------------------
+void set_error(const char* fmt, ...);
+int check_launch(const char* what);
+void count_launch(int n = 1);
+
+inline int num_sms() {
+    static int sms = 0;
+    if (!sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (sms <= 0) sms = 148;
+    }
+    return sms;
+}
+
+// ---- packed seed coordinates --------------------------------------------------
+__host__ __device__ __forceinline__ int32_t pack_ijk(int i, int j, int k) {
+    return (i << 20) | (j << 10) | k;
+}
+__device__ __forceinline__ int unpack_i(int32_t p) { return (int)((uint32_t)p >> 20); }
+__device__ __forceinline__ int unpack_j(int32_t p) { return (p >> 10) & 1023; }
+__device__ __forceinline__ int unpack_k(int32_t p) { return p & 1023; }
+
+// jfa.py:72-76 _center_d2, fp64, left to right, no contraction
+__device__ __forceinline__ double center_d2(int di, int dj, int dk, double hx, double hy,
+                                            double hz) {
+    double dx = __dmul_rn((double)di, hx);
+    double dy = __dmul_rn((double)dj, hy);
+    double dz = __dmul_rn((double)dk, hz);
+    return __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
+}
+
+// ---- field.py:95-128 trilinear (f32 samples promoted to fp64) -------------------
+struct FieldView {
+    const float* data;
+    int nx, ny, nz;
+    double lox, loy, loz, hx, hy, hz;
+};
+
+__device__ __forceinline__ double dmin_(double a, double b) { return a < b ? a : b; }
+__device__ __forceinline__ double dmax_(double a, double b) { return a > b ? a : b; }
+
+__device__ __forceinline__ double trilinear(const FieldView& f, double px, double py,
+                                            double pz) {
+    double gx = __dsub_rn(__ddiv_rn(__dsub_rn(px, f.lox), f.hx), 0.5);
+    double gy = __dsub_rn(__ddiv_rn(__dsub_rn(py, f.loy), f.hy), 0.5);
+    double gz = __dsub_rn(__ddiv_rn(__dsub_rn(pz, f.loz), f.hz), 0.5);
+    gx = dmin_(dmax_(gx, 0.0), (double)f.nx - 1.0);
+    gy = dmin_(dmax_(gy, 0.0), (double)f.ny - 1.0);
+    gz = dmin_(dmax_(gz, 0.0), (double)f.nz - 1.0);
+    int ix = f.nx > 1 ? min((int)gx, f.nx - 2) : 0;
+    int iy = f.ny > 1 ? min((int)gy, f.ny - 2) : 0;
+    int iz = f.nz > 1 ? min((int)gz, f.nz - 2) : 0;
+    double fx = __dsub_rn(gx, (double)ix);
+    double fy = __dsub_rn(gy, (double)iy);
+    double fz = __dsub_rn(gz, (double)iz);
+    int jx = f.nx > 1 ? ix + 1 : ix;
+    int jy = f.ny > 1 ? iy + 1 : iy;
+    int jz = f.nz > 1 ? iz + 1 : iz;
+    const int64_t sx = (int64_t)f.ny * f.nz, sy = f.nz;
+    const float* d = f.data;
+    double c000 = __ldg(d + ix * sx + iy * sy + iz);
+    double c100 = __ldg(d + jx * sx + iy * sy + iz);
+    double c010 = __ldg(d + ix * sx + jy * sy + iz);
+    double c110 = __ldg(d + jx * sx + jy * sy + iz);
+    double c001 = __ldg(d + ix * sx + iy * sy + jz);
+    double c101 = __ldg(d + jx * sx + iy * sy + jz);
+    double c011 = __ldg(d + ix * sx + jy * sy + jz);
+    double c111 = __ldg(d + jx * sx + jy * sy + jz);
+    double ofx = __dsub_rn(1.0, fx), ofy = __dsub_rn(1.0, fy), ofz = __dsub_rn(1.0, fz);
+    double c00 = __dadd_rn(__dmul_rn(c000, ofx), __dmul_rn(c100, fx));
+    double c10 = __dadd_rn(__dmul_rn(c010, ofx), __dmul_rn(c110, fx));
+    double c01 = __dadd_rn(__dmul_rn(c001, ofx), __dmul_rn(c101, fx));
+    double c11 = __dadd_rn(__dmul_rn(c011, ofx), __dmul_rn(c111, fx));
+    double c0 = __dadd_rn(__dmul_rn(c00, ofy), __dmul_rn(c10, fy));
+    double c1 = __dadd_rn(__dmul_rn(c01, ofy), __dmul_rn(c11, fy));
+    return __dadd_rn(__dmul_rn(c0, ofz), __dmul_rn(c1, fz));
+}
+
+// ---- rng.py:18-53 counter-based SplitMix64 --------------------------------------
+#define RTSDF_GOLDEN 0x9E3779B97F4A7C15ull
+__host__ __device__ __forceinline__ uint64_t mix64(uint64_t x) {
+    uint64_t z = x + RTSDF_GOLDEN;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+__host__ __device__ __forceinline__ uint64_t stream_key(uint64_t seed, uint64_t stream,
+                                                        uint64_t tick) {
+    uint64_t k = mix64(seed ^ RTSDF_GOLDEN);
+    k = mix64(k ^ stream);
+    return mix64(k ^ tick);
+}
+__device__ __forceinline__ double uniform01(uint64_t key, uint64_t counter) {
+    uint64_t bits = mix64(key + counter * RTSDF_GOLDEN);
+    return __dmul_rn((double)(bits >> 11), 1.0 / 9007199254740992.0);
+}
+__device__ __forceinline__ void unit_sphere_dir(uint64_t key, uint64_t counter, double& dx,
+                                                double& dy, double& dz) {
+    double u = uniform01(key, 2 * counter);
+    double v = uniform01(key, 2 * counter + 1);
+    double z = __dsub_rn(1.0, __dmul_rn(2.0, u));
+    double r = __dsqrt_rn(dmax_(0.0, __dsub_rn(1.0, __dmul_rn(z, z))));
+    double phi = __dmul_rn(6.283185307179586, v);
+    double s, c;
+    sincos(phi, &s, &c);  // CUDA libdevice; may differ from glibc in the last ulp
+    dx = __dmul_rn(r, c);
+    dy = __dmul_rn(r, s);
+    dz = z;
+}
+
+// ---- packed BVH (geometry.py:177-195 re-laid out for the GPU) --------------------
+struct __align__(64) BvhNode {
+    double lo[3];
+    double hi[3];
+    int32_t left;   // internal: child index; leaf: -(start + 1)
+    int32_t right;  // internal: child index; leaf: count
+};
+struct __align__(128) BvhTri {
+    double a[3], e1[3], e2[3], n[3];
+    int32_t orig;
+    int32_t pad[7];
+};
+static_assert(sizeof(BvhNode) == 64, "node layout");
+static_assert(sizeof(BvhTri) == 128, "tri layout");
+
+struct BvhView {
+    const BvhNode* nodes;
+    const BvhTri* tris;
+};
+__host__ __device__ inline BvhView bvh_view(const void* packed, int64_t n_nodes) {
+    BvhView v;
+    v.nodes = (const BvhNode*)packed;
+    v.tris = (const BvhTri*)((const char*)packed + n_nodes * sizeof(BvhNode));
+    return v;
+}
+
+// geometry.py:281-299 _ray_box_entry
+__device__ __forceinline__ double ray_box_entry(const BvhNode* nd, double ox, double oy,
+                                                double oz, double ix, double iy, double iz,
+                                                double t_best) {
+    double2 l01 = __ldg((const double2*)&nd->lo[0]);
+    double2 l2h0 = __ldg((const double2*)&nd->lo[2]);
+    double2 h12 = __ldg((const double2*)&nd->hi[1]);
+    double t0 = __dmul_rn(__dsub_rn(l01.x, ox), ix), t1 = __dmul_rn(__dsub_rn(l2h0.y, ox), ix);
+    double tmin = dmin_(t0, t1), tmax = dmax_(t0, t1);
+    t0 = __dmul_rn(__dsub_rn(l01.y, oy), iy);
+    t1 = __dmul_rn(__dsub_rn(h12.x, oy), iy);
+    tmin = dmax_(tmin, dmin_(t0, t1));
+    tmax = dmin_(tmax, dmax_(t0, t1));
+    t0 = __dmul_rn(__dsub_rn(l2h0.x, oz), iz);
+    t1 = __dmul_rn(__dsub_rn(h12.y, oz), iz);
+    tmin = dmax_(tmin, dmin_(t0, t1));
+    tmax = dmin_(tmax, dmax_(t0, t1));
+    double entry = dmax_(tmin, 0.0);
+    if (tmax >= entry && tmin <= t_best) return entry;
+    return -1.0;
+}
+
+// geometry.py:302-328 _ray_tri (Moller-Trumbore, fp64)
+__device__ __forceinline__ double ray_tri(double ox, double oy, double oz, double dx, double dy,
+                                          double dz, const BvhTri* tr) {
+    const double* a = tr->a;
+    const double* e1 = tr->e1;
+    const double* e2 = tr->e2;
+    double e2x = __ldg(e2), e2y = __ldg(e2 + 1), e2z = __ldg(e2 + 2);
+    double e1x = __ldg(e1), e1y = __ldg(e1 + 1), e1z = __ldg(e1 + 2);
+    double px = __dsub_rn(__dmul_rn(dy, e2z), __dmul_rn(dz, e2y));
+    double py = __dsub_rn(__dmul_rn(dz, e2x), __dmul_rn(dx, e2z));
+    double pz = __dsub_rn(__dmul_rn(dx, e2y), __dmul_rn(dy, e2x));
+    double det = __dadd_rn(__dadd_rn(__dmul_rn(e1x, px), __dmul_rn(e1y, py)), __dmul_rn(e1z, pz));
+    if (-1e-14 < det && det < 1e-14) return -1.0;
+    double inv = __ddiv_rn(1.0, det);
+    double tx = __dsub_rn(ox, __ldg(a)), ty = __dsub_rn(oy, __ldg(a + 1)),
+           tz = __dsub_rn(oz, __ldg(a + 2));
+    double u = __dmul_rn(
+        __dadd_rn(__dadd_rn(__dmul_rn(tx, px), __dmul_rn(ty, py)), __dmul_rn(tz, pz)), inv);
+    if (u < 0.0 || u > 1.0) return -1.0;
+    double qx = __dsub_rn(__dmul_rn(ty, e1z), __dmul_rn(tz, e1y));
+    double qy = __dsub_rn(__dmul_rn(tz, e1x), __dmul_rn(tx, e1z));
+    double qz = __dsub_rn(__dmul_rn(tx, e1y), __dmul_rn(ty, e1x));
+    double v = __dmul_rn(
+        __dadd_rn(__dadd_rn(__dmul_rn(dx, qx), __dmul_rn(dy, qy)), __dmul_rn(dz, qz)), inv);
+    if (v < 0.0 || __dadd_rn(u, v) > 1.0) return -1.0;
+    double t = __dmul_rn(
+        __dadd_rn(__dadd_rn(__dmul_rn(e2x, qx), __dmul_rn(e2y, qy)), __dmul_rn(e2z, qz)), inv);
+    if (t < 1e-12) return -1.0;
+    return t;
+}
+
+// geometry.py:331-392 _bvh_ray: closest hit, ties -> smaller original id,
+// near child first (tl <= tr).  Returns t (or -1) with id/facing.
+#define RTSDF_STACK 64
+__device__ __forceinline__ double bvh_ray(const BvhView& b, double ox, double oy, double oz,
+                                          double dx, double dy, double dz, double t_max,
+                                          int32_t& out_id, int& out_facing) {
+    int32_t stack[RTSDF_STACK];
+    double ix = dx != 0.0 ? __ddiv_rn(1.0, dx) : (dx >= 0 ? 1e300 : -1e300);
+    double iy = dy != 0.0 ? __ddiv_rn(1.0, dy) : (dy >= 0 ? 1e300 : -1e300);
+    double iz = dz != 0.0 ? __ddiv_rn(1.0, dz) : (dz >= 0 ? 1e300 : -1e300);
+    double best_t = t_max;
+    int32_t best_id = -1;
+    int best_facing = 0;
+    out_id = -1;
+    out_facing = 0;
+    if (ray_box_entry(b.nodes, ox, oy, oz, ix, iy, iz, best_t) < 0.0) return -1.0;
+    stack[0] = 0;
+    int sp = 1;
+    while (sp > 0) {
+        int32_t node = stack[--sp];
+        int2 lr = __ldg((const int2*)&b.nodes[node].left);
+        if (lr.x < 0) {
+            int start = -lr.x - 1, count = lr.y;
+            for (int k = start; k < start + count; ++k) {
+                const BvhTri* tr = b.tris + k;
+                double t = ray_tri(ox, oy, oz, dx, dy, dz, tr);
+                if (t >= 0.0 && t <= best_t) {
+                    int32_t orig = __ldg(&tr->orig);
+                    if (t < best_t || best_id < 0 || orig < best_id) {
+                        best_t = t;
+                        best_id = orig;
+                        double dot = __dadd_rn(
+                            __dadd_rn(__dmul_rn(dx, __ldg(tr->n)), __dmul_rn(dy, __ldg(tr->n + 1))),
+                            __dmul_rn(dz, __ldg(tr->n + 2)));
+                        best_facing = dot < 0.0 ? 1 : 2;
+                    }
+                }
+            }
+        } else {
+            double tl = ray_box_entry(b.nodes + lr.x, ox, oy, oz, ix, iy, iz, best_t);
+            double tr = ray_box_entry(b.nodes + lr.y, ox, oy, oz, ix, iy, iz, best_t);
+            if (tl >= 0.0) {
+                if (tr >= 0.0) {
+                    if (tl <= tr) {
+                        stack[sp] = lr.y;
+                        stack[sp + 1] = lr.x;
+                    } else {
+                        stack[sp] = lr.x;
+                        stack[sp + 1] = lr.y;
+                    }
+                    sp += 2;
+                } else {
+                    stack[sp++] = lr.x;
+                }
+            } else if (tr >= 0.0) {
+                stack[sp++] = lr.y;
+            }
+            if (sp > RTSDF_STACK - 2) sp = RTSDF_STACK - 2;  // unreachable for depth < 62
+        }
+    }
+    if (best_id < 0) return -1.0;
+    out_id = best_id;
+    out_facing = best_facing;
+    return best_t;
+}
+
+}  // namespace rtsdf

@@ -1,0 +1,313 @@
+// jfa.cu -- K2 (JFA pass), jfa_init, K3 (seeds -> SDF) and seed format helpers.
+//
+// Restates jfa.py:47-181.  Seeds are packed int32 (i<<20 | j<<10 | k) so the
+// lexicographic tie rule (jfa.py:116-124) is a plain integer compare and the
+// decode is shifts/masks instead of the reference's two integer divisions.
+//
+// Exactness: the reference orders candidates by fp64 d2
+// evaluated as ((dx*hx)^2 + (dy*hy)^2) + (dz*hz)^2 and falls back to the
+// lexicographic rule only among fp64-EQUAL values.  When the host proves
+// hx^2 : hy^2 : hz^2 = wx : wy : wz exactly (rational arithmetic on the fp64
+// cell sizes), the true d2 is s*q with q = wx dx^2 + wy dy^2 + wz dz^2 an
+// integer, and fp64's <= 5 ulp relative error cannot reorder distinct q (the
+// relative gap is >= 1/q_max ~ 1e-7).  So the INT path orders by q and only
+// evaluates the reference's fp64 expression when q ties -- bit-exact, with
+// integer work on the common path.  (0,0,0) weights select the FP64 path.
+#include "common.cuh"
+
+namespace rtsdf {
+
+enum { JFA_INT = 0, JFA_FP64 = 1 };
+
+struct JfaGeom {
+    int nx, ny, nz;     // global grid
+    int x0, nxl;        // owned planes [x0, x0 + nxl)
+    int lo_first, n_lo; // halo planes below
+    int hi_first, n_hi; // halo planes above
+    int offset;
+    double hx, hy, hz;
+    int wx, wy, wz;
+};
+
+struct PlaneSrc {
+    const int32_t* local;
+    const int32_t* halo_lo;
+    const int32_t* halo_hi;
+};
+
+__device__ __forceinline__ const int32_t* plane_ptr(const PlaneSrc& s, const JfaGeom& g, int q,
+                                                    int64_t plane) {
+    if (q >= g.x0 && q < g.x0 + g.nxl) return s.local + (int64_t)(q - g.x0) * plane;
+    if (q >= g.lo_first && q < g.lo_first + g.n_lo) return s.halo_lo + (int64_t)(q - g.lo_first) * plane;
+    if (q >= g.hi_first && q < g.hi_first + g.n_hi) return s.halo_hi + (int64_t)(q - g.hi_first) * plane;
+    return nullptr;
+}
+
+template <int MODE>
+struct Best {
+    int32_t p;
+    int q;      // INT: weighted integer d2; unused for FP64
+    double d2;  // FP64: reference d2; INT: lazily evaluated on ties
+};
+
+// Consider candidate seed c for the cell (i, j, k); jfa.py:108-124.
+template <int MODE>
+__device__ __forceinline__ void consider(Best<MODE>& b, int32_t c, int i, int j, int k,
+                                         const JfaGeom& g) {
+    if (c == RTSDF_EMPTY || c == b.p) return;
+    int dx = i - unpack_i(c), dy = j - unpack_j(c), dz = k - unpack_k(c);
+    if (MODE == JFA_INT) {
+        int q = g.wx * dx * dx + g.wy * dy * dy + g.wz * dz * dz;
+        if (q < b.q) {
+            b.p = c;
+            b.q = q;
+        } else if (q == b.q && b.p != RTSDF_EMPTY) {
+            // integer tie: decide on the reference's fp64 values
+            double dc = center_d2(dx, dy, dz, g.hx, g.hy, g.hz);
+            double db = center_d2(i - unpack_i(b.p), j - unpack_j(b.p), k - unpack_k(b.p), g.hx,
+                                  g.hy, g.hz);
+            if (dc < db || (dc == db && c < b.p)) {
+                b.p = c;
+                b.q = q;
+            }
+        }
+    } else {
+        double d2 = center_d2(dx, dy, dz, g.hx, g.hy, g.hz);
+        if (d2 < b.d2 || (d2 == b.d2 && b.p != RTSDF_EMPTY && c < b.p)) {
+            b.p = c;
+            b.d2 = d2;
+        }
+    }
+}
+
+// One thread per cell; block = 32 (z) x 8 (y), grid.z walks the owned planes.
+template <int MODE, bool SLAB>
+__global__ void __launch_bounds__(256) jfa_step_kernel(PlaneSrc src, int32_t* __restrict__ dst,
+                                                       JfaGeom g) {
+    const int k = blockIdx.x * 32 + threadIdx.x;
+    const int j = blockIdx.y * 8 + threadIdx.y;
+    const int il = blockIdx.z;  // local plane
+    if (k >= g.nz || j >= g.ny) return;
+    const int i = g.x0 + il;
+    const int64_t plane = (int64_t)g.ny * g.nz;
+    const int off = g.offset;
+    Best<MODE> b;
+    b.p = __ldg(src.local + (int64_t)il * plane + (int64_t)j * g.nz + k);
+    if (b.p != RTSDF_EMPTY) {
+        int dx = i - unpack_i(b.p), dy = j - unpack_j(b.p), dz = k - unpack_k(b.p);
+        if (MODE == JFA_INT) b.q = g.wx * dx * dx + g.wy * dy * dy + g.wz * dz * dz;
+        else b.d2 = center_d2(dx, dy, dz, g.hx, g.hy, g.hz);
+    } else {
+        b.q = 0x7fffffff;
+        b.d2 = 1e300;
+    }
+#pragma unroll
+    for (int di = -1; di <= 1; ++di) {
+        const int qi = i + di * off;
+        if (qi < 0 || qi >= g.nx) continue;
+        const int32_t* pl = SLAB ? plane_ptr(src, g, qi, plane)
+                                 : src.local + (int64_t)qi * plane;
+#pragma unroll
+        for (int dj = -1; dj <= 1; ++dj) {
+            const int qj = j + dj * off;
+            if (qj < 0 || qj >= g.ny) continue;
+            const int32_t* row = pl + (int64_t)qj * g.nz;
+#pragma unroll
+            for (int dk = -1; dk <= 1; ++dk) {
+                if (di == 0 && dj == 0 && dk == 0) continue;
+                const int qk = k + dk * off;
+                if (qk < 0 || qk >= g.nz) continue;
+                consider<MODE>(b, __ldg(row + qk), i, j, k, g);
+            }
+        }
+    }
+    dst[(int64_t)il * plane + (int64_t)j * g.nz + k] = b.p;
+}
+
+__global__ void jfa_init_kernel(const uint8_t* __restrict__ occ, int ny, int nz, int64_t n,
+                                int32_t* __restrict__ seed, int64_t* __restrict__ count) {
+    int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    bool on = false;
+    if (c < n) {
+        on = occ[c] != 0;
+        int64_t nyz = (int64_t)ny * nz;
+        int i = (int)(c / nyz), j = (int)((c / nz) % ny), k = (int)(c % nz);
+        seed[c] = on ? pack_ijk(i, j, k) : RTSDF_EMPTY;
+    }
+    if (count) {
+        unsigned m = __ballot_sync(0xffffffffu, on);
+        if ((threadIdx.x & 31) == 0 && m) atomicAdd((unsigned long long*)count, (unsigned long long)__popc(m));
+    }
+}
+
+// jfa.py:148-160: f32(sqrt(d2_fp64) - beta)
+__global__ void seeds_to_sdf_kernel(const int32_t* __restrict__ seed, float* __restrict__ out,
+                                    int nx, int ny, int nz, double hx, double hy, double hz,
+                                    double beta, int64_t* __restrict__ empty_count) {
+    const int k = blockIdx.x * 32 + threadIdx.x;
+    const int j = blockIdx.y * 8 + threadIdx.y;
+    const int i = blockIdx.z;
+    bool empty = false;
+    if (k < nz && j < ny) {
+        int64_t c = ((int64_t)i * ny + j) * nz + k;
+        int32_t s = __ldg(seed + c);
+        empty = s == RTSDF_EMPTY;
+        double d2 = center_d2(i - unpack_i(s), j - unpack_j(s), k - unpack_k(s), hx, hy, hz);
+        out[c] = (float)__dsub_rn(__dsqrt_rn(d2), beta);
+    }
+    if (empty_count) {
+        unsigned m = __ballot_sync(0xffffffffu, empty);
+        if (((threadIdx.y * 32 + threadIdx.x) & 31) == 0 && m)
+            atomicAdd((unsigned long long*)empty_count, (unsigned long long)__popc(m));
+    }
+}
+
+__global__ void packed_to_linear_kernel(const int32_t* __restrict__ p, int32_t* __restrict__ l,
+                                        int ny, int nz, int64_t n) {
+    int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (c >= n) return;
+    int32_t s = p[c];
+    l[c] = s == RTSDF_EMPTY ? RTSDF_EMPTY
+                            : (int32_t)(((int64_t)unpack_i(s) * ny + unpack_j(s)) * nz + unpack_k(s));
+}
+
+__global__ void linear_to_packed_kernel(const int32_t* __restrict__ l, int32_t* __restrict__ p,
+                                        int ny, int nz, int64_t n) {
+    int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (c >= n) return;
+    int32_t s = l[c];
+    if (s == RTSDF_EMPTY) {
+        p[c] = RTSDF_EMPTY;
+        return;
+    }
+    int64_t nyz = (int64_t)ny * nz;
+    p[c] = pack_ijk((int)(s / nyz), (int)((s / nz) % ny), (int)(s % nz));
+}
+
+static bool dims_ok(int nx, int ny, int nz) {
+    if (nx < 1 || ny < 1 || nz < 1 || nx > RTSDF_MAX_DIM || ny > RTSDF_MAX_DIM || nz > RTSDF_MAX_DIM) {
+        set_error("dims (%d, %d, %d) outside 1..%d (packed 10:10:10 seeds)", nx, ny, nz, RTSDF_MAX_DIM);
+        return false;
+    }
+    return true;
+}
+
+static int launch_step(PlaneSrc s, int32_t* dst, const JfaGeom& g, bool slab, cudaStream_t st) {
+    dim3 block(32, 8, 1);
+    dim3 grid((g.nz + 31) / 32, (g.ny + 7) / 8, g.nxl);
+    bool int_mode = g.wx > 0 && g.wy > 0 && g.wz > 0;
+    if (int_mode) {
+        if (slab) jfa_step_kernel<JFA_INT, true><<<grid, block, 0, st>>>(s, dst, g);
+        else jfa_step_kernel<JFA_INT, false><<<grid, block, 0, st>>>(s, dst, g);
+    } else {
+        if (slab) jfa_step_kernel<JFA_FP64, true><<<grid, block, 0, st>>>(s, dst, g);
+        else jfa_step_kernel<JFA_FP64, false><<<grid, block, 0, st>>>(s, dst, g);
+    }
+    count_launch();
+    return check_launch("jfa_step");
+}
+
+static bool weights_ok(int nx, int ny, int nz, int wx, int wy, int wz) {
+    if (wx == 0 && wy == 0 && wz == 0) return true;
+    if (wx <= 0 || wy <= 0 || wz <= 0) return false;
+    double qmax = (double)wx * (nx - 1) * (nx - 1) + (double)wy * (ny - 1) * (ny - 1) +
+                  (double)wz * (nz - 1) * (nz - 1);
+    return qmax < 2147483647.0;
+}
+
+}  // namespace rtsdf
+
+using namespace rtsdf;
+
+extern "C" int rtsdf_jfa_init(const uint8_t* occ, int nx, int ny, int nz, int32_t* seed,
+                              int64_t* count, void* stream) {
+    if (!dims_ok(nx, ny, nz)) return RTSDF_ERR_DIMS;
+    int64_t n = (int64_t)nx * ny * nz;
+    jfa_init_kernel<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(occ, ny, nz, n,
+                                                                                  seed, count);
+    count_launch();
+    return check_launch("jfa_init");
+}
+
+extern "C" int rtsdf_jfa_step(const int32_t* src, int32_t* dst, int nx, int ny, int nz,
+                              int offset, double hx, double hy, double hz, int wx, int wy,
+                              int wz, void* stream) {
+    if (!dims_ok(nx, ny, nz)) return RTSDF_ERR_DIMS;
+    if (offset < 1 || !weights_ok(nx, ny, nz, wx, wy, wz)) {
+        set_error("jfa_step: bad offset %d or weights (%d,%d,%d)", offset, wx, wy, wz);
+        return RTSDF_ERR_INVALID;
+    }
+    JfaGeom g{nx, ny, nz, 0, nx, 0, 0, 0, 0, offset, hx, hy, hz, wx, wy, wz};
+    PlaneSrc s{src, nullptr, nullptr};
+    return launch_step(s, dst, g, false, (cudaStream_t)stream);
+}
+
+extern "C" int rtsdf_jfa_step_slab(const int32_t* local, const int32_t* halo_lo,
+                                   const int32_t* halo_hi, int32_t* dst, int nx, int x0, int nxl,
+                                   int lo_first, int n_lo, int hi_first, int n_hi, int ny, int nz,
+                                   int offset, double hx, double hy, double hz, int wx, int wy,
+                                   int wz, void* stream) {
+    if (!dims_ok(nx, ny, nz)) return RTSDF_ERR_DIMS;
+    if (offset < 1 || nxl < 1 || x0 < 0 || x0 + nxl > nx || !weights_ok(nx, ny, nz, wx, wy, wz)) {
+        set_error("jfa_step_slab: bad slab/offset/weights");
+        return RTSDF_ERR_INVALID;
+    }
+    JfaGeom g{nx, ny, nz, x0, nxl, lo_first, n_lo, hi_first, n_hi, offset, hx, hy, hz, wx, wy, wz};
+    PlaneSrc s{local, halo_lo, halo_hi};
+    return launch_step(s, dst, g, true, (cudaStream_t)stream);
+}
+
+extern "C" int rtsdf_jfa_run(int32_t* a, int32_t* b, int nx, int ny, int nz, double hx,
+                             double hy, double hz, int wx, int wy, int wz, int* which,
+                             void* stream) {
+    if (!dims_ok(nx, ny, nz)) return RTSDF_ERR_DIMS;
+    int m = nx > ny ? nx : ny;
+    if (nz > m) m = nz;
+    int n = 1;
+    while (n < m) n *= 2;  // jfa.py:58-68
+    int32_t* src = a;
+    int32_t* dst = b;
+    int w = 0;
+    for (int off = n / 2; off >= 1; off /= 2) {
+        int rc = rtsdf_jfa_step(src, dst, nx, ny, nz, off, hx, hy, hz, wx, wy, wz, stream);
+        if (rc) return rc;
+        int32_t* t = src;
+        src = dst;
+        dst = t;
+        w ^= 1;
+    }
+    if (which) *which = w;
+    return RTSDF_OK;
+}
+
+extern "C" int rtsdf_seeds_to_sdf(const int32_t* seed, float* out, int nx, int ny, int nz,
+                                  double hx, double hy, double hz, double beta,
+                                  int64_t* empty_count, void* stream) {
+    if (!dims_ok(nx, ny, nz)) return RTSDF_ERR_DIMS;
+    dim3 block(32, 8, 1);
+    dim3 grid((nz + 31) / 32, (ny + 7) / 8, nx);
+    seeds_to_sdf_kernel<<<grid, block, 0, (cudaStream_t)stream>>>(seed, out, nx, ny, nz, hx, hy,
+                                                                  hz, beta, empty_count);
+    count_launch();
+    return check_launch("seeds_to_sdf");
+}
+
+extern "C" int rtsdf_seeds_packed_to_linear(const int32_t* p, int32_t* l, int nx, int ny, int nz,
+                                            void* stream) {
+    if (!dims_ok(nx, ny, nz)) return RTSDF_ERR_DIMS;
+    int64_t n = (int64_t)nx * ny * nz;
+    packed_to_linear_kernel<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(p, l, ny,
+                                                                                          nz, n);
+    count_launch();
+    return check_launch("seeds_packed_to_linear");
+}
+
+extern "C" int rtsdf_seeds_linear_to_packed(const int32_t* l, int32_t* p, int nx, int ny, int nz,
+                                            void* stream) {
+    if (!dims_ok(nx, ny, nz)) return RTSDF_ERR_DIMS;
+    int64_t n = (int64_t)nx * ny * nz;
+    linear_to_packed_kernel<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(l, p, ny,
+                                                                                          nz, n);
+    count_launch();
+    return check_launch("seeds_linear_to_packed");
+}

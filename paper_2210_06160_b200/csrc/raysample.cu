@@ -1,0 +1,183 @@
+// raysample.cu -- K6 + K7: ray-sampled refinement fused with the Eq. 1
+// combine/sign update.
+//
+// Restates raysample.py:132-176 (_sample_rays / _sample_masked_kernel),
+// rng.py:30-53 and raysample.py:215-244 (_update_masked_kernel).  Mapping:
+// a warp owns floor(32 / x) masked texels (or one texel in ceil(x / 32)
+// rounds when x > 32); each lane traces one ray of its texel through the
+// reference's own BVH in fp64; a segmented warp reduction produces
+// (min t, front, back) for each texel and the texel's first lane applies the
+// band reset + Eq. 1 + sign and writes the fine value.  Every texel is owned
+// by exactly one lane for the update, so no atomics are used anywhere and
+// the result is independent of scheduling.
+#include "common.cuh"
+
+namespace rtsdf {
+
+struct SampleParams {
+    BvhView bvh;
+    const int64_t* idx;
+    const int64_t* count;
+    int64_t m_cap;
+    FieldView coarse;
+    int fnx, fny, fnz;
+    double fhx, fhy, fhz;
+    int x;
+    uint64_t seed;
+    int64_t frame;
+    double t_max;
+    const double* dirs;
+    double* samp_min;
+    int32_t* samp_front;
+    int32_t* samp_back;
+    const float* prev;
+    const uint8_t* mask_old;
+    float* run_min;
+    int32_t* front;
+    int32_t* back;
+    double alpha;
+    float* out;
+};
+
+__global__ void __launch_bounds__(128) sample_update_kernel(SampleParams P) {
+    const int lane = threadIdx.x & 31;
+    const int64_t M = min(*P.count, P.m_cap);
+    const int x = P.x;
+    const int tpw = x >= 32 || x == 0 ? 1 : 32 / x;  // texels per warp
+    const int seg = x >= 32 || x == 0 ? 32 : x;      // lanes per texel
+    const int rounds = x > 32 ? (x + 31) / 32 : 1;
+    const int my_t = lane / seg, pos = lane - my_t * seg;
+    const int64_t nyz = (int64_t)P.fny * P.fnz;
+    const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+    for (int64_t wbase = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; wbase * tpw < M;
+         wbase += warps) {
+        const int64_t n = wbase * tpw + my_t;
+        const bool active = my_t < tpw && n < M;
+        int64_t lin = active ? __ldg(P.idx + n) : 0;
+        int i = (int)(lin / nyz), j = (int)((lin / P.fnz) % P.fny), k = (int)(lin % P.fnz);
+        // raysample.py:167-169: texel centre from the coarse lo (same box)
+        double px = P.coarse.lox + ((double)i + 0.5) * P.fhx;
+        double py = P.coarse.loy + ((double)j + 0.5) * P.fhy;
+        double pz = P.coarse.loz + ((double)k + 0.5) * P.fhz;
+        uint64_t key = stream_key(P.seed, (uint64_t)lin, (uint64_t)P.frame);
+        double best = __longlong_as_double(0x7ff0000000000000ll);  // +inf
+        int fr = 0, bk = 0;
+        for (int rd = 0; rd < rounds; ++rd) {
+            int r = rd * 32 + pos;
+            if (active && x > 0 && r < x && pos < seg) {
+                double dx, dy, dz;
+                if (P.dirs) {
+                    const double* d = P.dirs + 3 * (n * x + r);
+                    dx = d[0];
+                    dy = d[1];
+                    dz = d[2];
+                } else {
+                    unit_sphere_dir(key, (uint64_t)r, dx, dy, dz);
+                }
+                int32_t id;
+                int facing;
+                double t = bvh_ray(P.bvh, px, py, pz, dx, dy, dz, P.t_max, id, facing);
+                if (id >= 0) {
+                    if (t < best) best = t;
+                    if (facing == 1) fr++;
+                    else bk++;
+                }
+            }
+        }
+        // segmented tree reduction: position p combines p + o inside its texel
+        for (int o = 16; o; o >>= 1) {
+            double ob = __shfl_down_sync(0xffffffffu, best, o);
+            int of = __shfl_down_sync(0xffffffffu, fr, o);
+            int obk = __shfl_down_sync(0xffffffffu, bk, o);
+            if (pos + o < seg && lane + o < 32) {
+                best = ob < best ? ob : best;
+                fr += of;
+                bk += obk;
+            }
+        }
+        if (!active || pos != 0) continue;
+        if (P.samp_min) P.samp_min[n] = best;
+        if (P.samp_front) P.samp_front[n] = fr;
+        if (P.samp_back) P.samp_back[n] = bk;
+        if (!P.prev) continue;
+        // raysample.py:229-244
+        float rm = P.run_min[lin];
+        int32_t f = P.front[lin], b = P.back[lin];
+        if (!P.mask_old[lin]) {
+            rm = __int_as_float(0x7f800000);
+            f = 0;
+            b = 0;
+        }
+        double m = best;
+        if (m < (double)rm) rm = (float)m;
+        f += fr;
+        b += bk;
+        P.run_min[lin] = rm;
+        P.front[lin] = f;
+        P.back[lin] = b;
+        double c = (double)(float)trilinear(P.coarse, px, py, pz);  // c_fine[i, j, k] (f32)
+        double blend = P.alpha * fabs((double)P.prev[lin]) + (1.0 - P.alpha) * c;
+        double mag = blend < m ? blend : m;
+        P.out[lin] = b > f ? (float)(-mag) : (float)mag;
+    }
+}
+
+}  // namespace rtsdf
+
+using namespace rtsdf;
+
+extern "C" int rtsdf_sample_update(const void* bvh_packed, int64_t n_nodes, const int64_t* idx,
+                                   const int64_t* count, int64_t m_cap,
+                                   const rtsdf_resample_desc* rs, int x, uint64_t seed,
+                                   int64_t frame, double t_max, const double* dirs,
+                                   double* samp_min, int32_t* samp_front, int32_t* samp_back,
+                                   const float* prev, const uint8_t* mask_old, float* run_min,
+                                   int32_t* front, int32_t* back, double alpha, float* out,
+                                   void* stream) {
+    if (x < 0 || !rs || !count || !idx) {
+        set_error("sample_update: bad arguments");
+        return RTSDF_ERR_INVALID;
+    }
+    if (prev && (!mask_old || !run_min || !front || !back || !out)) {
+        set_error("sample_update: update needs mask_old/run_min/front/back/out");
+        return RTSDF_ERR_INVALID;
+    }
+    if (m_cap <= 0) return RTSDF_OK;
+    SampleParams P;
+    P.bvh = bvh_view(bvh_packed, n_nodes);
+    P.idx = idx;
+    P.count = count;
+    P.m_cap = m_cap;
+    P.coarse = FieldView{rs->coarse, rs->cnx, rs->cny, rs->cnz, rs->clo[0], rs->clo[1],
+                         rs->clo[2], rs->ch[0], rs->ch[1], rs->ch[2]};
+    P.fnx = rs->fnx;
+    P.fny = rs->fny;
+    P.fnz = rs->fnz;
+    P.fhx = rs->fh[0];
+    P.fhy = rs->fh[1];
+    P.fhz = rs->fh[2];
+    P.x = x;
+    P.seed = seed;
+    P.frame = frame;
+    P.t_max = t_max;
+    P.dirs = dirs;
+    P.samp_min = samp_min;
+    P.samp_front = samp_front;
+    P.samp_back = samp_back;
+    P.prev = prev;
+    P.mask_old = mask_old;
+    P.run_min = run_min;
+    P.front = front;
+    P.back = back;
+    P.alpha = alpha;
+    P.out = out;
+    int tpw = x >= 32 || x == 0 ? 1 : 32 / x;
+    int64_t warps_needed = (m_cap + tpw - 1) / tpw;
+    int64_t blocks = (warps_needed + 3) / 4;
+    int64_t cap = (int64_t)num_sms() * 16;
+    if (blocks > cap) blocks = cap;
+    if (blocks < 1) blocks = 1;
+    sample_update_kernel<<<(unsigned)blocks, 128, 0, (cudaStream_t)stream>>>(P);
+    count_launch();
+    return check_launch("sample_update");
+}

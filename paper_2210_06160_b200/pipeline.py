@@ -1,0 +1,242 @@
+"""Per-frame hybrid SDF pipeline: voxelize -> jump flood -> ray refine -> deferred light.
+
+Mirrors sdfshadow.pipeline (pipeline.py:1-165): FramePipeline owns the
+temporal state (previous fine field + accumulator) and re-runs the coarse
+passes every frame.  B200 form: every buffer is allocated once and stays in
+HBM; a frame is a fixed sequence of ~12 kernel launches on one stream (no host
+sync unless timing is requested), with the JFA seeds emitted directly by the
+voxelizer and the fine field updated in place.  Pass durations come from CUDA
+events, not the host clock.
+
+`hybrid_sdf(scene, config, frames)` is the north-star entry point.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field as dc_field
+
+import numpy as np
+import torch
+
+from . import jfa as _jfa
+from . import raysample as _rs
+from . import render as _render
+from . import voxel as _voxel
+from ._device import device
+from .field import DistanceField, apply_bias, make_field
+from .raymarch import MarchParams
+from .raysample import AccumulatorField, SamplingParams
+from .scenes import Scene
+
+PASSES = ("V", "JF", "RT", "DL")
+
+
+@dataclass(frozen=True)
+class PipelineConfig:
+    coarse_dims: tuple = (128, 128, 128)
+    fine_dims: tuple = (256, 256, 256)
+    sampling: SamplingParams = dc_field(default_factory=SamplingParams)
+    beta: float = 0.0
+    bias: float = 0.01
+    max_step: float = 0.05
+    max_iterations: int = 256
+    jitter: float = 1.0
+    shade_draws: int = 1
+    repeats: int = 1
+
+    def __post_init__(self):
+        for f, c in zip(self.fine_dims, self.coarse_dims):
+            if f % c != 0:
+                raise ValueError(
+                    f"fine dims {self.fine_dims} must be multiples of coarse dims {self.coarse_dims}")
+
+
+class FrameRecord:
+    """frame, durations_ns (pass -> int), masked_texels, rays_traced (pipeline.py:49-58).
+
+    Device-side values are resolved lazily so advance() never has to sync.
+    """
+
+    def __init__(self, frame, durations, masked_dev, rays_per_texel, events=None):
+        self.frame = frame
+        self._durations = durations
+        self._events = events
+        self._masked_dev = masked_dev
+        self._rays = rays_per_texel
+
+    @property
+    def durations_ns(self) -> dict:
+        if self._events is not None:
+            ev = self._events
+            ev[-1].synchronize()
+            for i, name in enumerate(PASSES):
+                a, b = ev[i], ev[i + 1]
+                self._durations[name] = int(round(a.elapsed_time(b) * 1e6))
+            self._events = None
+        return self._durations
+
+    @property
+    def masked_texels(self) -> int:
+        if not isinstance(self._masked_dev, int):
+            self._masked_dev = int(self._masked_dev.item())
+        return self._masked_dev
+
+    @property
+    def rays_traced(self) -> int:
+        return self.masked_texels * self._rays
+
+    @property
+    def total_ns(self):
+        return sum(self.durations_ns.values())
+
+
+class FramePipeline:
+    def __init__(self, scene: Scene, config: PipelineConfig):
+        self.scene = scene
+        self.cfg = config
+        self.frame = 0
+        self.coarse: DistanceField | None = None
+        self.fine: DistanceField | None = None
+        self.accum: AccumulatorField | None = None
+        self.records: list[FrameRecord] = []
+        self.last_image = None
+        self.last_occlusion = None
+        self._bufs = None
+        self._checked_view = None
+        self.directions = None  # optional host direction table for the next frame (parity)
+
+    # ------------------------------------------------------------- buffers
+    def _buffers(self):
+        if self._bufs is None:
+            cfg = self.cfg
+            dev = device()
+            cd = tuple(int(n) for n in cfg.coarse_dims)
+            fd = tuple(int(n) for n in cfg.fine_dims)
+            nf = int(np.prod(fd))
+            self._bufs = dict(
+                seed_a=torch.empty(cd, dtype=torch.int32, device=dev),
+                seed_b=torch.empty(cd, dtype=torch.int32, device=dev),
+                coarse=torch.empty(cd, dtype=torch.float32, device=dev),
+                mask_a=torch.zeros(fd, dtype=torch.bool, device=dev),
+                mask_b=torch.zeros(fd, dtype=torch.bool, device=dev),
+                compact=_rs.CompactBuffers(nf, dev),
+                masked=torch.zeros(1, dtype=torch.int64, device=dev),
+            )
+        return self._bufs
+
+    def march_params(self, **kw) -> MarchParams:
+        fine = self.fine if self.fine is not None else self._fine_placeholder()
+        kw.setdefault("max_step", self.cfg.max_step)
+        kw.setdefault("max_iterations", self.cfg.max_iterations)
+        kw.setdefault("jitter", self.cfg.jitter)
+        kw.setdefault("light_angle", self.scene.light.angular_radius)
+        return MarchParams.for_field(fine, **kw)
+
+    def _fine_placeholder(self):
+        return make_field(np.zeros((2, 2, 2), np.float32) + 1.0, self.scene.lo, self.scene.hi)
+
+    @property
+    def fine_for_shading(self) -> DistanceField:
+        if self.fine is None:
+            raise RuntimeError("advance() at least one frame first")
+        return apply_bias(self.fine, self.cfg.bias)
+
+    @property
+    def coarse_for_shading(self) -> DistanceField:
+        if self.coarse is None:
+            raise RuntimeError("advance() at least one frame first")
+        return apply_bias(self.coarse, self.cfg.bias)
+
+    # --------------------------------------------------------------- frame
+    def advance(self, render=False, camera=None, timing=True) -> FrameRecord:
+        """Run one frame of V -> JF -> RT (-> DL when render=True)."""
+        cfg = self.cfg
+        frame = self.frame
+        view = self.scene.view(frame)
+        b = self._buffers()
+        lo, hi = self.scene.lo, self.scene.hi
+        events = None
+        if timing:
+            events = [torch.cuda.Event(enable_timing=True) for _ in range(len(PASSES) + 1)]
+            events[0].record()
+
+        # V: packed self-seeds straight from the triangles (K1)
+        first = self._checked_view is not view
+        vox = _voxel.voxelize_seeds(view.mesh, cfg.coarse_dims, (lo, hi), check=first,
+                                    buffers=view.mesh_buffers(), out=b["seed_a"])
+        if first:
+            if not vox.any_occupied():
+                raise _jfa.NoSeedsError("voxel grid has no occupied cells")
+            self._checked_view = view
+        if timing:
+            events[1].record()
+
+        # JF: full schedule (K2) + seeds -> SDF (K3)
+        h = vox.cell_size
+        seeds = _jfa.flood_inplace(b["seed_a"], b["seed_b"], h)
+        _jfa.launch_seeds_to_sdf(seeds, b["coarse"], h, cfg.beta)
+        self.coarse = DistanceField(b["coarse"], np.asarray(lo, np.float64), np.asarray(hi, np.float64),
+                                    beta=cfg.beta)
+        if self.fine is None:
+            self.fine = _rs.fine_from_coarse(self.coarse, cfg.fine_dims)
+            self.accum = AccumulatorField.empty(cfg.fine_dims)
+            self.accum.mask = b["mask_a"]
+        if timing:
+            events[2].record()
+
+        # RT: resample + mask + band reset (K4), compaction, fused sample + Eq. 1 (K6/K7)
+        g = _rs._RsGeom(self.coarse, tuple(cfg.fine_dims))
+        mask_new = b["mask_b"] if self.accum.mask is b["mask_a"] else b["mask_a"]
+        cb = b["compact"]
+        _rs.launch_resample(g, cfg.sampling.mask_distance, out_unmasked=self.fine.data,
+                            mask_new=mask_new, block_counts=cb.block_counts, accum=self.accum)
+        _rs.launch_compact(mask_new, cb)
+        t_max = cfg.sampling.t_max
+        if t_max is None:
+            t_max = float(np.linalg.norm(self.coarse.hi - self.coarse.lo))
+        dirs = None
+        if self.directions is not None:
+            dirs = self.directions
+            self.directions = None
+        _rs.launch_sample_update(view.bvh, g, cb, cfg.sampling, frame, t_max, dirs=dirs,
+                                 prev=self.fine.data, accum=self.accum, out=self.fine.data)
+        self.accum.mask = mask_new
+        self.accum.frames_seen += 1
+        self.fine = DistanceField(self.fine.data, self.coarse.lo, self.coarse.hi,
+                                  beta=self.coarse.beta, bias=self.fine.bias, frame=frame)
+        masked = cb.count.clone()
+        if timing:
+            events[3].record()
+
+        self.last_image = None
+        if render:
+            cam = camera or self.scene.camera
+            gb = _render.rasterize_gbuffer(view, cam)
+            occ = _render.occlusion_image(gb, self.fine_for_shading, self.scene.light,
+                                          self.march_params(), draws=cfg.shade_draws,
+                                          seed=cfg.sampling.seed)
+            self.last_occlusion = occ
+            self.last_image = _render.compose(gb, occ, self.scene.light)
+        if timing:
+            events[4].record()
+
+        rec = FrameRecord(frame, {p: 0 for p in PASSES}, masked, cfg.sampling.rays_per_frame,
+                          events)
+        self.records.append(rec)
+        self.frame += 1
+        return rec
+
+    def run(self, frames: int, render_last=False, camera=None):
+        for i in range(frames):
+            self.advance(render=render_last and i == frames - 1, camera=camera)
+        return self.records
+
+
+def hybrid_sdf(scene: Scene, config: PipelineConfig, frames: int = 1, render_last=False):
+    """North-star entry point: run `frames` hybrid-SDF frames, return the pipeline."""
+    pipe = FramePipeline(scene, config)
+    pipe.run(frames, render_last=render_last)
+    return pipe
+
+
+__all__ = ["PASSES", "PipelineConfig", "FrameRecord", "FramePipeline", "hybrid_sdf"]
