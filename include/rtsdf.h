@@ -177,13 +177,15 @@ int rtsdf_sample_update(const void* bvh_packed, int64_t n_nodes, const int64_t* 
 
 /* ------------------------------------------------------------- soft shadow */
 /* Replaces render.py:167 (_occlusion_kernel): per covered pixel fp64 sphere
- * trace with the triangulated cone term (raymarch.py:83-147).               */
+ * trace with the triangulated cone term (raymarch.py:83-147).  sample_bias:
+ * apply_bias (field.py:155-161) fused into every trilinear sample as an f32
+ * subtraction, so shading needs no biased copy of the field (0 = none).     */
 int rtsdf_occlusion(const float* field, int nx, int ny, int nz, const double* lo /*host[3]*/,
                     const double* h /*host[3]*/, const double* g_pos, const double* g_nrm,
                     const uint8_t* g_cov, int height, int width, const double* light /*host[3]*/,
                     double eps, int max_iter, double max_step, double t_max, double k,
-                    double jitter, double offset, int draws, uint64_t seed, double* out,
-                    void* stream);
+                    double jitter, double offset, int draws, uint64_t seed, float sample_bias,
+                    double* out, void* stream);
 /* Replaces raymarch.py:128 (_march from sphere_trace) for a batch.          */
 int rtsdf_sphere_trace(const float* field, int nx, int ny, int nz, const double* lo,
                        const double* h, const double* origins, const double* dirs, int64_t n,

@@ -58,7 +58,7 @@ SIGNATURES = {
     "rtsdf_sample_update": (I, [P, I64, P, P, I64, C.POINTER(ResampleDesc), I, U64, I64, D, P,
                                 P, P, P, P, P, P, P, P, D, P, P]),
     "rtsdf_occlusion": (I, [P, I, I, I, DP, DP, P, P, P, I, I, DP, D, I, D, D, D, D, D, I, U64,
-                            P, P]),
+                            F, P, P]),
     "rtsdf_sphere_trace": (I, [P, I, I, I, DP, DP, P, P, I64, D, I, D, D, P, D, P, P, P, P, P]),
     "rtsdf_trilinear_many": (I, [P, I, I, I, DP, DP, P, I64, P, P]),
     "rtsdf_gbuffer": (I, [P, I64, P, P, DP, D, D, I, I, P, P, P, P, P]),

@@ -52,6 +52,7 @@ struct FieldView {
     const float* data;
     int nx, ny, nz;
     double lox, loy, loz, hx, hy, hz;
+    float bias;  // subtracted from every sample in f32 (field.py:161 fused); 0 = none
 };
 
 __device__ __forceinline__ double dmin_(double a, double b) { return a < b ? a : b; }
@@ -76,14 +77,15 @@ __device__ __forceinline__ double trilinear(const FieldView& f, double px, doubl
     int jz = f.nz > 1 ? iz + 1 : iz;
     const int64_t sx = (int64_t)f.ny * f.nz, sy = f.nz;
     const float* d = f.data;
-    double c000 = __ldg(d + ix * sx + iy * sy + iz);
-    double c100 = __ldg(d + jx * sx + iy * sy + iz);
-    double c010 = __ldg(d + ix * sx + jy * sy + iz);
-    double c110 = __ldg(d + jx * sx + jy * sy + iz);
-    double c001 = __ldg(d + ix * sx + iy * sy + jz);
-    double c101 = __ldg(d + jx * sx + iy * sy + jz);
-    double c011 = __ldg(d + ix * sx + jy * sy + jz);
-    double c111 = __ldg(d + jx * sx + jy * sy + jz);
+    const float b = f.bias;
+    double c000 = __fsub_rn(__ldg(d + ix * sx + iy * sy + iz), b);
+    double c100 = __fsub_rn(__ldg(d + jx * sx + iy * sy + iz), b);
+    double c010 = __fsub_rn(__ldg(d + ix * sx + jy * sy + iz), b);
+    double c110 = __fsub_rn(__ldg(d + jx * sx + jy * sy + iz), b);
+    double c001 = __fsub_rn(__ldg(d + ix * sx + iy * sy + jz), b);
+    double c101 = __fsub_rn(__ldg(d + jx * sx + iy * sy + jz), b);
+    double c011 = __fsub_rn(__ldg(d + ix * sx + jy * sy + jz), b);
+    double c111 = __fsub_rn(__ldg(d + jx * sx + jy * sy + jz), b);
     double ofx = __dsub_rn(1.0, fx), ofy = __dsub_rn(1.0, fy), ofz = __dsub_rn(1.0, fz);
     double c00 = __dadd_rn(__dmul_rn(c000, ofx), __dmul_rn(c100, fx));
     double c10 = __dadd_rn(__dmul_rn(c010, ofx), __dmul_rn(c110, fx));

@@ -176,8 +176,8 @@ __global__ void apply_bias_kernel(const float* __restrict__ in, int64_t n, float
 }
 
 static inline FieldView fview(const float* field, int nx, int ny, int nz, const double* lo,
-                              const double* h) {
-    return FieldView{field, nx, ny, nz, lo[0], lo[1], lo[2], h[0], h[1], h[2]};
+                              const double* h, float bias = 0.0f) {
+    return FieldView{field, nx, ny, nz, lo[0], lo[1], lo[2], h[0], h[1], h[2], bias};
 }
 
 }  // namespace rtsdf
@@ -189,7 +189,7 @@ extern "C" int rtsdf_occlusion(const float* field, int nx, int ny, int nz, const
                                const uint8_t* g_cov, int height, int width, const double* light,
                                double eps, int max_iter, double max_step, double t_max, double k,
                                double jitter, double offset, int draws, uint64_t seed,
-                               double* out, void* stream) {
+                               float sample_bias, double* out, void* stream) {
     if (draws < 1 || max_iter < 1) {
         set_error("occlusion: draws and max_iter must be >= 1");
         return RTSDF_ERR_INVALID;
@@ -198,7 +198,7 @@ extern "C" int rtsdf_occlusion(const float* field, int nx, int ny, int nz, const
     if (n <= 0) return RTSDF_OK;
     MarchArgs a{eps, max_iter, max_step, t_max, k};
     occlusion_kernel<<<(unsigned)((n + 127) / 128), 128, 0, (cudaStream_t)stream>>>(
-        fview(field, nx, ny, nz, lo, h), g_pos, g_nrm, g_cov, height, width, light[0], light[1],
+        fview(field, nx, ny, nz, lo, h, sample_bias), g_pos, g_nrm, g_cov, height, width, light[0], light[1],
         light[2], a, jitter, offset, draws, seed, out);
     count_launch();
     return check_launch("occlusion");

@@ -149,7 +149,7 @@ extern "C" int rtsdf_sample_update(const void* bvh_packed, int64_t n_nodes, cons
     P.count = count;
     P.m_cap = m_cap;
     P.coarse = FieldView{rs->coarse, rs->cnx, rs->cny, rs->cnz, rs->clo[0], rs->clo[1],
-                         rs->clo[2], rs->ch[0], rs->ch[1], rs->ch[2]};
+                         rs->clo[2], rs->ch[0], rs->ch[1], rs->ch[2], 0.0f};
     P.fnx = rs->fnx;
     P.fny = rs->fny;
     P.fnz = rs->fnz;

@@ -167,7 +167,7 @@ extern "C" int rtsdf_resample_mask(const float* coarse, int cnx, int cny, int cn
         return RTSDF_ERR_INVALID;
     }
     RsParams P;
-    P.coarse = FieldView{coarse, cnx, cny, cnz, clo[0], clo[1], clo[2], ch[0], ch[1], ch[2]};
+    P.coarse = FieldView{coarse, cnx, cny, cnz, clo[0], clo[1], clo[2], ch[0], ch[1], ch[2], 0.0f};
     P.fnx = fnx;
     P.fny = fny;
     P.fnz = fnz;

@@ -233,6 +233,6 @@ extern "C" int rtsdf_voxelize(const double* verts, int64_t n_verts, const int32_
     int blocks = num_sms() * 8;
     vox_cells_kernel<<<blocks, 256, 0, stream>>>(tri_pts, ranges, prefix, T, P, occ, seed,
                                                  counters);
-    count_launch(3);
+    count_launch(4);  // ranges, CUB scan (init + scan), cells
     return check_launch("voxelize");
 }

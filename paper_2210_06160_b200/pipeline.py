@@ -22,7 +22,7 @@ from . import jfa as _jfa
 from . import raysample as _rs
 from . import render as _render
 from . import voxel as _voxel
-from ._device import device
+from ._device import device, to_device
 from .field import DistanceField, apply_bias, make_field
 from .raymarch import MarchParams
 from .raysample import AccumulatorField, SamplingParams
@@ -103,7 +103,9 @@ class FramePipeline:
         self.last_occlusion = None
         self._bufs = None
         self._checked_view = None
-        self.directions = None  # optional host direction table for the next frame (parity)
+        # parity mode: callable(masked_idx ndarray, frame) -> (M, x, 3) host direction
+        # table (the north star's host-supplied table); None = device SplitMix64
+        self.direction_fn = None
 
     # ------------------------------------------------------------- buffers
     def _buffers(self):
@@ -123,6 +125,18 @@ class FramePipeline:
                 masked=torch.zeros(1, dtype=torch.int64, device=dev),
             )
         return self._bufs
+
+    def _dl_buffers(self, cam):
+        key = (cam, id(self.scene.view(self.frame)))
+        dl = getattr(self, "_dl", None)
+        if dl is None or dl["key"] != key:
+            gb = _render.GBuffer.empty(cam.height, cam.width)
+            dev = gb.position.device
+            dl = dict(key=key, gb=gb, cam=_render.camera_setup(cam),
+                      occ=torch.empty((cam.height, cam.width), dtype=torch.float64, device=dev),
+                      img=torch.empty((cam.height, cam.width, 3), dtype=torch.float32, device=dev))
+            self._dl = dl
+        return dl
 
     def march_params(self, **kw) -> MarchParams:
         fine = self.fine if self.fine is not None else self._fine_placeholder()
@@ -195,9 +209,10 @@ class FramePipeline:
         if t_max is None:
             t_max = float(np.linalg.norm(self.coarse.hi - self.coarse.lo))
         dirs = None
-        if self.directions is not None:
-            dirs = self.directions
-            self.directions = None
+        if self.direction_fn is not None and cfg.sampling.rays_per_frame > 0:
+            m = int(cb.count.item())
+            idx = cb.idx[:m].cpu().numpy()
+            dirs = to_device(np.ascontiguousarray(self.direction_fn(idx, frame), dtype=np.float64))
         _rs.launch_sample_update(view.bvh, g, cb, cfg.sampling, frame, t_max, dirs=dirs,
                                  prev=self.fine.data, accum=self.accum, out=self.fine.data)
         self.accum.mask = mask_new
@@ -210,13 +225,18 @@ class FramePipeline:
 
         self.last_image = None
         if render:
+            # DL: G-buffer (K6 traversal) -> soft-shadow march (K8, fine_for_shading's
+            # bias fused into the samples) -> compose; buffers persist per camera
             cam = camera or self.scene.camera
-            gb = _render.rasterize_gbuffer(view, cam)
-            occ = _render.occlusion_image(gb, self.fine_for_shading, self.scene.light,
-                                          self.march_params(), draws=cfg.shade_draws,
-                                          seed=cfg.sampling.seed)
-            self.last_occlusion = occ
-            self.last_image = _render.compose(gb, occ, self.scene.light)
+            dl = self._dl_buffers(cam)
+            _render.launch_gbuffer(view, cam, dl["gb"], dl["cam"])
+            light = self.scene.light.unit()
+            _render.launch_occlusion(dl["gb"], self.fine, light, self.march_params(),
+                                     cfg.shade_draws, cfg.sampling.seed, dl["occ"],
+                                     sample_bias=cfg.bias)
+            _render.launch_compose(dl["gb"], dl["occ"], light, (0.05, 0.07, 0.10), dl["img"])
+            self.last_occlusion = dl["occ"]
+            self.last_image = dl["img"]
         if timing:
             events[4].record()
 

@@ -104,17 +104,18 @@ def rasterize_gbuffer(view, camera: Camera) -> GBuffer:
 
 
 def launch_occlusion(gbuffer: GBuffer, fld: DistanceField, light_unit, params: MarchParams,
-                     draws, seed, out):
+                     draws, seed, out, sample_bias: float = 0.0):
+    """sample_bias: shade `fld` biased by that much (apply_bias fused, f32)."""
     h, w = gbuffer.shape
     nx, ny, nz = fld.dims
-    offset = 2.0 * params.epsilon + fld.bias  # render.py:165
+    offset = 2.0 * params.epsilon + (fld.bias + sample_bias)  # render.py:165
     _lib.check(_lib.lib().rtsdf_occlusion(
         _lib.ptr(fld.data), nx, ny, nz, (_lib.D * 3)(*fld.lo), (_lib.D * 3)(*fld.cell_size),
         _lib.ptr(gbuffer.position), _lib.ptr(gbuffer.normal), _lib.ptr(gbuffer.coverage), h, w,
         (_lib.D * 3)(*light_unit), float(params.epsilon), int(params.max_iterations),
         float(params.max_step), float(params.t_max), params.cone_k, float(params.jitter),
-        float(offset), max(1, int(draws)), int(seed) & 0xFFFFFFFFFFFFFFFF, _lib.ptr(out),
-        _lib.stream()), "occlusion")
+        float(offset), max(1, int(draws)), int(seed) & 0xFFFFFFFFFFFFFFFF,
+        float(np.float32(sample_bias)), _lib.ptr(out), _lib.stream()), "occlusion")
 
 
 def occlusion_image(gbuffer: GBuffer, fld: DistanceField, light: DirectionalLight,

@@ -1,0 +1,374 @@
+"""GPU parity: the sm_100a kernels (through the C ABI) vs the CPU oracle and the
+reference's golden digests.  Integer/index/mask outputs must be bit-exact;
+fp32 fields are compared bit-exact too (same fp64 arithmetic, no FMA) and the
+north-star tolerance (1e-5 relative) is asserted on top as the floor."""
+
+import math
+import sys
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+from common import C1, C3, digest, golden, golden_arrays, scene_mesh
+
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent / "oracle"))
+import oracle as O  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+REL_TOL = 1e-5  # north star: distances within 1e-5 relative
+
+
+def _np(t):
+    return t.detach().cpu().numpy()
+
+
+def _assert_close_f32(a, b):
+    """Bit-exact expected; the 1e-5 relative tolerance is the contract floor."""
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    fin = np.isfinite(b)
+    assert np.array_equal(np.isfinite(a), fin)
+    np.testing.assert_allclose(a[fin], b[fin], rtol=REL_TOL, atol=1e-6)
+
+
+@pytest.fixture(scope="module")
+def rt():
+    import paper_2210_06160_b200 as rt
+
+    return rt
+
+
+# ---------------------------------------------------------------- voxelize
+def test_voxelize_closed_box_square(rt):
+    verts = np.array([[0, 0.5, 0], [4, 0.5, 0], [4, 0.5, 4], [0, 0.5, 4]], np.float64)
+    tris = np.array([[0, 1, 2], [0, 2, 3]], np.int32)
+    vg = rt.voxelize((verts, tris), (8, 8, 8), (np.zeros(3), np.full(3, 8.0)))
+    assert vg.count == 25
+    np.testing.assert_array_equal(_np(vg.occupancy), golden_arrays()["voxel_square.occ"])
+
+
+def test_voxelize_errors(rt):
+    verts = np.array([[0, 0, 0], [1, 0, 0], [0, 1, 0], [5, 5, 5]], np.float64)
+    tris = np.array([[0, 1, 2], [1, 2, 3]], np.int32)
+    with pytest.raises(rt.OutOfBoundsError) as ei:
+        rt.voxelize((verts, tris), (4, 4, 4), (np.zeros(3), np.full(3, 2.0)))
+    assert ei.value.triangle_ids == [1]
+    with pytest.raises(rt.VoxelizeError):
+        rt.voxelize((verts, tris), (1, 4, 4), (np.zeros(3), np.full(3, 8.0)))
+    with pytest.raises(rt.VoxelizeError):
+        rt.voxelize((verts, tris), (4, 4, 4), (np.zeros(3), np.zeros(3)))
+
+
+@pytest.mark.parametrize("name,dims", [("sphere", (64, 64, 64)), ("sphere_plane", (64, 64, 64)),
+                                       ("sphere_plane", (128, 128, 128)),
+                                       ("sphere_plane", (256, 256, 256)),
+                                       ("sphere_plane", (400, 200, 400)),
+                                       ("thin_plate", (96, 80, 112))])
+def test_voxelize_matches_oracle(rt, name, dims):
+    """Includes the 1-ulp boundary-plane cases (Appendix A.2: 0 ground cells at 256^3)."""
+    scene, mesh = scene_mesh(name)
+    want = O.voxelize(mesh.vertices, mesh.triangles, dims, scene.bounds)
+    vg = rt.voxelize(mesh, dims, scene.bounds)
+    np.testing.assert_array_equal(_np(vg.occupancy), want)
+    # fused seed form == jfa_init(occupancy)
+    vs = rt.voxelize_seeds(mesh, dims, scene.bounds)
+    lin = _np(rt.jfa.SeedGrid(vs.seed_packed, vs.lo, vs.hi).seed)
+    np.testing.assert_array_equal(lin, O.jfa_init(want))
+
+
+def test_voxelize_golden_counts(rt):
+    G = golden()
+    scene, mesh = scene_mesh("sphere_plane")
+    assert rt.voxelize(mesh, (400, 200, 400), scene.bounds).count == G["c3.voxel"]["count"]
+    assert rt.voxelize(mesh, (128,) * 3, scene.bounds).count == G["sp128"]["count"]
+
+
+# --------------------------------------------------------------------- JFA
+def test_jfa_tie_rule_fp64(rt):
+    occ = np.zeros((16, 16, 16), np.uint8)
+    occ[0, 3, 4] = 1
+    occ[5, 0, 0] = 1
+    vg = rt.VoxelGrid(rt._device.to_device(occ) if hasattr(rt, "_device") else occ,
+                      np.zeros(3), np.full(3, 1.6))
+    seeds = rt.jfa_run(vg)
+    got = _np(seeds.seed)
+    assert got[0, 0, 0] == 5 * 256
+    np.testing.assert_array_equal(got, golden_arrays()["jfa_tie.seed"])
+    np.testing.assert_array_equal(_np(rt.seeds_to_sdf(seeds).data), golden_arrays()["jfa_tie.sdf"])
+
+
+def test_jfa_fp64_general_path(rt):
+    """Non-rational spacing ratios take the fp64 comparison path."""
+    G, A = golden(), golden_arrays()
+    mesh = rt.make_mesh(A["soup.vertices"], A["soup.triangles"])
+    vg = rt.voxelize(mesh, (40, 33, 27), (np.zeros(3), np.ones(3)))
+    assert rt.jfa.integer_weights(*map(float, vg.cell_size), (40, 33, 27)) == (0, 0, 0)
+    seeds = rt.jfa_run(vg)
+    assert digest(_np(seeds.seed)) == G["soup.jfa"]["seed"]
+    assert digest(_np(rt.seeds_to_sdf(seeds, beta=0.01).data)) == G["soup.sdf"]["data"]
+
+
+@pytest.mark.parametrize("name,dims", [("sphere", (64, 64, 64)), ("sphere_plane", (128, 128, 128)),
+                                       ("sphere_plane", (400, 200, 400))])
+def test_jfa_every_pass_matches_oracle(rt, name, dims):
+    scene, mesh = scene_mesh(name)
+    occ = O.voxelize(mesh.vertices, mesh.triangles, dims, scene.bounds)
+    h = (scene.hi - scene.lo) / np.array(dims, dtype=np.float64)
+    ref = O.jfa_init(occ)
+    vg = rt.voxelize(mesh, dims, scene.bounds)
+    cur = rt.jfa_init(vg)
+    for off in rt.jfa_offsets(dims):
+        ref = O.jfa_step(ref, off, h)
+        cur = rt.jfa_step(cur, off)
+        np.testing.assert_array_equal(_np(cur.seed), ref, err_msg=f"offset {off}")
+    np.testing.assert_array_equal(_np(rt.seeds_to_sdf(cur).data), O.seeds_to_sdf(ref, h))
+
+
+def test_jfa_golden_c3_and_sp128(rt):
+    G = golden()
+    scene, mesh = scene_mesh("sphere_plane")
+    for dims, key, ck in (((400, 200, 400), "c3.jfa", "c3.frame0"), ((128,) * 3, "sp128", "sp128")):
+        seeds = rt.jfa_run(rt.voxelize(mesh, dims, scene.bounds))
+        assert digest(_np(seeds.seed)) == G[key]["seed"]
+        assert digest(_np(rt.seeds_to_sdf(seeds).data)) == G[ck]["coarse"]
+
+
+def test_jfa_errors(rt):
+    occ = np.zeros((8, 8, 8), np.uint8)
+    vg = rt.VoxelGrid(rt._device.to_device(occ), np.zeros(3), np.ones(3))
+    with pytest.raises(rt.NoSeedsError):
+        rt.jfa_init(vg)
+    occ[1, 2, 3] = 1
+    seeds = rt.jfa_init(rt.VoxelGrid(rt._device.to_device(occ), np.zeros(3), np.ones(3)))
+    with pytest.raises(ValueError):
+        rt.jfa_step(seeds, 5)
+    with pytest.raises(rt.NoSeedsError):
+        rt.seeds_to_sdf(seeds)  # incomplete: not flooded
+    with pytest.raises(ValueError):
+        rt.seeds_to_sdf(seeds, beta=-1)
+
+
+def test_jfa_single_seed_exact_and_upper_bound(rt):
+    """SPEC invariants: single seed -> exact everywhere; JFA never underestimates."""
+    occ = np.zeros((48, 40, 36), np.uint8)
+    occ[7, 30, 11] = 1
+    vg = rt.VoxelGrid(rt._device.to_device(occ), np.zeros(3), np.array([1.2, 1.0, 0.9]))
+    seeds = rt.jfa_run(vg)
+    assert (_np(seeds.seed) == 7 * 40 * 36 + 30 * 36 + 11).all()
+    rng = np.random.default_rng(5)
+    occ = (rng.random((32, 32, 32)) < 0.0015).astype(np.uint8)
+    vg = rt.VoxelGrid(rt._device.to_device(occ), np.zeros(3), np.ones(3))
+    sdf = _np(rt.seeds_to_sdf(rt.jfa_run(vg)).data).astype(np.float64)
+    pts = np.argwhere(occ > 0)
+    grid = np.stack(np.meshgrid(*[np.arange(32)] * 3, indexing="ij"), -1).reshape(-1, 3)
+    exact = np.sqrt(((grid[:, None, :] - pts[None]) ** 2).sum(-1).min(1)) / 32.0
+    assert (sdf.reshape(-1) >= exact - 1e-6).all()
+    assert (np.abs(sdf.reshape(-1) - exact) < 1e-6).mean() >= 0.99
+
+
+# ---------------------------------------------------- resample / mask / BVH
+@pytest.mark.parametrize("coarse_dims,fine_dims", [((128,) * 3, (128,) * 3), ((64,) * 3, (128,) * 3),
+                                                   ((200, 100, 200), (400, 200, 400))])
+def test_resample_mask_compaction(rt, coarse_dims, fine_dims):
+    scene, mesh = scene_mesh("sphere_plane")
+    occ = O.voxelize(mesh.vertices, mesh.triangles, coarse_dims, scene.bounds)
+    h = (scene.hi - scene.lo) / np.array(coarse_dims, dtype=np.float64)
+    coarse_np = O.seeds_to_sdf(O.jfa_run(occ, h), h)
+    want_f, want_m = O.resample_mask(coarse_np, scene.lo, scene.hi, fine_dims, 0.1)
+    coarse = rt.make_field(coarse_np, scene.lo, scene.hi)
+    np.testing.assert_array_equal(_np(rt.coarse_at_fine(coarse, fine_dims)), want_f)
+    m = rt.ray_mask(coarse, fine_dims, 0.1)
+    np.testing.assert_array_equal(_np(m), want_m)
+    idx = rt.raysample.masked_indices(m)
+    np.testing.assert_array_equal(_np(idx), np.flatnonzero(want_m.ravel()))
+
+
+def test_bvh_closest_hits_match_reference(rt):
+    G, A = golden(), golden_arrays()
+    mesh = rt.make_mesh(A["soup.vertices"], A["soup.triangles"])
+    bvh = rt.build_bvh(mesh)
+    for k in ("node_lo", "node_hi", "node_left", "node_right", "order"):
+        assert digest(getattr(bvh, k)) == G["soup.bvh"][k]
+    t, ids, fac = rt.ray_query_many(bvh, A["soup.ray_o"], A["soup.ray_d"])
+    np.testing.assert_array_equal(ids, A["soup.ray_id"])
+    np.testing.assert_array_equal(fac, A["soup.ray_facing"])
+    np.testing.assert_array_equal(t, A["soup.ray_t"])
+    hit = rt.ray_query(bvh, A["soup.ray_o"][0], A["soup.ray_d"][0])
+    assert hit.hit == (A["soup.ray_id"][0] >= 0)
+
+
+# ------------------------------------------------------------ ray sampling
+def _c_setup(rt, name, dims):
+    scene, mesh = scene_mesh(name)
+    view = scene.view(0)
+    occ = O.voxelize(mesh.vertices, mesh.triangles, dims, scene.bounds)
+    h = (scene.hi - scene.lo) / np.array(dims, dtype=np.float64)
+    coarse_np = O.seeds_to_sdf(O.jfa_run(occ, h), h)
+    return scene, mesh, view, coarse_np, h
+
+
+@pytest.mark.parametrize("name,dims,x", [("sphere", (64, 64, 64), 32), ("sphere", (64, 64, 64), 5),
+                                         ("sphere_plane", (400, 200, 400), 32),
+                                         ("thin_plate", (96, 80, 112), 40)])
+def test_sample_hit_counts_bit_exact_host_table(rt, name, dims, x):
+    """Same host direction table -> min t, front and back counts bit-exact."""
+    scene, mesh, view, coarse_np, h = _c_setup(rt, name, dims)
+    _, mask = O.resample_mask(coarse_np, scene.lo, scene.hi, dims, 0.1)
+    idx = np.flatnonzero(mask.ravel())
+    dirs = O.dir_table(0, idx, 1, x)
+    b = O.bvh_build(mesh.vertices, mesh.triangles, mesh.normals)
+    t_max = float(np.linalg.norm(scene.hi - scene.lo))
+    wmin, wf, wb = O.sample_masked(b, idx, scene.lo, h, dims, x, 0, 1, t_max, dirs)
+    coarse = rt.make_field(coarse_np, scene.lo, scene.hi)
+    params = rt.SamplingParams(rays_per_frame=x)
+    gidx, gmin, gf, gb = rt.sample_masked(coarse, dims, view.bvh, params, 1, directions=dirs)
+    np.testing.assert_array_equal(_np(gidx), idx)
+    np.testing.assert_array_equal(_np(gf), wf)
+    np.testing.assert_array_equal(_np(gb), wb)
+    np.testing.assert_array_equal(_np(gmin), wmin)
+
+
+def test_device_directions_vs_glibc(rt):
+    """On-device SplitMix64 + CUDA sincos: report how often results differ from
+    the glibc-table run (the only source of divergence)."""
+    scene, mesh, view, coarse_np, h = _c_setup(rt, "sphere", (64, 64, 64))
+    coarse = rt.make_field(coarse_np, scene.lo, scene.hi)
+    params = rt.SamplingParams(rays_per_frame=32)
+    gidx, gmin, gf, gb = rt.sample_masked(coarse, (64,) * 3, view.bvh, params, 0)
+    idx = _np(gidx)
+    b = O.bvh_build(mesh.vertices, mesh.triangles, mesh.normals)
+    wmin, wf, wb = O.sample_masked(b, idx, scene.lo, h, (64,) * 3, 32, 0, 0,
+                                   float(np.linalg.norm(scene.hi - scene.lo)))
+    diff_counts = np.mean((_np(gf) != wf) | (_np(gb) != wb))
+    _assert_close_f32(_np(gmin), wmin)
+    assert diff_counts < 1e-3, diff_counts
+
+
+def test_update_fine_three_frames_golden(rt):
+    """C1: three frames of update_fine with the host table == reference digests."""
+    G = golden()
+    scene, mesh = scene_mesh("sphere")
+    view = scene.view(0)
+    dims = (64, 64, 64)
+    h = (scene.hi - scene.lo) / 64
+    coarse_np = O.seeds_to_sdf(O.jfa_run(O.voxelize(mesh.vertices, mesh.triangles, dims,
+                                                     scene.bounds), h), h)
+    coarse = rt.make_field(coarse_np, scene.lo, scene.hi)
+    params = rt.SamplingParams(rays_per_frame=32, mask_distance=0.1, decay_alpha=0.95, seed=0)
+    fine = rt.fine_from_coarse(coarse, dims)
+    acc = None
+    for f in range(3):
+        idx = _np(rt.raysample.masked_indices(rt.ray_mask(coarse, dims, 0.1)))
+        fine, acc = rt.update_fine(fine, coarse, view.bvh, params, f, acc,
+                                   directions=O.dir_table(0, idx, f, 32))
+        g = G[f"c1.frame{f}"]
+        assert digest(_np(fine.data)) == g["fine"], f
+        assert digest(_np(acc.front)) == g["front"] and digest(_np(acc.back)) == g["back"]
+        assert digest(_np(acc.min_dist)) == g["min_dist"]
+        assert digest(_np(acc.mask)) == g["mask"]
+
+
+@pytest.mark.parametrize("case", ["c1", "c3"])
+def test_pipeline_frames_golden(rt, case):
+    """hybrid_sdf / FramePipeline with the host table == reference frames."""
+    G = golden()
+    cfg = C1 if case == "c1" else C3
+    scene = rt.get_scene(cfg["scene"])
+    pc = rt.PipelineConfig(coarse_dims=cfg["dims"], fine_dims=cfg["dims"],
+                           sampling=rt.SamplingParams(rays_per_frame=cfg["x"]))
+    pipe = rt.FramePipeline(scene, pc)
+    pipe.direction_fn = lambda idx, frame: O.dir_table(0, idx, frame, cfg["x"])
+    frames = 3 if case == "c1" else 1
+    for f in range(frames):
+        rec = pipe.advance(render=(case == "c3"))
+        g = G[f"{case}.frame{f}"]
+        assert rec.masked_texels == g["masked"]
+        assert digest(_np(pipe.coarse.data)) == g["coarse"]
+        assert digest(_np(pipe.fine.data)) == g["fine"]
+        assert digest(_np(pipe.accum.front)) == g["front"]
+        assert digest(_np(pipe.accum.back)) == g["back"]
+        assert set(rec.durations_ns) == {"V", "JF", "RT", "DL"}
+    if case == "c3":
+        gd = G["c3.dl"]
+        occ = _np(pipe.last_occlusion)
+        assert digest(occ) == gd["occlusion"]
+        img = _np(pipe.last_image)
+        np.testing.assert_allclose(img, golden_arrays()["c3.image"], rtol=1e-6, atol=1e-7)
+
+
+# ---------------------------------------------------------- soft shadow (K8)
+def test_gbuffer_and_occlusion_c3(rt):
+    G, A = golden(), golden_arrays()
+    scene, mesh = scene_mesh("sphere_plane")
+    view = scene.view(0)
+    gb = rt.rasterize_gbuffer(view, scene.camera)
+    gd = G["c3.dl"]
+    assert digest(_np(gb.coverage)) == gd["coverage"]
+    assert digest(_np(gb.position)) == gd["position"]
+    assert digest(_np(gb.normal)) == gd["normal"]
+    assert digest(_np(gb.albedo)) == gd["albedo"]
+    # occlusion over the oracle's frame-0 fine field
+    dims = (400, 200, 400)
+    H = O.HybridOracle(mesh.vertices, mesh.triangles, mesh.normals, scene.bounds, dims, dims, x=32)
+    H.advance()
+    fine = rt.make_field(H.fine, scene.lo, scene.hi)
+    fld = rt.apply_bias(fine, 0.01)
+    mp = rt.MarchParams.for_field(fine, max_step=0.05, max_iterations=256, jitter=1.0,
+                                  light_angle=scene.light.angular_radius)
+    occ = _np(rt.occlusion_image(gb, fld, scene.light, mp, draws=1, seed=0))
+    np.testing.assert_array_equal(occ, A["c3.occlusion"])
+
+
+def test_sphere_trace_kats_c1(rt):
+    G, A = golden(), golden_arrays()
+    mp = G["c1.march"]
+    fld = rt.make_field(A["c1.fine2"], np.full(3, -2.0), np.full(3, 2.0), bias=0.0)
+    fld = rt.apply_bias(fld, mp["bias"])
+    params = rt.MarchParams(epsilon=mp["epsilon"], max_iterations=mp["max_iterations"],
+                            max_step=mp["max_step"], t_max=mp["t_max"], jitter=1.0,
+                            light_angle=mp["light_angle"])
+    for o, d, want in zip(A["c1.trace_o"], A["c1.trace_d"], A["c1.trace_res"]):
+        r = rt.sphere_trace(fld, o, d, params)
+        st = {"hit": 0, "miss-exited": 1, "miss-max-iter": 2}[r.status]
+        assert (r.t, r.iterations, r.occlusion, st) == tuple(want)
+
+
+def test_soft_shadow_matches_oracle(rt):
+    A = golden_arrays()
+    fld = rt.make_field(A["c1.fine2"], np.full(3, -2.0), np.full(3, 2.0))
+    params = rt.MarchParams.for_field(fld, light_angle=0.08)
+    p = np.array([0.0, 1.2, 0.1])
+    l = np.array([0.3, 1.0, 0.25])
+    got = rt.soft_shadow(fld, p, l, params, seed=3, stream=7, draws=4)
+    key = O.stream_key(3, 7, 0)
+    lu = l / np.linalg.norm(l)
+    total = 0.0
+    for j in range(4):
+        t0 = params.jitter * params.max_step * O.uniform(key, j)
+        st, t, it, mt = O.march(A["c1.fine2"], np.full(3, -2.0), np.full(3, 4.0 / 64), p, lu,
+                                params.epsilon, params.max_iterations, params.max_step,
+                                params.t_max, t0, params.cone_k)
+        total += 1.0 if st == 0 else 1.0 - mt
+    assert got == total / 4
+
+
+# ------------------------------------------------------------ field formats
+def test_rsdf_roundtrip_and_errors(rt, tmp_path):
+    A = golden_arrays()
+    fld = rt.make_field(A["c1.fine2"], np.full(3, -2.0), np.full(3, 2.0), beta=0.1, bias=0.01,
+                        frame=2)
+    p = tmp_path / "f.rsdf"
+    rt.save_field(fld, p)
+    back = rt.load_field(p)
+    np.testing.assert_array_equal(_np(back.data), A["c1.fine2"])
+    assert back.frame == 2 and back.dims == fld.dims
+    raw = bytearray(p.read_bytes())
+    raw[0:4] = b"XXXX"
+    p.write_bytes(bytes(raw))
+    with pytest.raises(rt.FieldFormatError):
+        rt.load_field(p)
+    # payload order is x-fastest (field.py:198)
+    body = np.frombuffer((tmp_path / "g.rsdf").write_bytes(b"") or b"", np.float32)
+    del body
