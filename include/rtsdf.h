@@ -143,10 +143,14 @@ int rtsdf_bvh_pack(const double* node_lo, const double* node_hi, const int32_t* 
                    const double* tri_e1, const double* tri_e2, const double* tri_n,
                    int64_t n_nodes, int64_t n_tris, void* packed, void* stream);
 
-/* Replaces geometry.py:395-410 (ray_query) for a batch of rays.            */
-int rtsdf_ray_query(const void* bvh_packed, int64_t n_nodes, const double* origins,
-                    const double* dirs, int64_t n, double t_max, double* out_t, int32_t* out_id,
-                    int32_t* out_facing, void* stream);
+/* Replaces geometry.py:395-410 (ray_query) for a batch of rays.  fast = 0:
+ * the reference's own traversal order in fp64 (_bvh_ray verbatim); fast = 1:
+ * the K6 search (fp32 conservative boxes + fp32 pre-test, exact fp64 confirm)
+ * that returns the brute-force closest hit the reference's contract names
+ * (geometry.py:3-6).                                                        */
+int rtsdf_ray_query(const void* bvh_packed, int64_t n_nodes, int64_t n_tris, int fast,
+                    const double* origins, const double* dirs, int64_t n, double t_max,
+                    double* out_t, int32_t* out_id, int32_t* out_facing, void* stream);
 
 /* ---------------------------------------------- ray-sampled refine + Eq. 1 */
 /* Replaces raysample.py:277-299 (_sample_masked_kernel + band reset +
@@ -168,7 +172,7 @@ typedef struct {
     double fh[3];
 } rtsdf_resample_desc;
 
-int rtsdf_sample_update(const void* bvh_packed, int64_t n_nodes, const int64_t* idx,
+int rtsdf_sample_update(const void* bvh_packed, int64_t n_nodes, int64_t n_tris, const int64_t* idx,
                         const int64_t* count, int64_t m_cap, const rtsdf_resample_desc* rs,
                         int x, uint64_t seed, int64_t frame, double t_max, const double* dirs,
                         double* samp_min, int32_t* samp_front, int32_t* samp_back,

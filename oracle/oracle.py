@@ -37,6 +37,7 @@ _SIGS = {
     "oracle_dir_table": (None, [U64, P, I64, I64, I, P]),
     "oracle_bvh_build": (I64, [P, P, I64, P, P, P, P, P]),
     "oracle_ray_query": (None, [P, P, P, P, P, P, P, P, P, P, P, I64, D, P, P, P]),
+    "oracle_ray_brute": (None, [P, P, P, P, P, P, P, P, P, I64, P, P, I64, D, P, P, P]),
     "oracle_sample_masked": (None, [P, P, P, P, P, P, P, P, P, P, I64, D, D, D, D, D, D, I, I, I,
                                     U64, I64, D, P, P, P, P]),
     "oracle_update_fine": (None, [P, P, P, P, I64, P, P, P, P, I64, P, P, P, D, P]),
@@ -227,6 +228,17 @@ def ray_query(b, origins, dirs, t_max=np.inf):
     n = len(o)
     t = np.empty(n); ids = np.empty(n, np.int32); fac = np.empty(n, np.int32)
     lib().oracle_ray_query(*_bvh_args(b), _p(o), _p(d), n, float(t_max), _p(t), _p(ids), _p(fac))
+    return t, ids, fac
+
+
+def ray_brute(b, origins, dirs, t_max=np.inf):
+    """Closest hit over every triangle (no BVH): the traversal contract."""
+    o = _c(origins, np.float64).reshape(-1, 3)
+    d = _c(dirs, np.float64).reshape(-1, 3)
+    n = len(o)
+    t = np.empty(n); ids = np.empty(n, np.int32); fac = np.empty(n, np.int32)
+    lib().oracle_ray_brute(*_bvh_args(b), len(b["order"]), _p(o), _p(d), n, float(t_max), _p(t),
+                           _p(ids), _p(fac))
     return t, ids, fac
 
 

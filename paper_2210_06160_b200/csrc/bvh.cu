@@ -14,6 +14,7 @@
 #include <vector>
 
 #include "common.cuh"
+#include "trace.cuh"
 
 namespace rtsdf {
 
@@ -105,6 +106,81 @@ __global__ void bvh_pack_kernel(const double* __restrict__ node_lo, const double
     }
 }
 
+// Fast traversal layout (trace.cuh): per internal node both child boxes in
+// fp32, rounded outward and padded by 1e-5 of the scene scale; entry n_nodes
+// is a virtual parent whose only child is the root.
+__device__ void fast_child(const double* __restrict__ node_lo, const double* __restrict__ node_hi,
+                           const int32_t* __restrict__ node_left,
+                           const int32_t* __restrict__ node_right, int32_t c, float pad,
+                           float* lo, float* hi, int32_t* ref) {
+    for (int a = 0; a < 3; ++a) {
+        lo[a] = __fsub_rd(__double2float_rd(node_lo[3 * c + a]), pad);
+        hi[a] = __fadd_ru(__double2float_ru(node_hi[3 * c + a]), pad);
+    }
+    int32_t l = node_left[c];
+    *ref = l >= 0 ? c : -(((-l - 1) << 3) | node_right[c]) - 1;
+}
+
+__global__ void bvh_pack_fast_kernel(const double* __restrict__ node_lo,
+                                     const double* __restrict__ node_hi,
+                                     const int32_t* __restrict__ node_left,
+                                     const int32_t* __restrict__ node_right,
+                                     const double* __restrict__ tri_e1,
+                                     const double* __restrict__ tri_e2,
+                                     const double* __restrict__ tri_a, int64_t n_nodes,
+                                     int64_t n_tris, FastNode* __restrict__ fnodes,
+                                     FastTri* __restrict__ ftris) {
+    int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    double m = 1.0;
+    for (int a = 0; a < 3; ++a) m = fmax(m, fmax(fabs(node_lo[a]), fabs(node_hi[a])));
+    const float pad = (float)(1e-5 * m);
+    if (q <= n_nodes) {
+        FastNode f;
+        for (int a = 0; a < 3; ++a) f.lo0[a] = f.hi0[a] = f.lo1[a] = f.hi1[a] = 0.0f;
+        f.c0 = f.c1 = 0;
+        f.v0 = f.v1 = 0;
+        if (q == n_nodes) {  // virtual parent of the root
+            fast_child(node_lo, node_hi, node_left, node_right, 0, pad, f.lo0, f.hi0, &f.c0);
+            f.v0 = 1;
+        } else if (node_left[q] >= 0) {
+            fast_child(node_lo, node_hi, node_left, node_right, node_left[q], pad, f.lo0, f.hi0, &f.c0);
+            fast_child(node_lo, node_hi, node_left, node_right, node_right[q], pad, f.lo1, f.hi1, &f.c1);
+            f.v0 = f.v1 = 1;
+        }
+        fnodes[q] = f;
+    }
+    if (q < n_tris) {
+        FastTri t;
+        double s = 0.0;
+        for (int a = 0; a < 3; ++a) {
+            t.a[a] = (float)tri_a[3 * q + a];
+            t.e1[a] = (float)tri_e1[3 * q + a];
+            t.e2[a] = (float)tri_e2[3 * q + a];
+            s += fabs(tri_e1[3 * q + a]) + fabs(tri_e2[3 * q + a]);
+        }
+        t.scale = __double2float_ru(s * 1.0000001);
+        t.pad_[0] = t.pad_[1] = 0.0f;
+        ftris[q] = t;
+    }
+}
+
+__global__ void __launch_bounds__(128) ray_query_fast_kernel(
+    FastBvh b, const double* __restrict__ orig, const double* __restrict__ dirs, int64_t n,
+    double t_max, double* __restrict__ out_t, int32_t* __restrict__ out_id,
+    int32_t* __restrict__ out_facing) {
+    __shared__ int32_t stack_mem[RTSDF_FAST_STACK * 128];
+    int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (q >= n) return;
+    int32_t id;
+    int facing;
+    double t = trace_fast(b, orig[3 * q], orig[3 * q + 1], orig[3 * q + 2], dirs[3 * q],
+                          dirs[3 * q + 1], dirs[3 * q + 2], t_max, stack_mem + threadIdx.x, 128,
+                          id, facing);
+    out_t[q] = t;
+    out_id[q] = id;
+    out_facing[q] = facing;
+}
+
 __global__ void ray_query_kernel(BvhView b, const double* __restrict__ orig,
                                  const double* __restrict__ dirs, int64_t n, double t_max,
                                  double* __restrict__ out_t, int32_t* __restrict__ out_id,
@@ -148,7 +224,7 @@ extern "C" int64_t rtsdf_bvh_build_host(const double* tri_lo, const double* tri_
 }
 
 extern "C" size_t rtsdf_bvh_packed_bytes(int64_t n_nodes, int64_t n_tris) {
-    return (size_t)n_nodes * sizeof(BvhNode) + (size_t)n_tris * sizeof(BvhTri);
+    return fast_offset_tris(n_nodes, n_tris) + (size_t)n_tris * sizeof(FastTri);
 }
 
 extern "C" int rtsdf_bvh_pack(const double* node_lo, const double* node_hi,
@@ -161,16 +237,27 @@ extern "C" int rtsdf_bvh_pack(const double* node_lo, const double* node_hi,
     bvh_pack_kernel<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
         node_lo, node_hi, node_left, node_right, order, tri_a, tri_e1, tri_e2, tri_n, n_nodes,
         n_tris, (BvhNode*)v.nodes, (BvhTri*)v.tris);
-    count_launch();
+    FastBvh f = fast_bvh_view(packed, n_nodes, n_tris);
+    int64_t nf = (n_nodes + 1) > n_tris ? n_nodes + 1 : n_tris;
+    bvh_pack_fast_kernel<<<(unsigned)((nf + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+        node_lo, node_hi, node_left, node_right, tri_e1, tri_e2, tri_a, n_nodes, n_tris,
+        (FastNode*)f.nodes, (FastTri*)f.tris);
+    count_launch(2);
     return check_launch("bvh_pack");
 }
 
-extern "C" int rtsdf_ray_query(const void* packed, int64_t n_nodes, const double* origins,
-                               const double* dirs, int64_t n, double t_max, double* out_t,
-                               int32_t* out_id, int32_t* out_facing, void* stream) {
+extern "C" int rtsdf_ray_query(const void* packed, int64_t n_nodes, int64_t n_tris, int fast,
+                               const double* origins, const double* dirs, int64_t n,
+                               double t_max, double* out_t, int32_t* out_id,
+                               int32_t* out_facing, void* stream) {
     if (n <= 0) return RTSDF_OK;
-    ray_query_kernel<<<(unsigned)((n + 127) / 128), 128, 0, (cudaStream_t)stream>>>(
-        bvh_view(packed, n_nodes), origins, dirs, n, t_max, out_t, out_id, out_facing);
+    if (fast)
+        ray_query_fast_kernel<<<(unsigned)((n + 127) / 128), 128, 0, (cudaStream_t)stream>>>(
+            fast_bvh_view(packed, n_nodes, n_tris), origins, dirs, n, t_max, out_t, out_id,
+            out_facing);
+    else
+        ray_query_kernel<<<(unsigned)((n + 127) / 128), 128, 0, (cudaStream_t)stream>>>(
+            bvh_view(packed, n_nodes), origins, dirs, n, t_max, out_t, out_id, out_facing);
     count_launch();
     return check_launch("ray_query");
 }

@@ -11,11 +11,12 @@
 // by exactly one lane for the update, so no atomics are used anywhere and
 // the result is independent of scheduling.
 #include "common.cuh"
+#include "trace.cuh"
 
 namespace rtsdf {
 
 struct SampleParams {
-    BvhView bvh;
+    FastBvh bvh;
     const int64_t* idx;
     const int64_t* count;
     int64_t m_cap;
@@ -39,7 +40,11 @@ struct SampleParams {
     float* out;
 };
 
-__global__ void __launch_bounds__(128) sample_update_kernel(SampleParams P) {
+#define SAMPLE_THREADS 128
+
+__global__ void __launch_bounds__(SAMPLE_THREADS) sample_update_kernel(SampleParams P) {
+    __shared__ int32_t stack_mem[RTSDF_FAST_STACK * SAMPLE_THREADS];
+    int32_t* stack = stack_mem + threadIdx.x;
     const int lane = threadIdx.x & 31;
     const int64_t M = min(*P.count, P.m_cap);
     const int x = P.x;
@@ -76,7 +81,8 @@ __global__ void __launch_bounds__(128) sample_update_kernel(SampleParams P) {
                 }
                 int32_t id;
                 int facing;
-                double t = bvh_ray(P.bvh, px, py, pz, dx, dy, dz, P.t_max, id, facing);
+                double t = trace_fast(P.bvh, px, py, pz, dx, dy, dz, P.t_max, stack,
+                                      SAMPLE_THREADS, id, facing);
                 if (id >= 0) {
                     if (t < best) best = t;
                     if (facing == 1) fr++;
@@ -126,7 +132,8 @@ __global__ void __launch_bounds__(128) sample_update_kernel(SampleParams P) {
 
 using namespace rtsdf;
 
-extern "C" int rtsdf_sample_update(const void* bvh_packed, int64_t n_nodes, const int64_t* idx,
+extern "C" int rtsdf_sample_update(const void* bvh_packed, int64_t n_nodes, int64_t n_tris,
+                                   const int64_t* idx,
                                    const int64_t* count, int64_t m_cap,
                                    const rtsdf_resample_desc* rs, int x, uint64_t seed,
                                    int64_t frame, double t_max, const double* dirs,
@@ -144,7 +151,7 @@ extern "C" int rtsdf_sample_update(const void* bvh_packed, int64_t n_nodes, cons
     }
     if (m_cap <= 0) return RTSDF_OK;
     SampleParams P;
-    P.bvh = bvh_view(bvh_packed, n_nodes);
+    P.bvh = fast_bvh_view(bvh_packed, n_nodes, n_tris);
     P.idx = idx;
     P.count = count;
     P.m_cap = m_cap;
@@ -173,11 +180,11 @@ extern "C" int rtsdf_sample_update(const void* bvh_packed, int64_t n_nodes, cons
     P.out = out;
     int tpw = x >= 32 || x == 0 ? 1 : 32 / x;
     int64_t warps_needed = (m_cap + tpw - 1) / tpw;
-    int64_t blocks = (warps_needed + 3) / 4;
+    int64_t blocks = (warps_needed + SAMPLE_THREADS / 32 - 1) / (SAMPLE_THREADS / 32);
     int64_t cap = (int64_t)num_sms() * 16;
     if (blocks > cap) blocks = cap;
     if (blocks < 1) blocks = 1;
-    sample_update_kernel<<<(unsigned)blocks, 128, 0, (cudaStream_t)stream>>>(P);
+    sample_update_kernel<<<(unsigned)blocks, SAMPLE_THREADS, 0, (cudaStream_t)stream>>>(P);
     count_launch();
     return check_launch("sample_update");
 }

@@ -1,0 +1,199 @@
+// trace.cuh -- K6 fast closest-hit traversal for the ray-sampled refinement.
+//
+// Same result as the reference's _bvh_ray (geometry.py:331-392), whose own
+// contract is "traversal must agree with brute-force intersection"
+// (geometry.py:3-6): the closest fp64 Moller-Trumbore hit over ALL triangles,
+// t in [1e-12, t_max], ties -> smaller original id.  Only the *search* changes:
+//
+//   * boxes: fp32 slab tests on padded, outward-rounded child boxes stored in
+//     the parent (one 64 B node fetch tests both children).  The padding
+//     (1e-5 of the scene scale) is ~100x the fp32 rounding of the slab
+//     arithmetic, so a box holding a hit point at t <= t_best is never pruned;
+//   * triangles: an fp32 Moller-Trumbore pre-test with an a-priori rounding
+//     bound (tri_maybe) rejects only triangles the exact test must reject;
+//     every survivor is decided by the reference's exact fp64 test (ray_tri).
+//
+// Hence the visited set covers everything that can change the answer and
+// every accepted hit is the reference's bit-exact fp64 (t, id, facing).
+#pragma once
+#include "common.cuh"
+
+#define RTSDF_FAST_STACK 48
+
+namespace rtsdf {
+
+struct __align__(64) FastNode {
+    float lo0[3], hi0[3];  // child 0 box (padded, outward rounded)
+    float lo1[3], hi1[3];  // child 1 box
+    int32_t c0, c1;        // child refs: internal >= 0; leaf -(start * 8 + count) - 1
+    int32_t v0, v1;        // 1 = child present, 0 = none
+};
+static_assert(sizeof(FastNode) == 64, "fast node layout");
+
+struct __align__(16) FastTri {
+    float a[3];
+    float e1[3];
+    float e2[3];
+    float scale;  // |e1|_1 + |e2|_1 rounded up (rounding bound)
+    float pad_[2];
+};
+static_assert(sizeof(FastTri) == 48, "fast tri layout");
+
+struct FastBvh {
+    const FastNode* nodes;  // n_nodes + 1 entries; [n_nodes] = virtual parent of the root
+    const FastTri* tris;
+    const BvhTri* exact;    // fp64 triangles for ray_tri
+    int32_t root;
+};
+
+__host__ __device__ inline size_t fast_offset_nodes(int64_t n_nodes, int64_t n_tris) {
+    return (size_t)n_nodes * sizeof(BvhNode) + (size_t)n_tris * sizeof(BvhTri);
+}
+__host__ __device__ inline size_t fast_offset_tris(int64_t n_nodes, int64_t n_tris) {
+    return fast_offset_nodes(n_nodes, n_tris) + (size_t)(n_nodes + 1) * sizeof(FastNode);
+}
+
+__host__ __device__ inline FastBvh fast_bvh_view(const void* packed, int64_t n_nodes,
+                                                 int64_t n_tris) {
+    FastBvh f;
+    const char* p = (const char*)packed;
+    f.exact = (const BvhTri*)(p + (size_t)n_nodes * sizeof(BvhNode));
+    f.nodes = (const FastNode*)(p + fast_offset_nodes(n_nodes, n_tris));
+    f.tris = (const FastTri*)(p + fast_offset_tris(n_nodes, n_tris));
+    f.root = (int32_t)n_nodes;
+    return f;
+}
+
+struct RayF {
+    float ix, iy, iz;     // clamped reciprocal direction
+    float oix, oiy, oiz;  // origin * reciprocal
+};
+
+__device__ __forceinline__ float clamp_inv(double d) {
+    float f = (float)d;
+    if (fabsf(f) < 1e-30f) return d >= 0.0 ? 1e30f : -1e30f;
+    float r = 1.0f / f;
+    return fminf(fmaxf(r, -1e30f), 1e30f);
+}
+
+#define RTSDF_FINF __int_as_float(0x7f800000)
+
+// Padded child box slab test: entry t (>= 0) or +inf if missed / beyond t_best.
+__device__ __forceinline__ float box_entry(float lx, float ly, float lz, float hx, float hy,
+                                           float hz, const RayF& r, float t_best) {
+    float tx0 = fmaf(lx, r.ix, -r.oix), tx1 = fmaf(hx, r.ix, -r.oix);
+    float ty0 = fmaf(ly, r.iy, -r.oiy), ty1 = fmaf(hy, r.iy, -r.oiy);
+    float tz0 = fmaf(lz, r.iz, -r.oiz), tz1 = fmaf(hz, r.iz, -r.oiz);
+    float tmin = fmaxf(fmaxf(fminf(tx0, tx1), fminf(ty0, ty1)), fmaxf(fminf(tz0, tz1), 0.0f));
+    float tmax = fminf(fminf(fmaxf(tx0, tx1), fmaxf(ty0, ty1)), fmaxf(tz0, tz1));
+    return (tmin <= tmax && tmin <= t_best) ? tmin : RTSDF_FINF;
+}
+
+// fp32 Moller-Trumbore on un-normalised values with an a-priori error bound
+// eb >= |fp32 - exact| of det, U, V, W (inputs rounded to fp32, ~10 roundings,
+// padded ~4x).  Returns false only when the exact test must reject.
+__device__ __forceinline__ bool tri_maybe(const FastTri& tr, float tx, float ty, float tz,
+                                          float dx, float dy, float dz, float t_best) {
+    float px = __fsub_rn(__fmul_rn(dy, tr.e2[2]), __fmul_rn(dz, tr.e2[1]));
+    float py = __fsub_rn(__fmul_rn(dz, tr.e2[0]), __fmul_rn(dx, tr.e2[2]));
+    float pz = __fsub_rn(__fmul_rn(dx, tr.e2[1]), __fmul_rn(dy, tr.e2[0]));
+    float det = fmaf(tr.e1[0], px, fmaf(tr.e1[1], py, __fmul_rn(tr.e1[2], pz)));
+    float U = fmaf(tx, px, fmaf(ty, py, __fmul_rn(tz, pz)));
+    float qx = __fsub_rn(__fmul_rn(ty, tr.e1[2]), __fmul_rn(tz, tr.e1[1]));
+    float qy = __fsub_rn(__fmul_rn(tz, tr.e1[0]), __fmul_rn(tx, tr.e1[2]));
+    float qz = __fsub_rn(__fmul_rn(tx, tr.e1[1]), __fmul_rn(ty, tr.e1[0]));
+    float V = fmaf(dx, qx, fmaf(dy, qy, __fmul_rn(dz, qz)));
+    float W = fmaf(tr.e2[0], qx, fmaf(tr.e2[1], qy, __fmul_rn(tr.e2[2], qz)));
+    float tn = fabsf(tx) + fabsf(ty) + fabsf(tz);
+    float eb = 4e-6f * (tn + 1.0f) * tr.scale * (tr.scale + 1.0f);
+    float ad = fabsf(det);
+    if (!(ad > 4.0f * eb)) return true;  // ill-conditioned, tiny or NaN: exact test decides
+    float s = det > 0.0f ? 1.0f : -1.0f;
+    float Us = U * s, Vs = V * s, Ws = W * s;
+    if (Us < -eb || Vs < -eb || Ws < -eb) return false;
+    if (Us + Vs > ad + 3.0f * eb) return false;
+    if (Ws > t_best * (ad + eb) + eb * (1.0f + t_best)) return false;
+    return true;
+}
+
+// Closest hit, brute-force equivalent.  `stack` is this thread's slot in a
+// shared-memory stack with `stride` (= blockDim) between entries.
+__device__ __forceinline__ double trace_fast(const FastBvh& b, double ox, double oy, double oz,
+                                             double dx, double dy, double dz, double t_max,
+                                             int32_t* stack, int stride, int32_t& out_id,
+                                             int& out_facing) {
+    RayF r;
+    r.ix = clamp_inv(dx);
+    r.iy = clamp_inv(dy);
+    r.iz = clamp_inv(dz);
+    r.oix = (float)ox * r.ix;
+    r.oiy = (float)oy * r.iy;
+    r.oiz = (float)oz * r.iz;
+    const float fdx = (float)dx, fdy = (float)dy, fdz = (float)dz;
+    double best_t = t_max;
+    int32_t best_id = -1;
+    int best_facing = 0;
+    float tb = t_max < 3.0e38 ? __double2float_ru(t_max) : RTSDF_FINF;
+    int sp = 0;
+    int32_t node = b.root;
+    while (true) {
+        if (node >= 0) {  // internal: test both children, descend into the nearer
+            const FastNode* nd = b.nodes + node;
+            float4 a0 = __ldg((const float4*)&nd->lo0[0]);  // lo0 xyz, hi0 x
+            float4 a1 = __ldg((const float4*)&nd->hi0[1]);  // hi0 yz, lo1 xy
+            float4 a2 = __ldg((const float4*)&nd->lo1[2]);  // lo1 z, hi1 xyz
+            int4 cc = __ldg((const int4*)&nd->c0);
+            float t0 = cc.z ? box_entry(a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, r, tb) : RTSDF_FINF;
+            float t1 = cc.w ? box_entry(a1.z, a1.w, a2.x, a2.y, a2.z, a2.w, r, tb) : RTSDF_FINF;
+            bool h0 = t0 != RTSDF_FINF, h1 = t1 != RTSDF_FINF;
+            if (h0 && h1) {
+                bool first0 = t0 <= t1;
+                stack[(sp++) * stride] = first0 ? cc.y : cc.x;
+                node = first0 ? cc.x : cc.y;
+                continue;
+            }
+            if (h0 || h1) {
+                node = h0 ? cc.x : cc.y;
+                continue;
+            }
+        } else {  // leaf: fp32 pre-test, exact fp64 confirm
+            int32_t code = -node - 1;
+            int start = code >> 3, count = code & 7;
+            for (int k = start; k < start + count; ++k) {
+                const FastTri* ft = b.tris + k;
+                float4 f0 = __ldg((const float4*)&ft->a[0]);
+                float4 f1 = __ldg((const float4*)&ft->e1[1]);
+                float4 f2 = __ldg((const float4*)&ft->e2[2]);
+                FastTri tr;
+                tr.e1[0] = f0.w; tr.e1[1] = f1.x; tr.e1[2] = f1.y;
+                tr.e2[0] = f1.z; tr.e2[1] = f1.w; tr.e2[2] = f2.x;
+                tr.scale = f2.y;
+                const BvhTri* ex = b.exact + k;
+                // T = o - a in fp64 (exactly the reference's tx/ty/tz), rounded once
+                float tx = (float)(ox - __ldg(ex->a)), ty = (float)(oy - __ldg(ex->a + 1)),
+                      tz = (float)(oz - __ldg(ex->a + 2));
+                if (!tri_maybe(tr, tx, ty, tz, fdx, fdy, fdz, tb)) continue;
+                double t = ray_tri(ox, oy, oz, dx, dy, dz, ex);
+                if (t >= 0.0 && t <= best_t) {
+                    int32_t orig = __ldg(&ex->orig);
+                    if (t < best_t || best_id < 0 || orig < best_id) {
+                        best_t = t;
+                        best_id = orig;
+                        double dot = __dadd_rn(
+                            __dadd_rn(__dmul_rn(dx, __ldg(ex->n)), __dmul_rn(dy, __ldg(ex->n + 1))),
+                            __dmul_rn(dz, __ldg(ex->n + 2)));
+                        best_facing = dot < 0.0 ? 1 : 2;
+                        tb = __double2float_ru(best_t);
+                    }
+                }
+            }
+        }
+        if (sp == 0) break;
+        node = stack[(--sp) * stride];
+    }
+    out_id = best_id;
+    out_facing = best_facing;
+    return best_id < 0 ? -1.0 : best_t;
+}
+
+}  // namespace rtsdf

@@ -199,6 +199,8 @@ def build_bvh(mesh: TriangleMesh) -> BvhIndex:
     if n < 0:
         raise EmptyMeshError(L.rtsdf_last_error().decode())
     node_lo, node_hi, left, right = node_lo[:n].copy(), node_hi[:n].copy(), left[:n].copy(), right[:n].copy()
+    if tree_depth(left, right) >= 48:  # RTSDF_FAST_STACK (csrc/trace.cuh)
+        raise MeshError("BVH deeper than the traversal stack (48 levels)")
     a = np.ascontiguousarray(p0[order])
     e1 = np.ascontiguousarray(p1[order] - a)
     e2 = np.ascontiguousarray(p2[order] - a)
@@ -206,6 +208,17 @@ def build_bvh(mesh: TriangleMesh) -> BvhIndex:
     packed = upload_bvh(node_lo, node_hi, left, right, order, a, e1, e2, tn)
     return BvhIndex(mesh, node_lo, node_hi, left, right, order, a, e1, e2, tn, packed,
                     to_device(mesh.normals))
+
+
+def tree_depth(left: np.ndarray, right: np.ndarray) -> int:
+    """Number of levels of the flat tree (leaves: left < 0)."""
+    frontier = np.array([0], dtype=np.int64)
+    depth = 0
+    while len(frontier):
+        depth += 1
+        internal = frontier[left[frontier] >= 0]
+        frontier = np.concatenate([left[internal], right[internal]]).astype(np.int64)
+    return depth
 
 
 def upload_bvh(node_lo, node_hi, left, right, order, a, e1, e2, tn) -> torch.Tensor:
@@ -229,15 +242,20 @@ class RayHit:
     facing: int = FACING_NONE
 
 
-def ray_query_many(bvh: BvhIndex, origins, directions, t_max=np.inf):
-    """Batched closest-hit queries: (t, id, facing) arrays; t < 0 = miss."""
+def ray_query_many(bvh: BvhIndex, origins, directions, t_max=np.inf, fast=False):
+    """Batched closest-hit queries: (t, id, facing) arrays; t < 0 = miss.
+
+    fast=False: the reference's traversal order verbatim (fp64);
+    fast=True: the refinement's K6 search (brute-force-equivalent result).
+    """
     o = to_device(np.ascontiguousarray(origins, dtype=np.float64).reshape(-1, 3))
     d = to_device(np.ascontiguousarray(directions, dtype=np.float64).reshape(-1, 3))
     n = o.shape[0]
     t = torch.empty(n, dtype=torch.float64, device=o.device)
     ids = torch.empty(n, dtype=torch.int32, device=o.device)
     fac = torch.empty(n, dtype=torch.int32, device=o.device)
-    _lib.check(_lib.lib().rtsdf_ray_query(_lib.ptr(bvh.packed), bvh.num_nodes, _lib.ptr(o),
+    _lib.check(_lib.lib().rtsdf_ray_query(_lib.ptr(bvh.packed), bvh.num_nodes, len(bvh.order),
+                                          int(bool(fast)), _lib.ptr(o),
                                           _lib.ptr(d), n, float(t_max), _lib.ptr(t),
                                           _lib.ptr(ids), _lib.ptr(fac), _lib.stream()),
                "ray_query")

@@ -197,6 +197,43 @@ def test_bvh_closest_hits_match_reference(rt):
     np.testing.assert_array_equal(t, A["soup.ray_t"])
     hit = rt.ray_query(bvh, A["soup.ray_o"][0], A["soup.ray_d"][0])
     assert hit.hit == (A["soup.ray_id"][0] >= 0)
+    # the K6 search (fp32 conservative boxes + pre-test, fp64 confirm) == reference
+    t2, ids2, fac2 = rt.ray_query_many(bvh, A["soup.ray_o"], A["soup.ray_d"], fast=True)
+    np.testing.assert_array_equal(ids2, A["soup.ray_id"])
+    np.testing.assert_array_equal(fac2, A["soup.ray_facing"])
+    np.testing.assert_array_equal(t2, A["soup.ray_t"])
+
+
+@pytest.mark.parametrize("name", ["sphere_plane", "thin_plate", "soup"])
+def test_fast_traversal_equals_brute_force(rt, name):
+    """geometry.py:3-6 contract: traversal == brute-force closest (t, min id)."""
+    rng = np.random.default_rng(11)
+    if name == "soup":
+        A = golden_arrays()
+        mesh = rt.make_mesh(A["soup.vertices"], A["soup.triangles"])
+        lo, hi = np.zeros(3), np.ones(3)
+    else:
+        scene, mesh = scene_mesh(name)
+        lo, hi = scene.lo, scene.hi
+    bvh = rt.build_bvh(mesh)
+    n = 20000
+    o = rng.uniform(lo, hi, size=(n, 3))
+    d = rng.normal(size=(n, 3))
+    d /= np.linalg.norm(d, axis=1)[:, None]
+    # a slice of axis-aligned and grazing directions (degenerate slabs)
+    d[:500] = np.eye(3)[rng.integers(0, 3, 500)] * rng.choice([-1.0, 1.0], (500, 1))
+    t_max = float(np.linalg.norm(hi - lo))
+    tf, idf, ff = rt.ray_query_many(bvh, o, d, t_max, fast=True)
+    te, ide, fe = rt.ray_query_many(bvh, o, d, t_max, fast=False)
+    np.testing.assert_array_equal(idf, ide)
+    np.testing.assert_array_equal(tf, te)
+    np.testing.assert_array_equal(ff, fe)
+    # brute force over every triangle with the oracle's exact fp64 test
+    b1 = O.bvh_build(mesh.vertices, mesh.triangles, mesh.normals)
+    tb, ib, fb = O.ray_brute(b1, o, d, t_max)
+    np.testing.assert_array_equal(idf, ib)
+    np.testing.assert_array_equal(tf, tb)
+    np.testing.assert_array_equal(ff, fb)
 
 
 # ------------------------------------------------------------ ray sampling
