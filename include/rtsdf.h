@@ -91,6 +91,14 @@ int rtsdf_jfa_step_slab(const int32_t* local, const int32_t* halo_lo, const int3
 int rtsdf_jfa_run(int32_t* buf_a, int32_t* buf_b, int nx, int ny, int nz, double hx, double hy,
                   double hz, int wx, int wy, int wz, int* which, void* stream);
 
+/* Replaces pipeline.py:120-124 (run_jf = jfa_run + seeds_to_sdf): the full
+ * schedule ping-ponging buf_a (init seeds) / buf_b, with the last (k = 1) pass
+ * writing the f32 SDF straight into `out` (K3 fused: no seed grid round trip).
+ * Both seed buffers are clobbered.  empty_count as in rtsdf_seeds_to_sdf.   */
+int rtsdf_jfa_run_sdf(int32_t* buf_a, int32_t* buf_b, float* out, int nx, int ny, int nz,
+                      double hx, double hy, double hz, int wx, int wy, int wz, double beta,
+                      int64_t* empty_count, void* stream);
+
 /* Replaces jfa.py:224 (_seed_distance_kernel): out = f32(sqrt(d2_fp64) - beta).
  * empty_count (device int64, nullable) += EMPTY cells (NoSeedsError check,
  * jfa.py:176-177).  x0/nx_global: slab offset (0 / nx for a whole grid).    */
@@ -135,6 +143,14 @@ int rtsdf_compact_mask(const uint8_t* mask, int64_t n_cells, int32_t* block_coun
 int64_t rtsdf_bvh_build_host(const double* tri_lo, const double* tri_hi, int64_t n_tris,
                              double* node_lo, double* node_hi, int32_t* node_left,
                              int32_t* node_right, int32_t* order);
+/* Binned-SAH build (host) in the same flat format, for the K6 search only:
+ * that search returns the brute-force closest hit whatever the tree, so it may
+ * use a tree built for speed (replaces nothing in the reference; the
+ * reference-order traversal keeps using rtsdf_bvh_build_host's tree).
+ * max_leaf in 1..7.                                                         */
+int64_t rtsdf_bvh_build_sah_host(const double* tri_lo, const double* tri_hi, int64_t n_tris,
+                                 int max_leaf, double* node_lo, double* node_hi,
+                                 int32_t* node_left, int32_t* node_right, int32_t* order);
 /* Pack the flat BVH (device SoA as in BvhIndex, geometry.py:186-195) into the
  * device traversal layout: nodes (64 B each) and triangles (128 B each).    */
 size_t rtsdf_bvh_packed_bytes(int64_t n_nodes, int64_t n_tris);

@@ -44,6 +44,7 @@ SIGNATURES = {
     "rtsdf_jfa_step": (I, [P, P, I, I, I, I, D, D, D, I, I, I, P]),
     "rtsdf_jfa_step_slab": (I, [P, P, P, P, I, I, I, I, I, I, I, I, I, I, D, D, D, I, I, I, P]),
     "rtsdf_jfa_run": (I, [P, P, I, I, I, D, D, D, I, I, I, C.POINTER(I), P]),
+    "rtsdf_jfa_run_sdf": (I, [P, P, P, I, I, I, D, D, D, I, I, I, D, P, P]),
     "rtsdf_seeds_to_sdf": (I, [P, P, I, I, I, D, D, D, D, P, P]),
     "rtsdf_seeds_packed_to_linear": (I, [P, P, I, I, I, P]),
     "rtsdf_seeds_linear_to_packed": (I, [P, P, I, I, I, P]),
@@ -52,6 +53,7 @@ SIGNATURES = {
     "rtsdf_compact_ws_bytes": (SZ, [I64]),
     "rtsdf_compact_mask": (I, [P, I64, P, P, P, P, SZ, P]),
     "rtsdf_bvh_build_host": (I64, [P, P, I64, P, P, P, P, P]),
+    "rtsdf_bvh_build_sah_host": (I64, [P, P, I64, I, P, P, P, P, P]),
     "rtsdf_bvh_packed_bytes": (SZ, [I64, I64]),
     "rtsdf_bvh_pack": (I, [P, P, P, P, P, P, P, P, P, I64, I64, P, P]),
     "rtsdf_ray_query": (I, [P, I64, I64, I, P, P, I64, D, P, P, P, P]),

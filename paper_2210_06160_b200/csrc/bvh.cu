@@ -74,6 +74,136 @@ struct HostBuild {
     }
 };
 
+// Binned SAH build for the K6 search.  The fast traversal returns the
+// brute-force closest hit whatever the tree, so it is free to use a tree built
+// for speed: the reference's median split puts the ground quad's two
+// 3.1-unit triangles into leaves next to small sphere triangles (huge leaf
+// boxes every ray enters); SAH isolates them near the root.
+struct SahBuild {
+    const double* tri_lo;
+    const double* tri_hi;
+    std::vector<double> cen;
+    std::vector<double> nlo, nhi;
+    std::vector<int32_t> left, right;
+    std::vector<int32_t> order;
+    int max_leaf;
+
+    static double area(const double* lo, const double* hi) {
+        double dx = hi[0] - lo[0], dy = hi[1] - lo[1], dz = hi[2] - lo[2];
+        if (dx < 0 || dy < 0 || dz < 0) return 0.0;
+        return 2.0 * (dx * dy + dy * dz + dz * dx);
+    }
+
+    int32_t emit(const double* lo, const double* hi) {
+        int32_t me = (int32_t)left.size();
+        for (int a = 0; a < 3; ++a) {
+            nlo.push_back(lo[a]);
+            nhi.push_back(hi[a]);
+        }
+        left.push_back(0);
+        right.push_back(0);
+        return me;
+    }
+
+    void make_leaf(int32_t me, int64_t* idx, int64_t n) {
+        left[me] = -(int32_t)(order.size() + 1);
+        right[me] = (int32_t)n;
+        for (int64_t q = 0; q < n; ++q) order.push_back((int32_t)idx[q]);
+    }
+
+    int32_t build(int64_t* idx, int64_t n) {
+        double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+        double clo[3] = {INFINITY, INFINITY, INFINITY}, chi[3] = {-INFINITY, -INFINITY, -INFINITY};
+        for (int64_t q = 0; q < n; ++q)
+            for (int a = 0; a < 3; ++a) {
+                lo[a] = fmin(lo[a], tri_lo[3 * idx[q] + a]);
+                hi[a] = fmax(hi[a], tri_hi[3 * idx[q] + a]);
+                clo[a] = fmin(clo[a], cen[3 * idx[q] + a]);
+                chi[a] = fmax(chi[a], cen[3 * idx[q] + a]);
+            }
+        int32_t me = emit(lo, hi);
+        if (n <= 2) {
+            make_leaf(me, idx, n);
+            return me;
+        }
+        const int B = 32;
+        double best = INFINITY;
+        int best_axis = -1, best_bin = -1;
+        for (int a = 0; a < 3; ++a) {
+            double ext = chi[a] - clo[a];
+            if (!(ext > 0)) continue;
+            int64_t cnt[B] = {0};
+            double blo[B][3], bhi[B][3];
+            for (int b = 0; b < B; ++b)
+                for (int c = 0; c < 3; ++c) {
+                    blo[b][c] = INFINITY;
+                    bhi[b][c] = -INFINITY;
+                }
+            for (int64_t q = 0; q < n; ++q) {
+                int b = (int)((cen[3 * idx[q] + a] - clo[a]) / ext * B);
+                b = b < 0 ? 0 : (b >= B ? B - 1 : b);
+                cnt[b]++;
+                for (int c = 0; c < 3; ++c) {
+                    blo[b][c] = fmin(blo[b][c], tri_lo[3 * idx[q] + c]);
+                    bhi[b][c] = fmax(bhi[b][c], tri_hi[3 * idx[q] + c]);
+                }
+            }
+            double rarea[B];
+            int64_t rcnt[B];
+            double rl[3] = {INFINITY, INFINITY, INFINITY}, rh[3] = {-INFINITY, -INFINITY, -INFINITY};
+            int64_t rc = 0;
+            for (int b = B - 1; b >= 1; --b) {
+                for (int c = 0; c < 3; ++c) {
+                    rl[c] = fmin(rl[c], blo[b][c]);
+                    rh[c] = fmax(rh[c], bhi[b][c]);
+                }
+                rc += cnt[b];
+                rarea[b] = area(rl, rh);
+                rcnt[b] = rc;
+            }
+            double ll[3] = {INFINITY, INFINITY, INFINITY}, lh[3] = {-INFINITY, -INFINITY, -INFINITY};
+            int64_t lc = 0;
+            for (int b = 0; b < B - 1; ++b) {
+                for (int c = 0; c < 3; ++c) {
+                    ll[c] = fmin(ll[c], blo[b][c]);
+                    lh[c] = fmax(lh[c], bhi[b][c]);
+                }
+                lc += cnt[b];
+                if (lc == 0 || rcnt[b + 1] == 0) continue;
+                double cost = area(ll, lh) * lc + rarea[b + 1] * rcnt[b + 1];
+                if (cost < best) {
+                    best = cost;
+                    best_axis = a;
+                    best_bin = b;
+                }
+            }
+        }
+        double leaf_cost = area(lo, hi) * n;
+        if (n <= max_leaf && (best_axis < 0 || best >= leaf_cost)) {
+            make_leaf(me, idx, n);
+            return me;
+        }
+        int64_t mid;
+        if (best_axis < 0) {  // all centroids coincide: split the list in half
+            mid = n / 2;
+        } else {
+            double ext = chi[best_axis] - clo[best_axis];
+            int64_t* p = std::partition(idx, idx + n, [&](int64_t t) {
+                int b = (int)((cen[3 * t + best_axis] - clo[best_axis]) / ext * B);
+                b = b < 0 ? 0 : (b >= B ? B - 1 : b);
+                return b <= best_bin;
+            });
+            mid = p - idx;
+            if (mid == 0 || mid == n) mid = n / 2;
+        }
+        int32_t l = build(idx, mid);
+        int32_t r = build(idx + mid, n - mid);
+        left[me] = l;
+        right[me] = r;
+        return me;
+    }
+};
+
 __global__ void bvh_pack_kernel(const double* __restrict__ node_lo, const double* __restrict__ node_hi,
                                 const int32_t* __restrict__ node_left,
                                 const int32_t* __restrict__ node_right,
@@ -221,6 +351,36 @@ extern "C" int64_t rtsdf_bvh_build_host(const double* tri_lo, const double* tri_
     std::iota(idx.begin(), idx.end(), (int64_t)0);
     b.build(idx.data(), n_tris);
     return b.n_nodes;
+}
+
+extern "C" int64_t rtsdf_bvh_build_sah_host(const double* tri_lo, const double* tri_hi,
+                                            int64_t n_tris, int max_leaf, double* node_lo,
+                                            double* node_hi, int32_t* node_left,
+                                            int32_t* node_right, int32_t* order) {
+    if (n_tris < 1 || max_leaf < 1 || max_leaf > 7) {
+        set_error("bvh_build_sah: empty mesh or bad leaf size");
+        return -1;
+    }
+    SahBuild b;
+    b.tri_lo = tri_lo;
+    b.tri_hi = tri_hi;
+    b.max_leaf = max_leaf;
+    b.cen.resize((size_t)(3 * n_tris));
+    for (int64_t q = 0; q < 3 * n_tris; ++q) b.cen[q] = (tri_lo[q] + tri_hi[q]) * 0.5;
+    std::vector<int64_t> idx((size_t)n_tris);
+    std::iota(idx.begin(), idx.end(), (int64_t)0);
+    b.build(idx.data(), n_tris);
+    int64_t n = (int64_t)b.left.size();
+    if (n > 2 * n_tris) {
+        set_error("bvh_build_sah: node overflow");
+        return -1;
+    }
+    std::copy(b.nlo.begin(), b.nlo.end(), node_lo);
+    std::copy(b.nhi.begin(), b.nhi.end(), node_hi);
+    std::copy(b.left.begin(), b.left.end(), node_left);
+    std::copy(b.right.begin(), b.right.end(), node_right);
+    std::copy(b.order.begin(), b.order.end(), order);
+    return n;
 }
 
 extern "C" size_t rtsdf_bvh_packed_bytes(int64_t n_nodes, int64_t n_tris) {

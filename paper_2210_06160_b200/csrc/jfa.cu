@@ -184,6 +184,12 @@ __global__ void linear_to_packed_kernel(const int32_t* __restrict__ l, int32_t* 
     p[c] = pack_ijk((int)(s / nyz), (int)((s / nz) % ny), (int)(s % nz));
 }
 
+}  // namespace rtsdf
+
+#include "jfa2.cuh"
+
+namespace rtsdf {
+
 static bool dims_ok(int nx, int ny, int nz) {
     if (nx < 1 || ny < 1 || nz < 1 || nx > RTSDF_MAX_DIM || ny > RTSDF_MAX_DIM || nz > RTSDF_MAX_DIM) {
         set_error("dims (%d, %d, %d) outside 1..%d (packed 10:10:10 seeds)", nx, ny, nz, RTSDF_MAX_DIM);
@@ -192,13 +198,38 @@ static bool dims_ok(int nx, int ny, int nz) {
     return true;
 }
 
+// K2 v2 launch (INT mode): task decomposition of jfa2.cuh.
+template <bool FINAL, bool SLAB>
+static void launch_pass2(PlaneSrc s, int32_t* dst, float* dst_sdf, const JfaGeom& g, double beta,
+                         int64_t* empty_count, cudaStream_t st) {
+    const int k = g.offset;
+    const int chain_y = (g.ny + k - 1) / k;  // longest j chain
+    const int ry = chain_y >= 4 ? 4 : (chain_y >= 2 ? 2 : 1);
+    Jfa2Task T;
+    T.L = 8;
+    T.nzb = (g.nz + 31) / 32;
+    T.jres = k < g.ny ? k : g.ny;
+    T.jgroups = (chain_y + ry - 1) / ry;
+    T.ires = k < g.nxl ? k : g.nxl;
+    const int chain_x = (g.nxl + k - 1) / k;
+    T.isegs = (chain_x + T.L - 1) / T.L;
+    int64_t warps = (int64_t)T.nzb * T.jres * T.jgroups * T.ires * T.isegs;
+    unsigned blocks = (unsigned)((warps + 3) / 4);
+    if (ry == 4)
+        jfa_pass2_kernel<4, FINAL, SLAB><<<blocks, 128, 0, st>>>(s, dst, dst_sdf, g, T, beta, empty_count);
+    else if (ry == 2)
+        jfa_pass2_kernel<2, FINAL, SLAB><<<blocks, 128, 0, st>>>(s, dst, dst_sdf, g, T, beta, empty_count);
+    else
+        jfa_pass2_kernel<1, FINAL, SLAB><<<blocks, 128, 0, st>>>(s, dst, dst_sdf, g, T, beta, empty_count);
+}
+
 static int launch_step(PlaneSrc s, int32_t* dst, const JfaGeom& g, bool slab, cudaStream_t st) {
     dim3 block(32, 8, 1);
     dim3 grid((g.nz + 31) / 32, (g.ny + 7) / 8, g.nxl);
     bool int_mode = g.wx > 0 && g.wy > 0 && g.wz > 0;
     if (int_mode) {
-        if (slab) jfa_step_kernel<JFA_INT, true><<<grid, block, 0, st>>>(s, dst, g);
-        else jfa_step_kernel<JFA_INT, false><<<grid, block, 0, st>>>(s, dst, g);
+        if (slab) launch_pass2<false, true>(s, dst, nullptr, g, 0.0, nullptr, st);
+        else launch_pass2<false, false>(s, dst, nullptr, g, 0.0, nullptr, st);
     } else {
         if (slab) jfa_step_kernel<JFA_FP64, true><<<grid, block, 0, st>>>(s, dst, g);
         else jfa_step_kernel<JFA_FP64, false><<<grid, block, 0, st>>>(s, dst, g);
@@ -210,9 +241,10 @@ static int launch_step(PlaneSrc s, int32_t* dst, const JfaGeom& g, bool slab, cu
 static bool weights_ok(int nx, int ny, int nz, int wx, int wy, int wz) {
     if (wx == 0 && wy == 0 && wz == 0) return true;
     if (wx <= 0 || wy <= 0 || wz <= 0) return false;
+    // keys relative to |x|^2 span about 2 qmax plus the increments: keep 2 bits spare
     double qmax = (double)wx * (nx - 1) * (nx - 1) + (double)wy * (ny - 1) * (ny - 1) +
                   (double)wz * (nz - 1) * (nz - 1);
-    return qmax < 2147483647.0;
+    return qmax < 536870912.0;
 }
 
 }  // namespace rtsdf
@@ -278,6 +310,39 @@ extern "C" int rtsdf_jfa_run(int32_t* a, int32_t* b, int nx, int ny, int nz, dou
     }
     if (which) *which = w;
     return RTSDF_OK;
+}
+
+extern "C" int rtsdf_jfa_run_sdf(int32_t* a, int32_t* b, float* out, int nx, int ny, int nz,
+                                 double hx, double hy, double hz, int wx, int wy, int wz,
+                                 double beta, int64_t* empty_count, void* stream) {
+    if (!dims_ok(nx, ny, nz)) return RTSDF_ERR_DIMS;
+    if (!weights_ok(nx, ny, nz, wx, wy, wz)) {
+        set_error("jfa_run_sdf: bad weights");
+        return RTSDF_ERR_INVALID;
+    }
+    const bool int_mode = wx > 0 && wy > 0 && wz > 0;
+    int m = nx > ny ? nx : ny;
+    if (nz > m) m = nz;
+    int n = 1;
+    while (n < m) n *= 2;
+    int32_t* src = a;
+    int32_t* dst = b;
+    cudaStream_t st = (cudaStream_t)stream;
+    for (int off = n / 2; off >= 1; off /= 2) {
+        JfaGeom g{nx, ny, nz, 0, nx, 0, 0, 0, 0, off, hx, hy, hz, wx, wy, wz};
+        PlaneSrc s{src, nullptr, nullptr};
+        if (off == 1 && int_mode) {  // last pass writes the SDF directly (K3 fused)
+            launch_pass2<true, false>(s, nullptr, out, g, beta, empty_count, st);
+            count_launch();
+            return check_launch("jfa_run_sdf");
+        }
+        int rc = launch_step(s, dst, g, false, st);
+        if (rc) return rc;
+        int32_t* t = src;
+        src = dst;
+        dst = t;
+    }
+    return rtsdf_seeds_to_sdf(src, out, nx, ny, nz, hx, hy, hz, beta, empty_count, stream);
 }
 
 extern "C" int rtsdf_seeds_to_sdf(const int32_t* seed, float* out, int nx, int ny, int nz,

@@ -171,10 +171,17 @@ class BvhIndex:
     tri_n: np.ndarray
     packed: torch.Tensor = dc_field(repr=False, compare=False, default=None)
     normals_dev: torch.Tensor = dc_field(repr=False, compare=False, default=None)
+    # K6 search tree (binned SAH) in the packed device layout, and its node count
+    search: torch.Tensor = dc_field(repr=False, compare=False, default=None)
+    search_nodes: int = 0
 
     @property
     def num_nodes(self):
         return len(self.node_left)
+
+    @property
+    def num_tris(self):
+        return len(self.order)
 
 
 def build_bvh(mesh: TriangleMesh) -> BvhIndex:
@@ -206,8 +213,23 @@ def build_bvh(mesh: TriangleMesh) -> BvhIndex:
     e2 = np.ascontiguousarray(p2[order] - a)
     tn = np.ascontiguousarray(mesh.normals[order])
     packed = upload_bvh(node_lo, node_hi, left, right, order, a, e1, e2, tn)
+    # the K6 search tree (binned SAH): same triangles, any tree gives the same
+    # brute-force-equivalent closest hit (csrc/trace.cuh)
+    slo, shi = np.empty((cap, 3)), np.empty((cap, 3))
+    sl, sr = np.empty(cap, np.int32), np.empty(cap, np.int32)
+    so = np.empty(T, np.int32)
+    ns = L.rtsdf_bvh_build_sah_host(_lib.host_ptr(tri_lo), _lib.host_ptr(tri_hi), T, 4,
+                                    *[_lib.host_ptr(x) for x in (slo, shi, sl, sr, so)])
+    if ns < 0:
+        raise MeshError(L.rtsdf_last_error().decode())
+    slo, shi, sl, sr = slo[:ns], shi[:ns], sl[:ns], sr[:ns]
+    if tree_depth(sl, sr) >= 48:
+        raise MeshError("SAH BVH deeper than the traversal stack (48 levels)")
+    sa = np.ascontiguousarray(p0[so])
+    search = upload_bvh(slo, shi, sl, sr, so, sa, np.ascontiguousarray(p1[so] - sa),
+                        np.ascontiguousarray(p2[so] - sa), np.ascontiguousarray(mesh.normals[so]))
     return BvhIndex(mesh, node_lo, node_hi, left, right, order, a, e1, e2, tn, packed,
-                    to_device(mesh.normals))
+                    to_device(mesh.normals), search, int(ns))
 
 
 def tree_depth(left: np.ndarray, right: np.ndarray) -> int:
@@ -254,7 +276,8 @@ def ray_query_many(bvh: BvhIndex, origins, directions, t_max=np.inf, fast=False)
     t = torch.empty(n, dtype=torch.float64, device=o.device)
     ids = torch.empty(n, dtype=torch.int32, device=o.device)
     fac = torch.empty(n, dtype=torch.int32, device=o.device)
-    _lib.check(_lib.lib().rtsdf_ray_query(_lib.ptr(bvh.packed), bvh.num_nodes, len(bvh.order),
+    buf, nn = (bvh.search, bvh.search_nodes) if fast else (bvh.packed, bvh.num_nodes)
+    _lib.check(_lib.lib().rtsdf_ray_query(_lib.ptr(buf), nn, bvh.num_tris,
                                           int(bool(fast)), _lib.ptr(o),
                                           _lib.ptr(d), n, float(t_max), _lib.ptr(t),
                                           _lib.ptr(ids), _lib.ptr(fac), _lib.stream()),

@@ -98,7 +98,7 @@ def integer_weights(hx: float, hy: float, hz: float, dims: tuple) -> tuple:
     if max(w) > 4096:
         return (0, 0, 0)
     qmax = sum(wi * (n - 1) ** 2 for wi, n in zip(w, dims))
-    if qmax >= 2**31 - 1:
+    if qmax >= 2**29:  # csrc/jfa.cu weights_ok: relative keys need 2 spare bits
         return (0, 0, 0)
     return tuple(w)
 
@@ -167,6 +167,17 @@ def flood_inplace(a: torch.Tensor, b: torch.Tensor, h) -> torch.Tensor:
     return src
 
 
+def flood_to_sdf(a: torch.Tensor, b: torch.Tensor, out: torch.Tensor, h, beta=0.0,
+                 empty_count=None):
+    """Full schedule with seeds -> SDF fused into the last pass (a, b clobbered)."""
+    nx, ny, nz = a.shape
+    w = _weights(h, (nx, ny, nz))
+    _lib.check(_lib.lib().rtsdf_jfa_run_sdf(_lib.ptr(a), _lib.ptr(b), _lib.ptr(out), nx, ny, nz,
+                                            float(h[0]), float(h[1]), float(h[2]), *w,
+                                            float(beta), _lib.ptr(empty_count), _lib.stream()),
+               "jfa_run_sdf")
+
+
 def jfa_run(voxels) -> SeedGrid:
     """Full schedule over a voxel grid (jfa.py:140-145)."""
     seeds = jfa_init(voxels)
@@ -205,8 +216,17 @@ def default_beta(voxels_or_seeds) -> float:
 
 
 def jump_flood(voxels, beta: float = 0.0) -> DistanceField:
-    """North-star alias: jfa_run followed by seeds_to_sdf."""
-    return seeds_to_sdf(jfa_run(voxels), beta=beta)
+    """North-star name for jfa_run followed by seeds_to_sdf, fused on the device
+    (the last pass writes the SDF)."""
+    if beta < 0:
+        raise ValueError("beta must be >= 0")
+    seeds = jfa_init(voxels)
+    out = torch.empty(seeds.dims, dtype=torch.float32, device=seeds.packed.device)
+    empty = torch.zeros(1, dtype=torch.int64, device=out.device)
+    flood_to_sdf(seeds.packed, torch.empty_like(seeds.packed), out, seeds.cell_size, beta, empty)
+    if int(empty.item()) > 0:
+        raise NoSeedsError("seed grid incomplete: flood before converting")
+    return make_field(out, seeds.lo, seeds.hi, beta=beta)
 
 
 __all__ = ["EMPTY", "NoSeedsError", "SeedGrid", "jfa_init", "jfa_offsets", "jfa_step",

@@ -187,8 +187,7 @@ class FramePipeline:
 
         # JF: full schedule (K2) + seeds -> SDF (K3)
         h = vox.cell_size
-        seeds = _jfa.flood_inplace(b["seed_a"], b["seed_b"], h)
-        _jfa.launch_seeds_to_sdf(seeds, b["coarse"], h, cfg.beta)
+        _jfa.flood_to_sdf(b["seed_a"], b["seed_b"], b["coarse"], h, cfg.beta)
         self.coarse = DistanceField(b["coarse"], np.asarray(lo, np.float64), np.asarray(hi, np.float64),
                                     beta=cfg.beta)
         if self.fine is None:

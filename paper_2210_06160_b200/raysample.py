@@ -160,7 +160,7 @@ def launch_sample_update(bvh: BvhIndex, g: _RsGeom, cb: CompactBuffers, params: 
     desc = g.desc()
     samp = samp or (None, None, None)
     _lib.check(_lib.lib().rtsdf_sample_update(
-        _lib.ptr(bvh.packed), bvh.num_nodes, len(bvh.order), _lib.ptr(cb.idx), _lib.ptr(cb.count),
+        _lib.ptr(bvh.search), bvh.search_nodes, bvh.num_tris, _lib.ptr(cb.idx), _lib.ptr(cb.count),
         int(m_cap if m_cap is not None else cb.n), desc, int(params.rays_per_frame),
         int(params.seed) & 0xFFFFFFFFFFFFFFFF, int(frame), float(t_max), _lib.ptr(dirs),
         _lib.ptr(samp[0]), _lib.ptr(samp[1]), _lib.ptr(samp[2]),

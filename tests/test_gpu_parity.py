@@ -135,6 +135,20 @@ def test_jfa_golden_c3_and_sp128(rt):
         assert digest(_np(rt.seeds_to_sdf(seeds).data)) == G[ck]["coarse"]
 
 
+@pytest.mark.parametrize("name,dims,beta", [("sphere", (64, 64, 64), 0.0),
+                                            ("sphere_plane", (400, 200, 400), 0.0),
+                                            ("sphere_plane", (128, 96, 80), 0.02),
+                                            ("thin_plate", (96, 80, 112), 0.0)])
+def test_jump_flood_fused_sdf(rt, name, dims, beta):
+    """jump_flood (last pass writes the SDF) == jfa_run + seeds_to_sdf on the oracle."""
+    scene, mesh = scene_mesh(name)
+    occ = O.voxelize(mesh.vertices, mesh.triangles, dims, scene.bounds)
+    h = (scene.hi - scene.lo) / np.array(dims, dtype=np.float64)
+    want = O.seeds_to_sdf(O.jfa_run(occ, h), h, beta)
+    got = rt.jump_flood(rt.voxelize(mesh, dims, scene.bounds), beta=beta)
+    np.testing.assert_array_equal(_np(got.data), want)
+
+
 def test_jfa_errors(rt):
     occ = np.zeros((8, 8, 8), np.uint8)
     vg = rt.VoxelGrid(rt._device.to_device(occ), np.zeros(3), np.ones(3))
