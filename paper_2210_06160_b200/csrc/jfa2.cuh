@@ -74,27 +74,44 @@ __global__ void __launch_bounds__(128) jfa_pass2_kernel(PlaneSrc src, int32_t* _
             W[s][b] = RTSDF_EMPTY;
         }
 
+    // the (RY + 2) x 3 taps of one plane, loaded as independent (predicated)
+    // loads; the next plane is fetched while the current one is folded in
+    int32_t cur[RY + 2][3], nxt[RY + 2][3];
+    auto load_plane = [&](int a, int32_t (&vals)[RY + 2][3]) {
+        const int pi = i_first + a * k;
+        const int32_t* pl = nullptr;
+        if (pi >= 0 && pi < g.nx && a <= L)
+            pl = SLAB ? plane_ptr(src, g, pi, plane) : src.local + (int64_t)pi * plane;
+#pragma unroll
+        for (int bt = -1; bt <= RY; ++bt) {
+            const int tj = j_base + bt * k;
+            const bool rok = pl != nullptr && tj >= 0 && tj < g.ny && zok;
+#pragma unroll
+            for (int c = -1; c <= 1; ++c) {
+                const int tz = z + c * k;
+                vals[bt + 1][c + 1] = (rok && tz >= 0 && tz < g.nz)
+                                          ? __ldg(pl + (int64_t)tj * g.nz + tz)
+                                          : RTSDF_EMPTY;
+            }
+        }
+    };
+    load_plane(-1, cur);
+
     int empties = 0;
     // tap planes a = -1 .. L; after plane a, output a - 1 is complete
     for (int a = -1; a <= L; ++a) {
         const int pi = i_first + a * k;        // tap plane (global)
         if (a >= 1 && i_first + (a - 1) * k >= i_end) break;  // no further outputs
+        load_plane(a + 1, nxt);
         const int cx = -2 * g.wx * pi;
-        const int32_t* pl = nullptr;
-        if (pi >= 0 && pi < g.nx)
-            pl = SLAB ? plane_ptr(src, g, pi, plane) : src.local + (int64_t)pi * plane;
-        if (pl != nullptr) {
+        {
 #pragma unroll
             for (int bt = -1; bt <= RY; ++bt) {
                 const int tj = j_base + bt * k;
-                if (tj < 0 || tj >= g.ny) continue;
                 const int cy = -2 * g.wy * tj;
-                const int32_t* row = pl + (int64_t)tj * g.nz;
 #pragma unroll
                 for (int c = -1; c <= 1; ++c) {
-                    const int tz = z + c * k;
-                    int32_t v = RTSDF_EMPTY;
-                    if (zok && tz >= 0 && tz < g.nz) v = __ldg(row + tz);
+                    const int32_t v = cur[bt + 1][c + 1];
                     if (v == RTSDF_EMPTY) continue;
                     const int sx = unpack_i(v), sy = unpack_j(v), sk = unpack_k(v);
                     // B = Key at (tap plane, tap row, this lane's z)
@@ -146,6 +163,10 @@ __global__ void __launch_bounds__(128) jfa_pass2_kernel(PlaneSrc src, int32_t* _
             Km[2][b] = 0x7fffffff;
             W[2][b] = RTSDF_EMPTY;
         }
+#pragma unroll
+        for (int bt = 0; bt < RY + 2; ++bt)
+#pragma unroll
+            for (int c = 0; c < 3; ++c) cur[bt][c] = nxt[bt][c];
     }
     if (FINAL && empty_count) {
         for (int o = 16; o; o >>= 1) empties += __shfl_xor_sync(0xffffffffu, empties, o);
