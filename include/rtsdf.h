@@ -73,7 +73,11 @@ int rtsdf_jfa_init(const uint8_t* occ, int nx, int ny, int nz, int32_t* seed_pac
  * q = wx dx^2 + wy dy^2 + wz dz^2 and evaluates fp64 d2 only on integer ties.
  * (0, 0, 0) = general fp64 path.                                            */
 int rtsdf_jfa_step(const int32_t* src, int32_t* dst, int nx, int ny, int nz, int offset,
-                   double hx, double hy, double hz, int wx, int wy, int wz, void* stream);
+                   double hx, double hy, double hz, int wx, int wy, int wz, void* ws,
+                   size_t ws_bytes, void* stream);
+/* Workspace of the JFA entry points: the integer-tie fix-up list (a device
+ * counter + one int32 slot per cell of the grid / slab).                    */
+size_t rtsdf_jfa_ws_bytes(int nx, int ny, int nz);
 
 /* Slab form for z-slab (outer-axis) sharding across GPUs: this rank owns global
  * planes [x0, x0 + nxl) of an nx-plane grid in `local`; halo_lo holds global
@@ -83,13 +87,15 @@ int rtsdf_jfa_step(const int32_t* src, int32_t* dst, int nx, int ny, int nz, int
 int rtsdf_jfa_step_slab(const int32_t* local, const int32_t* halo_lo, const int32_t* halo_hi,
                         int32_t* dst, int nx, int x0, int nxl, int lo_first, int n_lo,
                         int hi_first, int n_hi, int ny, int nz, int offset, double hx,
-                        double hy, double hz, int wx, int wy, int wz, void* stream);
+                        double hy, double hz, int wx, int wy, int wz, void* ws,
+                        size_t ws_bytes, void* stream);
 
 /* Replaces jfa.py:140-145 (jfa_run's pass loop): runs the whole schedule
  * n/2 .. 1 ping-ponging between buf_a (holding the init seeds) and buf_b.
  * *which (host) = 0 if the result is in buf_a, 1 if in buf_b.               */
 int rtsdf_jfa_run(int32_t* buf_a, int32_t* buf_b, int nx, int ny, int nz, double hx, double hy,
-                  double hz, int wx, int wy, int wz, int* which, void* stream);
+                  double hz, int wx, int wy, int wz, int* which, void* ws, size_t ws_bytes,
+                  void* stream);
 
 /* Replaces pipeline.py:120-124 (run_jf = jfa_run + seeds_to_sdf): the full
  * schedule ping-ponging buf_a (init seeds) / buf_b, with the last (k = 1) pass
@@ -97,7 +103,7 @@ int rtsdf_jfa_run(int32_t* buf_a, int32_t* buf_b, int nx, int ny, int nz, double
  * Both seed buffers are clobbered.  empty_count as in rtsdf_seeds_to_sdf.   */
 int rtsdf_jfa_run_sdf(int32_t* buf_a, int32_t* buf_b, float* out, int nx, int ny, int nz,
                       double hx, double hy, double hz, int wx, int wy, int wz, double beta,
-                      int64_t* empty_count, void* stream);
+                      int64_t* empty_count, void* ws, size_t ws_bytes, void* stream);
 
 /* Replaces jfa.py:224 (_seed_distance_kernel): out = f32(sqrt(d2_fp64) - beta).
  * empty_count (device int64, nullable) += EMPTY cells (NoSeedsError check,

@@ -41,10 +41,12 @@ SIGNATURES = {
     "rtsdf_voxelize_ws_bytes": (SZ, [I64]),
     "rtsdf_voxelize": (I, [P, I64, P, I64, DP, DP, I, I, I, P, P, P, P, P, SZ, P]),
     "rtsdf_jfa_init": (I, [P, I, I, I, P, P, P]),
-    "rtsdf_jfa_step": (I, [P, P, I, I, I, I, D, D, D, I, I, I, P]),
-    "rtsdf_jfa_step_slab": (I, [P, P, P, P, I, I, I, I, I, I, I, I, I, I, D, D, D, I, I, I, P]),
-    "rtsdf_jfa_run": (I, [P, P, I, I, I, D, D, D, I, I, I, C.POINTER(I), P]),
-    "rtsdf_jfa_run_sdf": (I, [P, P, P, I, I, I, D, D, D, I, I, I, D, P, P]),
+    "rtsdf_jfa_ws_bytes": (SZ, [I, I, I]),
+    "rtsdf_jfa_step": (I, [P, P, I, I, I, I, D, D, D, I, I, I, P, SZ, P]),
+    "rtsdf_jfa_step_slab": (I, [P, P, P, P, I, I, I, I, I, I, I, I, I, I, D, D, D, I, I, I, P, SZ,
+                                P]),
+    "rtsdf_jfa_run": (I, [P, P, I, I, I, D, D, D, I, I, I, C.POINTER(I), P, SZ, P]),
+    "rtsdf_jfa_run_sdf": (I, [P, P, P, I, I, I, D, D, D, I, I, I, D, P, P, SZ, P]),
     "rtsdf_seeds_to_sdf": (I, [P, P, I, I, I, D, D, D, D, P, P]),
     "rtsdf_seeds_packed_to_linear": (I, [P, P, I, I, I, P]),
     "rtsdf_seeds_linear_to_packed": (I, [P, P, I, I, I, P]),

@@ -198,10 +198,19 @@ static bool dims_ok(int nx, int ny, int nz) {
     return true;
 }
 
-// K2 v2 launch (INT mode): task decomposition of jfa2.cuh.
+// K2 v2 launch (INT mode): task decomposition of jfa2.cuh, then the exact
+// re-decision of the (rare) integer-tie cells the pass flagged.
+static JfaFixList fix_list(void* ws, int64_t n_cells) {
+    JfaFixList f;
+    f.count = (int64_t*)ws;
+    f.cells = (int32_t*)((char*)ws + 256);
+    f.cap = n_cells;
+    return f;
+}
+
 template <bool FINAL, bool SLAB>
 static void launch_pass2(PlaneSrc s, int32_t* dst, float* dst_sdf, const JfaGeom& g, double beta,
-                         int64_t* empty_count, cudaStream_t st) {
+                         int64_t* empty_count, void* ws, cudaStream_t st) {
     const int k = g.offset;
     const int chain_y = (g.ny + k - 1) / k;  // longest j chain
     const int ry = chain_y >= 4 ? 4 : (chain_y >= 2 ? 2 : 1);
@@ -213,28 +222,33 @@ static void launch_pass2(PlaneSrc s, int32_t* dst, float* dst_sdf, const JfaGeom
     T.ires = k < g.nxl ? k : g.nxl;
     const int chain_x = (g.nxl + k - 1) / k;
     T.isegs = (chain_x + T.L - 1) / T.L;
+    JfaFixList fix = fix_list(ws, (int64_t)g.nxl * g.ny * g.nz);
+    cudaMemsetAsync(fix.count, 0, sizeof(int64_t), st);
     int64_t warps = (int64_t)T.nzb * T.jres * T.jgroups * T.ires * T.isegs;
     unsigned blocks = (unsigned)((warps + 3) / 4);
     if (ry == 4)
-        jfa_pass2_kernel<4, FINAL, SLAB><<<blocks, 128, 0, st>>>(s, dst, dst_sdf, g, T, beta, empty_count);
+        jfa_pass2_kernel<4, FINAL, SLAB><<<blocks, 128, 0, st>>>(s, dst, dst_sdf, g, T, beta, empty_count, fix);
     else if (ry == 2)
-        jfa_pass2_kernel<2, FINAL, SLAB><<<blocks, 128, 0, st>>>(s, dst, dst_sdf, g, T, beta, empty_count);
+        jfa_pass2_kernel<2, FINAL, SLAB><<<blocks, 128, 0, st>>>(s, dst, dst_sdf, g, T, beta, empty_count, fix);
     else
-        jfa_pass2_kernel<1, FINAL, SLAB><<<blocks, 128, 0, st>>>(s, dst, dst_sdf, g, T, beta, empty_count);
+        jfa_pass2_kernel<1, FINAL, SLAB><<<blocks, 128, 0, st>>>(s, dst, dst_sdf, g, T, beta, empty_count, fix);
+    jfa_fixup_kernel<FINAL, SLAB><<<(unsigned)(num_sms() * 4), 128, 0, st>>>(s, dst, dst_sdf, g, beta, fix);
+    count_launch(2);
 }
 
-static int launch_step(PlaneSrc s, int32_t* dst, const JfaGeom& g, bool slab, cudaStream_t st) {
+static int launch_step(PlaneSrc s, int32_t* dst, const JfaGeom& g, bool slab, void* ws,
+                       cudaStream_t st) {
     dim3 block(32, 8, 1);
     dim3 grid((g.nz + 31) / 32, (g.ny + 7) / 8, g.nxl);
     bool int_mode = g.wx > 0 && g.wy > 0 && g.wz > 0;
     if (int_mode) {
-        if (slab) launch_pass2<false, true>(s, dst, nullptr, g, 0.0, nullptr, st);
-        else launch_pass2<false, false>(s, dst, nullptr, g, 0.0, nullptr, st);
+        if (slab) launch_pass2<false, true>(s, dst, nullptr, g, 0.0, nullptr, ws, st);
+        else launch_pass2<false, false>(s, dst, nullptr, g, 0.0, nullptr, ws, st);
     } else {
         if (slab) jfa_step_kernel<JFA_FP64, true><<<grid, block, 0, st>>>(s, dst, g);
         else jfa_step_kernel<JFA_FP64, false><<<grid, block, 0, st>>>(s, dst, g);
+        count_launch();
     }
-    count_launch();
     return check_launch("jfa_step");
 }
 
@@ -247,9 +261,21 @@ static bool weights_ok(int nx, int ny, int nz, int wx, int wy, int wz) {
     return qmax < 536870912.0;
 }
 
+static bool ws_ok(void* ws, size_t ws_bytes, int64_t n_cells) {
+    if (!ws || ws_bytes < 256 + (size_t)n_cells * sizeof(int32_t)) {
+        set_error("jfa: workspace too small (rtsdf_jfa_ws_bytes)");
+        return false;
+    }
+    return true;
+}
+
 }  // namespace rtsdf
 
 using namespace rtsdf;
+
+extern "C" size_t rtsdf_jfa_ws_bytes(int nx, int ny, int nz) {
+    return 256 + (size_t)nx * ny * nz * sizeof(int32_t);
+}
 
 extern "C" int rtsdf_jfa_init(const uint8_t* occ, int nx, int ny, int nz, int32_t* seed,
                               int64_t* count, void* stream) {
@@ -263,35 +289,37 @@ extern "C" int rtsdf_jfa_init(const uint8_t* occ, int nx, int ny, int nz, int32_
 
 extern "C" int rtsdf_jfa_step(const int32_t* src, int32_t* dst, int nx, int ny, int nz,
                               int offset, double hx, double hy, double hz, int wx, int wy,
-                              int wz, void* stream) {
+                              int wz, void* ws, size_t ws_bytes, void* stream) {
     if (!dims_ok(nx, ny, nz)) return RTSDF_ERR_DIMS;
     if (offset < 1 || !weights_ok(nx, ny, nz, wx, wy, wz)) {
         set_error("jfa_step: bad offset %d or weights (%d,%d,%d)", offset, wx, wy, wz);
         return RTSDF_ERR_INVALID;
     }
+    if (!ws_ok(ws, ws_bytes, (int64_t)nx * ny * nz)) return RTSDF_ERR_WORKSPACE;
     JfaGeom g{nx, ny, nz, 0, nx, 0, 0, 0, 0, offset, hx, hy, hz, wx, wy, wz};
     PlaneSrc s{src, nullptr, nullptr};
-    return launch_step(s, dst, g, false, (cudaStream_t)stream);
+    return launch_step(s, dst, g, false, ws, (cudaStream_t)stream);
 }
 
 extern "C" int rtsdf_jfa_step_slab(const int32_t* local, const int32_t* halo_lo,
                                    const int32_t* halo_hi, int32_t* dst, int nx, int x0, int nxl,
                                    int lo_first, int n_lo, int hi_first, int n_hi, int ny, int nz,
                                    int offset, double hx, double hy, double hz, int wx, int wy,
-                                   int wz, void* stream) {
+                                   int wz, void* ws, size_t ws_bytes, void* stream) {
     if (!dims_ok(nx, ny, nz)) return RTSDF_ERR_DIMS;
     if (offset < 1 || nxl < 1 || x0 < 0 || x0 + nxl > nx || !weights_ok(nx, ny, nz, wx, wy, wz)) {
         set_error("jfa_step_slab: bad slab/offset/weights");
         return RTSDF_ERR_INVALID;
     }
+    if (!ws_ok(ws, ws_bytes, (int64_t)nxl * ny * nz)) return RTSDF_ERR_WORKSPACE;
     JfaGeom g{nx, ny, nz, x0, nxl, lo_first, n_lo, hi_first, n_hi, offset, hx, hy, hz, wx, wy, wz};
     PlaneSrc s{local, halo_lo, halo_hi};
-    return launch_step(s, dst, g, true, (cudaStream_t)stream);
+    return launch_step(s, dst, g, true, ws, (cudaStream_t)stream);
 }
 
 extern "C" int rtsdf_jfa_run(int32_t* a, int32_t* b, int nx, int ny, int nz, double hx,
-                             double hy, double hz, int wx, int wy, int wz, int* which,
-                             void* stream) {
+                             double hy, double hz, int wx, int wy, int wz, int* which, void* ws,
+                             size_t ws_bytes, void* stream) {
     if (!dims_ok(nx, ny, nz)) return RTSDF_ERR_DIMS;
     int m = nx > ny ? nx : ny;
     if (nz > m) m = nz;
@@ -301,7 +329,8 @@ extern "C" int rtsdf_jfa_run(int32_t* a, int32_t* b, int nx, int ny, int nz, dou
     int32_t* dst = b;
     int w = 0;
     for (int off = n / 2; off >= 1; off /= 2) {
-        int rc = rtsdf_jfa_step(src, dst, nx, ny, nz, off, hx, hy, hz, wx, wy, wz, stream);
+        int rc = rtsdf_jfa_step(src, dst, nx, ny, nz, off, hx, hy, hz, wx, wy, wz, ws, ws_bytes,
+                                stream);
         if (rc) return rc;
         int32_t* t = src;
         src = dst;
@@ -314,12 +343,14 @@ extern "C" int rtsdf_jfa_run(int32_t* a, int32_t* b, int nx, int ny, int nz, dou
 
 extern "C" int rtsdf_jfa_run_sdf(int32_t* a, int32_t* b, float* out, int nx, int ny, int nz,
                                  double hx, double hy, double hz, int wx, int wy, int wz,
-                                 double beta, int64_t* empty_count, void* stream) {
+                                 double beta, int64_t* empty_count, void* ws, size_t ws_bytes,
+                                 void* stream) {
     if (!dims_ok(nx, ny, nz)) return RTSDF_ERR_DIMS;
     if (!weights_ok(nx, ny, nz, wx, wy, wz)) {
         set_error("jfa_run_sdf: bad weights");
         return RTSDF_ERR_INVALID;
     }
+    if (!ws_ok(ws, ws_bytes, (int64_t)nx * ny * nz)) return RTSDF_ERR_WORKSPACE;
     const bool int_mode = wx > 0 && wy > 0 && wz > 0;
     int m = nx > ny ? nx : ny;
     if (nz > m) m = nz;
@@ -332,11 +363,10 @@ extern "C" int rtsdf_jfa_run_sdf(int32_t* a, int32_t* b, float* out, int nx, int
         JfaGeom g{nx, ny, nz, 0, nx, 0, 0, 0, 0, off, hx, hy, hz, wx, wy, wz};
         PlaneSrc s{src, nullptr, nullptr};
         if (off == 1 && int_mode) {  // last pass writes the SDF directly (K3 fused)
-            launch_pass2<true, false>(s, nullptr, out, g, beta, empty_count, st);
-            count_launch();
+            launch_pass2<true, false>(s, nullptr, out, g, beta, empty_count, ws, st);
             return check_launch("jfa_run_sdf");
         }
-        int rc = launch_step(s, dst, g, false, st);
+        int rc = launch_step(s, dst, g, false, ws, st);
         if (rc) return rc;
         int32_t* t = src;
         src = dst;

@@ -6,18 +6,24 @@
 // j0, j0 + k, ..., j0 + (RY-1)k x a segment of L planes i0, i0 + k, ...,
 // i0 + (L-1)k of one residue class.  With offset k every tap of an output in
 // the unit is itself on the unit's lattice (or its one-step halo), so each
-// plane of (RY + 2) x 3 taps is loaded ONCE and folded into every output that
-// sees it: 3 planes in flight x RY rows.
+// plane of (RY + 2) x 3 taps is loaded ONCE (as independent loads, the next
+// plane in flight while the current one is folded in) and folded into every
+// output that sees it: 3 planes in flight x RY rows.
 //
 // For a loaded seed s at tap plane a / tap row bt, the key of output (a', b')
 //     Key = |s|^2_w - 2 w . (x * s) = q(s, x) - |x|^2_w
 // is B - (a' - a) Gx - (b' - bt) Gy with B, Gx = 2 wx k si, Gy = 2 wy k sj
-// computed once per value: every candidate costs one IADD3 plus the compare.
-// The minimum integer key is the reference's fp64 minimum; an integer tie
-// between different seeds (a few % of cells in the late passes) takes a rare
-// branch that applies the reference's fp64 rule (jfa.py:116-124) in place.
+// computed once per value: every candidate costs one IADD plus a compare and
+// two selects.  The minimum integer key is the reference's fp64 minimum.  An
+// integer tie between two DIFFERENT seeds (a few % of cells in the late
+// passes) only sets a per-output flag; flagged cells are appended to a list
+// and re-decided by jfa_fixup_kernel with the reference's own rule
+// (fp64 d2, then lexicographic; jfa.py:108-124), so the hot loop has no fp64
+// and no divergent branch.
 #pragma once
 #include "common.cuh"
+
+#define JFA2_EMPTY_KEY (1 << 30)  // larger than any real key (|key| < 2^29)
 
 namespace rtsdf {
 
@@ -25,23 +31,18 @@ struct Jfa2Task {
     int nzb, jres, jgroups, ires, isegs, L;
 };
 
-__device__ __forceinline__ void jfa2_consider(int K, int32_t v, int& Km, int32_t& W, int oi,
-                                              int oj, int oz, double hx, double hy, double hz) {
-    if (K < Km) {
-        Km = K;
-        W = v;
-    } else if (K == Km && v != W) {  // rare: integer tie between distinct seeds
-        double dv = center_d2(oi - unpack_i(v), oj - unpack_j(v), oz - unpack_k(v), hx, hy, hz);
-        double dw = center_d2(oi - unpack_i(W), oj - unpack_j(W), oz - unpack_k(W), hx, hy, hz);
-        if (dv < dw || (dv == dw && v < W)) W = v;
-    }
-}
+struct JfaFixList {
+    int32_t* cells;  // local linear cell indices needing the exact rule
+    int64_t* count;  // device counter
+    int64_t cap;
+};
 
 template <int RY, bool FINAL, bool SLAB>
 __global__ void __launch_bounds__(128) jfa_pass2_kernel(PlaneSrc src, int32_t* __restrict__ dst,
                                                         float* __restrict__ dst_sdf, JfaGeom g,
                                                         Jfa2Task T, double beta,
-                                                        int64_t* __restrict__ empty_count) {
+                                                        int64_t* __restrict__ empty_count,
+                                                        JfaFixList fix) {
     const int lane = threadIdx.x & 31;
     int64_t t = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t total = (int64_t)T.nzb * T.jres * T.jgroups * T.ires * T.isegs;
@@ -66,18 +67,18 @@ __global__ void __launch_bounds__(128) jfa_pass2_kernel(PlaneSrc src, int32_t* _
 
     int Km[3][RY];
     int32_t W[3][RY];
+    bool tie[3][RY];
 #pragma unroll
     for (int s = 0; s < 3; ++s)
 #pragma unroll
         for (int b = 0; b < RY; ++b) {
             Km[s][b] = 0x7fffffff;
             W[s][b] = RTSDF_EMPTY;
+            tie[s][b] = false;
         }
 
-    // the (RY + 2) x 3 taps of one plane, loaded as independent (predicated)
-    // loads; the next plane is fetched while the current one is folded in
     int32_t cur[RY + 2][3], nxt[RY + 2][3];
-    auto load_plane = [&](int a, int32_t (&vals)[RY + 2][3]) {
+    auto load_plane = [&](int a, int32_t(&vals)[RY + 2][3]) {
         const int pi = i_first + a * k;
         const int32_t* pl = nullptr;
         if (pi >= 0 && pi < g.nx && a <= L)
@@ -100,36 +101,36 @@ __global__ void __launch_bounds__(128) jfa_pass2_kernel(PlaneSrc src, int32_t* _
     int empties = 0;
     // tap planes a = -1 .. L; after plane a, output a - 1 is complete
     for (int a = -1; a <= L; ++a) {
-        const int pi = i_first + a * k;        // tap plane (global)
-        if (a >= 1 && i_first + (a - 1) * k >= i_end) break;  // no further outputs
+        if (a >= 1 && i_first + (a - 1) * k >= i_end) break;  // no further outputs (uniform)
         load_plane(a + 1, nxt);
-        const int cx = -2 * g.wx * pi;
-        {
+        const int cx = -2 * g.wx * (i_first + a * k);
 #pragma unroll
-            for (int bt = -1; bt <= RY; ++bt) {
-                const int tj = j_base + bt * k;
-                const int cy = -2 * g.wy * tj;
+        for (int bt = -1; bt <= RY; ++bt) {
+            const int cy = -2 * g.wy * (j_base + bt * k);
 #pragma unroll
-                for (int c = -1; c <= 1; ++c) {
-                    const int32_t v = cur[bt + 1][c + 1];
-                    if (v == RTSDF_EMPTY) continue;
-                    const int sx = unpack_i(v), sy = unpack_j(v), sk = unpack_k(v);
-                    // B = Key at (tap plane, tap row, this lane's z)
-                    const int B = sx * (g.wx * sx + cx) + sy * (g.wy * sy + cy) + sk * (g.wz * sk + cz);
-                    const int Gx = gxk * sx, Gy = gyk * sy;
+            for (int c = -1; c <= 1; ++c) {
+                const int32_t v = cur[bt + 1][c + 1];
+                if (__all_sync(0xffffffffu, v == RTSDF_EMPTY)) continue;  // warp-uniform skip
+                const bool ok = v != RTSDF_EMPTY;
+                const int sx = unpack_i(v), sy = unpack_j(v), sk = unpack_k(v);
+                const int B0 = sx * (g.wx * sx + cx) + sy * (g.wy * sy + cy) + sk * (g.wz * sk + cz);
+                const int B = ok ? B0 : JFA2_EMPTY_KEY;
+                const int Gx = ok ? gxk * sx : 0;
+                const int Gy = ok ? gyk * sy : 0;
+                // K(a', b') = B - (a' - a) Gx - (b' - bt) Gy; slot s <-> a' = a - 1 + s
+                const int Bs[3] = {B + Gx, B, B - Gx};
 #pragma unroll
-                    for (int s = 0; s < 3; ++s) {  // slot s <-> output a' = a - 1 + s
-                        const int da = s - 1;       // a' - a
-                        const int oa = a + da;
-                        if (oa < 0 || oa >= L) continue;
+                for (int s = 0; s < 3; ++s) {
 #pragma unroll
-                        for (int db = -1; db <= 1; ++db) {  // output row b' = bt + db
-                            const int b = bt + db;
-                            if (b < 0 || b >= RY) continue;
-                            const int K = B - da * Gx - db * Gy;
-                            jfa2_consider(K, v, Km[s][b], W[s][b], i_first + oa * k,
-                                          j_base + b * k, z, g.hx, g.hy, g.hz);
-                        }
+                    for (int db = -1; db <= 1; ++db) {
+                        const int b = bt + db;
+                        if (b < 0 || b >= RY) continue;  // compile-time
+                        const int K = db == 0 ? Bs[s] : (db < 0 ? Bs[s] + Gy : Bs[s] - Gy);
+                        const bool lt = K < Km[s][b];
+                        const bool tq = (K == Km[s][b]) & (v != W[s][b]);
+                        Km[s][b] = lt ? K : Km[s][b];
+                        W[s][b] = lt ? v : W[s][b];
+                        tie[s][b] = lt ? false : (tie[s][b] | tq);
                     }
                 }
             }
@@ -137,20 +138,35 @@ __global__ void __launch_bounds__(128) jfa_pass2_kernel(PlaneSrc src, int32_t* _
         // output a - 1 (slot 0) is complete
         const int oa = a - 1;
         const int oi = i_first + oa * k;
-        if (oa >= 0 && oa < L && oi < i_end && zok) {
+        if (oa >= 0 && oa < L && oi < i_end) {
 #pragma unroll
             for (int b = 0; b < RY; ++b) {
                 const int oj = j_base + b * k;
-                if (oj >= g.ny) continue;
+                const bool live = zok && oj < g.ny;
                 const int64_t cell = (int64_t)(oi - g.x0) * plane + (int64_t)oj * g.nz + z;
                 const int32_t w = W[0][b];
-                if (FINAL) {
-                    empties += w == RTSDF_EMPTY;
-                    double d2 = center_d2(oi - unpack_i(w), oj - unpack_j(w), z - unpack_k(w),
-                                          g.hx, g.hy, g.hz);
-                    dst_sdf[cell] = (float)__dsub_rn(__dsqrt_rn(d2), beta);
-                } else {
-                    dst[cell] = w;
+                if (live) {
+                    if (FINAL) {
+                        empties += w == RTSDF_EMPTY;
+                        double d2 = center_d2(oi - unpack_i(w), oj - unpack_j(w), z - unpack_k(w),
+                                              g.hx, g.hy, g.hz);
+                        dst_sdf[cell] = (float)__dsub_rn(__dsqrt_rn(d2), beta);
+                    } else {
+                        dst[cell] = w;
+                    }
+                }
+                // integer tie between distinct seeds: defer to the exact rule
+                const bool flag = live && tie[0][b];
+                const unsigned m = __ballot_sync(0xffffffffu, flag);
+                if (m) {
+                    int64_t base = 0;
+                    if (lane == 0) base = (int64_t)atomicAdd((unsigned long long*)fix.count,
+                                                             (unsigned long long)__popc(m));
+                    base = __shfl_sync(0xffffffffu, base, 0);
+                    if (flag) {
+                        int64_t slot = base + __popc(m & ((1u << lane) - 1));
+                        if (slot < fix.cap) fix.cells[slot] = (int32_t)cell;
+                    }
                 }
             }
         }
@@ -158,10 +174,13 @@ __global__ void __launch_bounds__(128) jfa_pass2_kernel(PlaneSrc src, int32_t* _
         for (int b = 0; b < RY; ++b) {
             Km[0][b] = Km[1][b];
             W[0][b] = W[1][b];
+            tie[0][b] = tie[1][b];
             Km[1][b] = Km[2][b];
             W[1][b] = W[2][b];
+            tie[1][b] = tie[2][b];
             Km[2][b] = 0x7fffffff;
             W[2][b] = RTSDF_EMPTY;
+            tie[2][b] = false;
         }
 #pragma unroll
         for (int bt = 0; bt < RY + 2; ++bt)
@@ -171,6 +190,49 @@ __global__ void __launch_bounds__(128) jfa_pass2_kernel(PlaneSrc src, int32_t* _
     if (FINAL && empty_count) {
         for (int o = 16; o; o >>= 1) empties += __shfl_xor_sync(0xffffffffu, empties, o);
         if (lane == 0 && empties) atomicAdd((unsigned long long*)empty_count, (unsigned long long)empties);
+    }
+}
+
+// Re-decide the flagged cells with the reference's exact rule (jfa.py:108-124).
+template <bool FINAL, bool SLAB>
+__global__ void __launch_bounds__(128) jfa_fixup_kernel(PlaneSrc src, int32_t* __restrict__ dst,
+                                                        float* __restrict__ dst_sdf, JfaGeom g,
+                                                        double beta, JfaFixList fix) {
+    const int64_t n = min(*fix.count, fix.cap);
+    const int64_t plane = (int64_t)g.ny * g.nz;
+    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n;
+         q += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t cell = fix.cells[q];
+        const int il = (int)(cell / plane);
+        const int j = (int)((cell / g.nz) % g.ny), z = (int)(cell % g.nz);
+        const int i = g.x0 + il;
+        int32_t best = RTSDF_EMPTY;
+        double bd = 1e300;
+        for (int di = -1; di <= 1; ++di) {
+            const int qi = i + di * g.offset;
+            if (qi < 0 || qi >= g.nx) continue;
+            const int32_t* pl = SLAB ? plane_ptr(src, g, qi, plane) : src.local + (int64_t)qi * plane;
+            for (int dj = -1; dj <= 1; ++dj) {
+                const int qj = j + dj * g.offset;
+                if (qj < 0 || qj >= g.ny) continue;
+                for (int dk = -1; dk <= 1; ++dk) {
+                    const int qk = z + dk * g.offset;
+                    if (qk < 0 || qk >= g.nz) continue;
+                    const int32_t c = __ldg(pl + (int64_t)qj * g.nz + qk);
+                    if (c == RTSDF_EMPTY || c == best) continue;
+                    double d2 = center_d2(i - unpack_i(c), j - unpack_j(c), z - unpack_k(c), g.hx,
+                                          g.hy, g.hz);
+                    if (d2 < bd || (d2 == bd && best != RTSDF_EMPTY && c < best)) {
+                        best = c;
+                        bd = d2;
+                    }
+                }
+            }
+        }
+        if (FINAL)
+            dst_sdf[cell] = (float)__dsub_rn(__dsqrt_rn(bd), beta);
+        else
+            dst[cell] = best;
     }
 }
 

@@ -138,11 +138,27 @@ def jfa_offsets(dims):
     return offsets
 
 
+_WS: dict = {}
+
+
+def workspace(nx: int, ny: int, nz: int) -> torch.Tensor:
+    """Per-device JFA workspace (the integer-tie fix-up list), grown on demand.
+    Shared by every JFA launch of this process on that device's streams."""
+    need = int(_lib.lib().rtsdf_jfa_ws_bytes(int(nx), int(ny), int(nz)))
+    dev = device()
+    ws = _WS.get(dev.index)
+    if ws is None or ws.numel() < need:
+        ws = torch.empty(need, dtype=torch.uint8, device=dev)
+        _WS[dev.index] = ws
+    return ws
+
+
 def launch_step(src: torch.Tensor, dst: torch.Tensor, offset: int, h, w):
     nx, ny, nz = src.shape
+    ws = workspace(nx, ny, nz)
     _lib.check(_lib.lib().rtsdf_jfa_step(_lib.ptr(src), _lib.ptr(dst), nx, ny, nz, int(offset),
                                          float(h[0]), float(h[1]), float(h[2]), *w,
-                                         _lib.stream()), "jfa_step")
+                                         _lib.ptr(ws), ws.numel(), _lib.stream()), "jfa_step")
 
 
 def jfa_step(seeds: SeedGrid, offset: int) -> SeedGrid:
@@ -172,10 +188,11 @@ def flood_to_sdf(a: torch.Tensor, b: torch.Tensor, out: torch.Tensor, h, beta=0.
     """Full schedule with seeds -> SDF fused into the last pass (a, b clobbered)."""
     nx, ny, nz = a.shape
     w = _weights(h, (nx, ny, nz))
+    ws = workspace(nx, ny, nz)
     _lib.check(_lib.lib().rtsdf_jfa_run_sdf(_lib.ptr(a), _lib.ptr(b), _lib.ptr(out), nx, ny, nz,
                                             float(h[0]), float(h[1]), float(h[2]), *w,
-                                            float(beta), _lib.ptr(empty_count), _lib.stream()),
-               "jfa_run_sdf")
+                                            float(beta), _lib.ptr(empty_count), _lib.ptr(ws),
+                                            ws.numel(), _lib.stream()), "jfa_run_sdf")
 
 
 def jfa_run(voxels) -> SeedGrid:
