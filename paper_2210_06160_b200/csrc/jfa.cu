@@ -255,6 +255,7 @@ static int launch_step(PlaneSrc s, int32_t* dst, const JfaGeom& g, bool slab, vo
 static bool weights_ok(int nx, int ny, int nz, int wx, int wy, int wz) {
     if (wx == 0 && wy == 0 && wz == 0) return true;
     if (wx <= 0 || wy <= 0 || wz <= 0) return false;
+    if (wx > 16 || wy > 16 || wz > 16) return false;  // EMPTY-key bound in jfa2.cuh
     // keys relative to |x|^2 span about 2 qmax plus the increments: keep 2 bits spare
     double qmax = (double)wx * (nx - 1) * (nx - 1) + (double)wy * (ny - 1) * (ny - 1) +
                   (double)wz * (nz - 1) * (nz - 1);

@@ -67,34 +67,45 @@ __global__ void __launch_bounds__(128) jfa_pass2_kernel(PlaneSrc src, int32_t* _
 
     int Km[3][RY];
     int32_t W[3][RY];
-    bool tie[3][RY];
+    int tie[3][RY];
 #pragma unroll
     for (int s = 0; s < 3; ++s)
 #pragma unroll
         for (int b = 0; b < RY; ++b) {
             Km[s][b] = 0x7fffffff;
             W[s][b] = RTSDF_EMPTY;
-            tie[s][b] = false;
+            tie[s][b] = 0;
         }
 
+    // the in-plane offsets of the (RY + 2) x 3 taps and their validity are
+    // loop invariants of the task: a plane load is 18 address adds + loads
+    int offs[RY + 2][3];
+    unsigned okmask = 0;
+#pragma unroll
+    for (int bt = 0; bt < RY + 2; ++bt) {
+        const int tj = j_base + (bt - 1) * k;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            const int tz = z + (c - 1) * k;
+            const bool ok = zok && tj >= 0 && tj < g.ny && tz >= 0 && tz < g.nz;
+            offs[bt][c] = ok ? tj * g.nz + tz : 0;
+            okmask |= (ok ? 1u : 0u) << (bt * 3 + c);
+        }
+    }
     int32_t cur[RY + 2][3], nxt[RY + 2][3];
     auto load_plane = [&](int a, int32_t(&vals)[RY + 2][3]) {
         const int pi = i_first + a * k;
-        const int32_t* pl = nullptr;
-        if (pi >= 0 && pi < g.nx && a <= L)
+        const int32_t* pl = src.local;
+        unsigned m = 0;
+        if (pi >= 0 && pi < g.nx && a <= L) {
             pl = SLAB ? plane_ptr(src, g, pi, plane) : src.local + (int64_t)pi * plane;
-#pragma unroll
-        for (int bt = -1; bt <= RY; ++bt) {
-            const int tj = j_base + bt * k;
-            const bool rok = pl != nullptr && tj >= 0 && tj < g.ny && zok;
-#pragma unroll
-            for (int c = -1; c <= 1; ++c) {
-                const int tz = z + c * k;
-                vals[bt + 1][c + 1] = (rok && tz >= 0 && tz < g.nz)
-                                          ? __ldg(pl + (int64_t)tj * g.nz + tz)
-                                          : RTSDF_EMPTY;
-            }
+            m = okmask;
         }
+#pragma unroll
+        for (int bt = 0; bt < RY + 2; ++bt)
+#pragma unroll
+            for (int c = 0; c < 3; ++c)
+                vals[bt][c] = (m >> (bt * 3 + c)) & 1u ? __ldg(pl + offs[bt][c]) : RTSDF_EMPTY;
     };
     load_plane(-1, cur);
 
@@ -111,12 +122,13 @@ __global__ void __launch_bounds__(128) jfa_pass2_kernel(PlaneSrc src, int32_t* _
             for (int c = -1; c <= 1; ++c) {
                 const int32_t v = cur[bt + 1][c + 1];
                 if (__all_sync(0xffffffffu, v == RTSDF_EMPTY)) continue;  // warp-uniform skip
-                const bool ok = v != RTSDF_EMPTY;
                 const int sx = unpack_i(v), sy = unpack_j(v), sk = unpack_k(v);
                 const int B0 = sx * (g.wx * sx + cx) + sy * (g.wy * sy + cy) + sk * (g.wz * sk + cz);
-                const int B = ok ? B0 : JFA2_EMPTY_KEY;
-                const int Gx = ok ? gxk * sx : 0;
-                const int Gy = ok ? gyk * sy : 0;
+                // EMPTY (-1) decodes to (4095, 1023, 1023): its increments stay bounded
+                // (|Gx|, |Gy| < 2^23), so an EMPTY base of 2^30 can never beat a real
+                // key (|key| < 2^29) -- no per-increment selects
+                const int B = v != RTSDF_EMPTY ? B0 : JFA2_EMPTY_KEY;
+                const int Gx = gxk * sx, Gy = gyk * sy;
                 // K(a', b') = B - (a' - a) Gx - (b' - bt) Gy; slot s <-> a' = a - 1 + s
                 const int Bs[3] = {B + Gx, B, B - Gx};
 #pragma unroll
@@ -127,10 +139,11 @@ __global__ void __launch_bounds__(128) jfa_pass2_kernel(PlaneSrc src, int32_t* _
                         if (b < 0 || b >= RY) continue;  // compile-time
                         const int K = db == 0 ? Bs[s] : (db < 0 ? Bs[s] + Gy : Bs[s] - Gy);
                         const bool lt = K < Km[s][b];
-                        const bool tq = (K == Km[s][b]) & (v != W[s][b]);
-                        Km[s][b] = lt ? K : Km[s][b];
+                        const bool eq = (K == Km[s][b]) & (v != W[s][b]);
+                        Km[s][b] = min(Km[s][b], K);
                         W[s][b] = lt ? v : W[s][b];
-                        tie[s][b] = lt ? false : (tie[s][b] | tq);
+                        if (eq) tie[s][b] = 1;
+                        if (lt) tie[s][b] = 0;
                     }
                 }
             }

@@ -95,7 +95,7 @@ def integer_weights(hx: float, hy: float, hz: float, dims: tuple) -> tuple:
     for v in w:
         g = gcd(g, v)
     w = [v // g for v in w]
-    if max(w) > 4096:
+    if max(w) > 16:  # csrc/jfa.cu weights_ok (EMPTY-key bound of the v2 pass)
         return (0, 0, 0)
     qmax = sum(wi * (n - 1) ** 2 for wi, n in zip(w, dims))
     if qmax >= 2**29:  # csrc/jfa.cu weights_ok: relative keys need 2 spare bits
