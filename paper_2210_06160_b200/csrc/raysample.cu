@@ -128,6 +128,155 @@ __global__ void __launch_bounds__(SAMPLE_THREADS) sample_update_kernel(SamplePar
     }
 }
 
+// ----------------------------------------------------------------------------
+// Direction-binned sampler.  A block takes a group of G masked texels (G * x <=
+// BIN_RAYS rays), generates every ray's direction, counting-sorts the rays by
+// cube-map direction bin in shared memory and traces them in sorted order, so
+// a warp holds ~32 rays of similar direction from neighbouring texels instead
+// of 32 random directions from one texel (the traversal's SIMD efficiency was
+// 36 %).  Per-ray results land in shared memory and each texel is reduced and
+// updated by one thread in ray order -- deterministic, no global atomics.
+#define BIN_THREADS 128
+#define BIN_RAYS 512
+#define BIN_COUNT 24
+#define BIN_STACK RTSDF_FAST_STACK
+
+__device__ __forceinline__ int dir_bin(double dx, double dy, double dz) {
+    double ax = fabs(dx), ay = fabs(dy), az = fabs(dz);
+    int face, u, v;
+    if (ax >= ay && ax >= az) { face = dx >= 0 ? 0 : 1; u = dy >= 0; v = dz >= 0; }
+    else if (ay >= az) { face = dy >= 0 ? 2 : 3; u = dx >= 0; v = dz >= 0; }
+    else { face = dz >= 0 ? 4 : 5; u = dx >= 0; v = dy >= 0; }
+    return face * 4 + u * 2 + v;
+}
+
+__global__ void __launch_bounds__(BIN_THREADS) sample_update_binned_kernel(SampleParams P) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int x = P.x;
+    const int G = BIN_RAYS / x;                            // texels per group (x <= BIN_RAYS)
+    double* sdir = (double*)smem;                          // [BIN_RAYS][3]
+    double* st = sdir + 3 * BIN_RAYS;                      // [BIN_RAYS] hit t (or -1)
+    int32_t* stack_mem = (int32_t*)(st + BIN_RAYS);        // [BIN_STACK][BIN_THREADS]
+    int16_t* sorder = (int16_t*)(stack_mem + BIN_STACK * BIN_THREADS);  // [BIN_RAYS]
+    uint8_t* sbin = (uint8_t*)(sorder + BIN_RAYS);         // [BIN_RAYS]
+    uint8_t* sfac = sbin + BIN_RAYS;                       // [BIN_RAYS]
+    double* scen = (double*)(sfac + BIN_RAYS);             // [G][3] texel centres
+    __shared__ int hist[BIN_COUNT], cursor[BIN_COUNT];
+
+    const int tid = threadIdx.x;
+    const int64_t M = min(*P.count, P.m_cap);
+    const int64_t nyz = (int64_t)P.fny * P.fnz;
+    const int64_t groups = (M + G - 1) / G;
+    for (int64_t grp = blockIdx.x; grp < groups; grp += gridDim.x) {
+        const int64_t n0 = grp * G;
+        const int g = (int)min((int64_t)G, M - n0);
+        const int R = g * x;
+        if (tid < BIN_COUNT) hist[tid] = 0;
+        // texel centres (raysample.py:167-169)
+        for (int q = tid; q < g; q += BIN_THREADS) {
+            int64_t lin = __ldg(P.idx + n0 + q);
+            int i = (int)(lin / nyz), j = (int)((lin / P.fnz) % P.fny), k = (int)(lin % P.fnz);
+            scen[3 * q] = P.coarse.lox + ((double)i + 0.5) * P.fhx;
+            scen[3 * q + 1] = P.coarse.loy + ((double)j + 0.5) * P.fhy;
+            scen[3 * q + 2] = P.coarse.loz + ((double)k + 0.5) * P.fhz;
+        }
+        __syncthreads();
+        // directions + bins
+        for (int r = tid; r < R; r += BIN_THREADS) {
+            const int q = r / x, ray = r - q * x;
+            const int64_t n = n0 + q;
+            double dx, dy, dz;
+            if (P.dirs) {
+                const double* d = P.dirs + 3 * (n * x + ray);
+                dx = d[0];
+                dy = d[1];
+                dz = d[2];
+            } else {
+                int64_t lin = __ldg(P.idx + n);
+                uint64_t key = stream_key(P.seed, (uint64_t)lin, (uint64_t)P.frame);
+                unit_sphere_dir(key, (uint64_t)ray, dx, dy, dz);
+            }
+            sdir[3 * r] = dx;
+            sdir[3 * r + 1] = dy;
+            sdir[3 * r + 2] = dz;
+            int b = dir_bin(dx, dy, dz);
+            sbin[r] = (uint8_t)b;
+            atomicAdd(&hist[b], 1);
+        }
+        __syncthreads();
+        if (tid == 0) {
+            int s = 0;
+            for (int b = 0; b < BIN_COUNT; ++b) {
+                cursor[b] = s;
+                s += hist[b];
+            }
+        }
+        __syncthreads();
+        for (int r = tid; r < R; r += BIN_THREADS) sorder[atomicAdd(&cursor[sbin[r]], 1)] = (int16_t)r;
+        __syncthreads();
+        // trace in bin order: consecutive lanes hold rays of one direction bin
+        for (int p = tid; p < R; p += BIN_THREADS) {
+            const int r = sorder[p];
+            const int q = r / x;
+            int32_t id;
+            int facing;
+            double t = trace_fast(P.bvh, scen[3 * q], scen[3 * q + 1], scen[3 * q + 2],
+                                  sdir[3 * r], sdir[3 * r + 1], sdir[3 * r + 2], P.t_max,
+                                  stack_mem + tid, BIN_THREADS, id, facing);
+            st[r] = id >= 0 ? t : -1.0;
+            sfac[r] = (uint8_t)(id >= 0 ? facing : 0);
+        }
+        __syncthreads();
+        // per texel, in ray order (raysample.py:140-152) + Eq. 1 (raysample.py:229-244)
+        for (int q = tid; q < g; q += BIN_THREADS) {
+            const int64_t n = n0 + q;
+            double best = __longlong_as_double(0x7ff0000000000000ll);
+            int fr = 0, bk = 0;
+            for (int ray = 0; ray < x; ++ray) {
+                const int r = q * x + ray;
+                const int f = sfac[r];
+                if (f) {
+                    const double t = st[r];
+                    if (t < best) best = t;
+                    fr += f == 1;
+                    bk += f == 2;
+                }
+            }
+            if (P.samp_min) P.samp_min[n] = best;
+            if (P.samp_front) P.samp_front[n] = fr;
+            if (P.samp_back) P.samp_back[n] = bk;
+            if (!P.prev) continue;
+            const int64_t lin = __ldg(P.idx + n);
+            float rm = P.run_min[lin];
+            int32_t f = P.front[lin], b = P.back[lin];
+            if (!P.mask_old[lin]) {
+                rm = __int_as_float(0x7f800000);
+                f = 0;
+                b = 0;
+            }
+            double m = best;
+            if (m < (double)rm) rm = (float)m;
+            f += fr;
+            b += bk;
+            P.run_min[lin] = rm;
+            P.front[lin] = f;
+            P.back[lin] = b;
+            double c = (double)(float)trilinear(P.coarse, scen[3 * q], scen[3 * q + 1],
+                                                scen[3 * q + 2]);
+            double blend = P.alpha * fabs((double)P.prev[lin]) + (1.0 - P.alpha) * c;
+            double mag = blend < m ? blend : m;
+            P.out[lin] = b > f ? (float)(-mag) : (float)mag;
+        }
+        __syncthreads();
+    }
+}
+
+static size_t binned_smem_bytes(int x) {
+    return (size_t)BIN_RAYS * (3 + 1) * sizeof(double) +
+           (size_t)BIN_STACK * BIN_THREADS * sizeof(int32_t) + BIN_RAYS * (2 + 1 + 1) +
+           (size_t)(BIN_RAYS / x) * 3 * sizeof(double);
+}
+
 }  // namespace rtsdf
 
 using namespace rtsdf;
@@ -178,13 +327,30 @@ extern "C" int rtsdf_sample_update(const void* bvh_packed, int64_t n_nodes, int6
     P.back = back;
     P.alpha = alpha;
     P.out = out;
-    int tpw = x >= 32 || x == 0 ? 1 : 32 / x;
-    int64_t warps_needed = (m_cap + tpw - 1) / tpw;
-    int64_t blocks = (warps_needed + SAMPLE_THREADS / 32 - 1) / (SAMPLE_THREADS / 32);
-    int64_t cap = (int64_t)num_sms() * 16;
-    if (blocks > cap) blocks = cap;
-    if (blocks < 1) blocks = 1;
-    sample_update_kernel<<<(unsigned)blocks, SAMPLE_THREADS, 0, (cudaStream_t)stream>>>(P);
+    if (x >= 1 && x <= BIN_RAYS) {  // direction-binned path
+        static bool attr = false;
+        const size_t smem = binned_smem_bytes(x);
+        if (!attr) {
+            cudaFuncSetAttribute(sample_update_binned_kernel,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)binned_smem_bytes(1));
+            attr = true;
+        }
+        const int G = BIN_RAYS / x;
+        int64_t blocks = (m_cap + G - 1) / G;
+        int64_t cap = (int64_t)num_sms() * 8;
+        if (blocks > cap) blocks = cap;
+        if (blocks < 1) blocks = 1;
+        sample_update_binned_kernel<<<(unsigned)blocks, BIN_THREADS, smem, (cudaStream_t)stream>>>(P);
+    } else {
+        int tpw = x >= 32 || x == 0 ? 1 : 32 / x;
+        int64_t warps_needed = (m_cap + tpw - 1) / tpw;
+        int64_t blocks = (warps_needed + SAMPLE_THREADS / 32 - 1) / (SAMPLE_THREADS / 32);
+        int64_t cap = (int64_t)num_sms() * 16;
+        if (blocks > cap) blocks = cap;
+        if (blocks < 1) blocks = 1;
+        sample_update_kernel<<<(unsigned)blocks, SAMPLE_THREADS, 0, (cudaStream_t)stream>>>(P);
+    }
     count_launch();
     return check_launch("sample_update");
 }

@@ -18,7 +18,7 @@
 #pragma once
 #include "common.cuh"
 
-#define RTSDF_FAST_STACK 48
+#define RTSDF_FAST_STACK 40  // the host rejects search trees deeper than this
 
 namespace rtsdf {
 

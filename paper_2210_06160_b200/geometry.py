@@ -206,8 +206,8 @@ def build_bvh(mesh: TriangleMesh) -> BvhIndex:
     if n < 0:
         raise EmptyMeshError(L.rtsdf_last_error().decode())
     node_lo, node_hi, left, right = node_lo[:n].copy(), node_hi[:n].copy(), left[:n].copy(), right[:n].copy()
-    if tree_depth(left, right) >= 48:  # RTSDF_FAST_STACK (csrc/trace.cuh)
-        raise MeshError("BVH deeper than the traversal stack (48 levels)")
+    if tree_depth(left, right) >= 64:  # RTSDF_STACK (csrc/common.cuh)
+        raise MeshError("BVH deeper than the traversal stack (64 levels)")
     a = np.ascontiguousarray(p0[order])
     e1 = np.ascontiguousarray(p1[order] - a)
     e2 = np.ascontiguousarray(p2[order] - a)
@@ -223,8 +223,8 @@ def build_bvh(mesh: TriangleMesh) -> BvhIndex:
     if ns < 0:
         raise MeshError(L.rtsdf_last_error().decode())
     slo, shi, sl, sr = slo[:ns], shi[:ns], sl[:ns], sr[:ns]
-    if tree_depth(sl, sr) >= 48:
-        raise MeshError("SAH BVH deeper than the traversal stack (48 levels)")
+    if tree_depth(sl, sr) >= 40:  # RTSDF_FAST_STACK (csrc/trace.cuh)
+        raise MeshError("SAH BVH deeper than the traversal stack (40 levels)")
     sa = np.ascontiguousarray(p0[so])
     search = upload_bvh(slo, shi, sl, sr, so, sa, np.ascontiguousarray(p1[so] - sa),
                         np.ascontiguousarray(p2[so] - sa), np.ascontiguousarray(mesh.normals[so]))
