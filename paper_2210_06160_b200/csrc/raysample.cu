@@ -327,7 +327,11 @@ extern "C" int rtsdf_sample_update(const void* bvh_packed, int64_t n_nodes, int6
     P.back = back;
     P.alpha = alpha;
     P.out = out;
-    if (x >= 1 && x <= BIN_RAYS) {  // direction-binned path
+    static const int binned_mode = [] {
+        const char* e = getenv("RTSDF_SAMPLER");
+        return e && e[0] == 'b' ? 1 : 0;
+    }();
+    if (binned_mode && x >= 1 && x <= BIN_RAYS) {  // direction-binned path (experimental)
         static bool attr = false;
         const size_t smem = binned_smem_bytes(x);
         if (!attr) {

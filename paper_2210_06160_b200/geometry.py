@@ -10,6 +10,7 @@ device traversal layout; queries run on the GPU (rtsdf_ray_query).
 from __future__ import annotations
 
 import logging
+import os
 from dataclasses import dataclass, field as dc_field
 
 import numpy as np
@@ -21,6 +22,8 @@ from ._device import to_device, to_numpy
 log = logging.getLogger(__name__)
 
 DEGENERATE_AREA = 1e-12
+# leaf size of the K6 search tree (binned SAH; csrc/bvh.cu)
+SAH_MAX_LEAF = int(os.environ.get("RTSDF_SAH_LEAF", "4"))
 FACING_NONE = 0
 FACING_FRONT = 1
 FACING_BACK = 2
@@ -218,7 +221,7 @@ def build_bvh(mesh: TriangleMesh) -> BvhIndex:
     slo, shi = np.empty((cap, 3)), np.empty((cap, 3))
     sl, sr = np.empty(cap, np.int32), np.empty(cap, np.int32)
     so = np.empty(T, np.int32)
-    ns = L.rtsdf_bvh_build_sah_host(_lib.host_ptr(tri_lo), _lib.host_ptr(tri_hi), T, 4,
+    ns = L.rtsdf_bvh_build_sah_host(_lib.host_ptr(tri_lo), _lib.host_ptr(tri_hi), T, SAH_MAX_LEAF,
                                     *[_lib.host_ptr(x) for x in (slo, shi, sl, sr, so)])
     if ns < 0:
         raise MeshError(L.rtsdf_last_error().decode())
