@@ -176,10 +176,15 @@ int rtsdf_ray_query(const void* bvh_packed, int64_t n_nodes, int64_t n_tris, int
 
 /* ---------------------------------------------- ray-sampled refine + Eq. 1 */
 /* Replaces raysample.py:277-299 (_sample_masked_kernel + band reset +
- * _update_masked_kernel) fused: one warp per masked texel idx[n], one lane
- * per ray (x <= 32 per round, looped), warp-reduced min/front/back -- no
- * atomics.  M is read from device memory (*count from rtsdf_compact_mask)
- * so no host sync is needed; m_cap bounds the grid.
+ * _update_masked_kernel).  Default (workspace given): wavefront -- every ray
+ * traced with a small node budget, budget-exhausted rays re-traced from a
+ * compacted queue, then one thread per texel reduces its rays in ray order
+ * and applies Eq. 1 (results independent of the queue order).  Without a
+ * workspace: one warp per texel, one lane per ray, warp-reduced.  Closest
+ * hits are the brute-force ones the reference's BVH contract names
+ * (geometry.py:3-6; trace.cuh).  No atomics touch results.  M is read from
+ * device memory (*count from rtsdf_compact_mask) so no host sync is needed;
+ * m_cap bounds the grid.
  *   dirs (nullable): host-supplied table dirs[(n*x + r)*3 + c] (parity mode);
  *                    NULL = on-device SplitMix64 stream (rng.py:30-53).
  *   samp_min/front/back (nullable): per-texel frame results.
@@ -194,12 +199,17 @@ typedef struct {
     double fh[3];
 } rtsdf_resample_desc;
 
+/* Workspace of the wavefront sampler for m_cap texels x rays: per-ray results
+ * (t fp64, facing u8) and the long-ray queue.  With ws == NULL the sampler
+ * falls back to the warp-per-texel kernel (same results).                   */
+size_t rtsdf_sample_ws_bytes(int64_t m_cap, int x);
 int rtsdf_sample_update(const void* bvh_packed, int64_t n_nodes, int64_t n_tris, const int64_t* idx,
                         const int64_t* count, int64_t m_cap, const rtsdf_resample_desc* rs,
                         int x, uint64_t seed, int64_t frame, double t_max, const double* dirs,
                         double* samp_min, int32_t* samp_front, int32_t* samp_back,
                         const float* prev, const uint8_t* mask_old, float* run_min,
-                        int32_t* front, int32_t* back, double alpha, float* out, void* stream);
+                        int32_t* front, int32_t* back, double alpha, float* out, void* ws,
+                        size_t ws_bytes, void* stream);
 
 /* ------------------------------------------------------------- soft shadow */
 /* Replaces render.py:167 (_occlusion_kernel): per covered pixel fp64 sphere

@@ -129,6 +129,152 @@ __global__ void __launch_bounds__(SAMPLE_THREADS) sample_update_kernel(SamplePar
 }
 
 // ----------------------------------------------------------------------------
+// Wavefront sampler (default).  Most rays are short: in the C3 scene ~95 % of
+// the masked texels hug the ground plane and their rays finish after 2-3 node
+// visits, while the few rays heading into the sphere need ~13 levels -- in the
+// warp-per-texel kernel every warp then waits for its longest lane (36 % SIMD
+// efficiency).  Pass 1 traces every ray with a small node budget and writes
+// the per-ray result; rays that run out of budget are appended to a queue
+// (warp-aggregated) and pass 2 re-traces only those, densely packed.  A third
+// kernel reduces each texel's x rays in ray order (one thread per texel) and
+// applies the Eq. 1 update.  The queue order varies run to run but every ray's
+// result is deterministic, and the per-texel reduction order is fixed.
+#define WF_THREADS 128
+#define WF_BUDGET 6
+
+struct WfBuffers {
+    double* t;        // [R] hit t, or -1 (miss)
+    uint8_t* facing;  // [R] 0 miss, 1 front, 2 back
+    int32_t* queue;   // [R] rays needing the full search
+    int64_t* qcount;
+};
+
+__device__ __forceinline__ void wf_ray(const SampleParams& P, int64_t r, double& ox, double& oy,
+                                       double& oz, double& dx, double& dy, double& dz) {
+    const int x = P.x;
+    const int64_t n = r / x;
+    const int ray = (int)(r - n * x);
+    const int64_t nyz = (int64_t)P.fny * P.fnz;
+    const int64_t lin = __ldg(P.idx + n);
+    const int i = (int)(lin / nyz), j = (int)((lin / P.fnz) % P.fny), k = (int)(lin % P.fnz);
+    ox = P.coarse.lox + ((double)i + 0.5) * P.fhx;  // raysample.py:167-169
+    oy = P.coarse.loy + ((double)j + 0.5) * P.fhy;
+    oz = P.coarse.loz + ((double)k + 0.5) * P.fhz;
+    if (P.dirs) {
+        const double* d = P.dirs + 3 * r;  // dirs[(n * x + ray) * 3 + c]
+        dx = d[0];
+        dy = d[1];
+        dz = d[2];
+    } else {
+        unit_sphere_dir(stream_key(P.seed, (uint64_t)lin, (uint64_t)P.frame), (uint64_t)ray, dx,
+                        dy, dz);
+    }
+}
+
+__global__ void __launch_bounds__(WF_THREADS) wf_pass1_kernel(SampleParams P, WfBuffers B) {
+    __shared__ int32_t stack_mem[RTSDF_FAST_STACK * WF_THREADS];
+    const int lane = threadIdx.x & 31;
+    const int64_t R = min(*P.count, P.m_cap) * P.x;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t r0 = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31); r0 < R; r0 += stride) {
+        const int64_t r = r0 + lane;
+        bool need = false;
+        if (r < R) {
+            double ox, oy, oz, dx, dy, dz;
+            wf_ray(P, r, ox, oy, oz, dx, dy, dz);
+            int32_t id;
+            int facing;
+            bool done;
+            double t = trace_fast(P.bvh, ox, oy, oz, dx, dy, dz, P.t_max,
+                                  stack_mem + threadIdx.x, WF_THREADS, id, facing, WF_BUDGET, &done);
+            if (done) {
+                B.t[r] = id >= 0 ? t : -1.0;
+                B.facing[r] = (uint8_t)(id >= 0 ? facing : 0);
+            }
+            need = !done;
+        }
+        const unsigned m = __ballot_sync(0xffffffffu, need);
+        if (m) {
+            int64_t base = 0;
+            if (lane == 0) base = (int64_t)atomicAdd((unsigned long long*)B.qcount, (unsigned long long)__popc(m));
+            base = __shfl_sync(0xffffffffu, base, 0);
+            if (need) B.queue[base + __popc(m & ((1u << lane) - 1))] = (int32_t)r;
+        }
+    }
+}
+
+__global__ void __launch_bounds__(WF_THREADS) wf_pass2_kernel(SampleParams P, WfBuffers B) {
+    __shared__ int32_t stack_mem[RTSDF_FAST_STACK * WF_THREADS];
+    const int64_t Q = *B.qcount;
+    for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < Q;
+         q += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = B.queue[q];
+        double ox, oy, oz, dx, dy, dz;
+        wf_ray(P, r, ox, oy, oz, dx, dy, dz);
+        int32_t id;
+        int facing;
+        double t = trace_fast(P.bvh, ox, oy, oz, dx, dy, dz, P.t_max, stack_mem + threadIdx.x,
+                              WF_THREADS, id, facing);
+        B.t[r] = id >= 0 ? t : -1.0;
+        B.facing[r] = (uint8_t)(id >= 0 ? facing : 0);
+    }
+}
+
+// raysample.py:140-152 (per-texel min / votes, in ray order) + :229-244 (Eq. 1)
+__global__ void __launch_bounds__(WF_THREADS) wf_reduce_update_kernel(SampleParams P, WfBuffers B) {
+    const int64_t M = min(*P.count, P.m_cap);
+    const int x = P.x;
+    const int64_t nyz = (int64_t)P.fny * P.fnz;
+    for (int64_t n = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; n < M;
+         n += (int64_t)gridDim.x * blockDim.x) {
+        double best = __longlong_as_double(0x7ff0000000000000ll);
+        int fr = 0, bk = 0;
+        for (int ray = 0; ray < x; ++ray) {
+            const int64_t r = n * x + ray;
+            const int f = B.facing[r];
+            if (f) {
+                const double t = B.t[r];
+                if (t < best) best = t;
+                fr += f == 1;
+                bk += f == 2;
+            }
+        }
+        if (P.samp_min) P.samp_min[n] = best;
+        if (P.samp_front) P.samp_front[n] = fr;
+        if (P.samp_back) P.samp_back[n] = bk;
+        if (!P.prev) continue;
+        const int64_t lin = __ldg(P.idx + n);
+        const int i = (int)(lin / nyz), j = (int)((lin / P.fnz) % P.fny), k = (int)(lin % P.fnz);
+        const double px = P.coarse.lox + ((double)i + 0.5) * P.fhx;
+        const double py = P.coarse.loy + ((double)j + 0.5) * P.fhy;
+        const double pz = P.coarse.loz + ((double)k + 0.5) * P.fhz;
+        float rm = P.run_min[lin];
+        int32_t f = P.front[lin], b = P.back[lin];
+        if (!P.mask_old[lin]) {
+            rm = __int_as_float(0x7f800000);
+            f = 0;
+            b = 0;
+        }
+        const double m = best;
+        if (m < (double)rm) rm = (float)m;
+        f += fr;
+        b += bk;
+        P.run_min[lin] = rm;
+        P.front[lin] = f;
+        P.back[lin] = b;
+        const double c = (double)(float)trilinear(P.coarse, px, py, pz);  // c_fine (f32)
+        const double blend = P.alpha * fabs((double)P.prev[lin]) + (1.0 - P.alpha) * c;
+        const double mag = blend < m ? blend : m;
+        P.out[lin] = b > f ? (float)(-mag) : (float)mag;
+    }
+}
+
+static size_t wf_ws_bytes(int64_t m_cap, int x) {
+    const int64_t R = m_cap * (x > 0 ? x : 1);
+    return 256 + (size_t)R * (sizeof(double) + sizeof(int32_t) + 1) + 256;
+}
+
+// ----------------------------------------------------------------------------
 // Direction-binned sampler.  A block takes a group of G masked texels (G * x <=
 // BIN_RAYS rays), generates every ray's direction, counting-sorts the rays by
 // cube-map direction bin in shared memory and traces them in sorted order, so
@@ -281,6 +427,8 @@ static size_t binned_smem_bytes(int x) {
 
 using namespace rtsdf;
 
+extern "C" size_t rtsdf_sample_ws_bytes(int64_t m_cap, int x) { return wf_ws_bytes(m_cap, x); }
+
 extern "C" int rtsdf_sample_update(const void* bvh_packed, int64_t n_nodes, int64_t n_tris,
                                    const int64_t* idx,
                                    const int64_t* count, int64_t m_cap,
@@ -289,7 +437,7 @@ extern "C" int rtsdf_sample_update(const void* bvh_packed, int64_t n_nodes, int6
                                    double* samp_min, int32_t* samp_front, int32_t* samp_back,
                                    const float* prev, const uint8_t* mask_old, float* run_min,
                                    int32_t* front, int32_t* back, double alpha, float* out,
-                                   void* stream) {
+                                   void* ws, size_t ws_bytes, void* stream) {
     if (x < 0 || !rs || !count || !idx) {
         set_error("sample_update: bad arguments");
         return RTSDF_ERR_INVALID;
@@ -327,11 +475,38 @@ extern "C" int rtsdf_sample_update(const void* bvh_packed, int64_t n_nodes, int6
     P.back = back;
     P.alpha = alpha;
     P.out = out;
-    static const int binned_mode = [] {
+    // sampler selection: wavefront (default, needs the workspace), warp-per-texel
+    // (RTSDF_SAMPLER=warp or no workspace) or direction-binned (experimental)
+    static const int mode = [] {
         const char* e = getenv("RTSDF_SAMPLER");
-        return e && e[0] == 'b' ? 1 : 0;
+        if (!e) return 0;
+        return e[0] == 'b' ? 2 : (e[0] == 'w' && e[1] == 'a' ? 1 : 0);
     }();
-    if (binned_mode && x >= 1 && x <= BIN_RAYS) {  // direction-binned path (experimental)
+    const bool wf_ok = x >= 1 && ws && ws_bytes >= wf_ws_bytes(m_cap, x) &&
+                       m_cap * (int64_t)x < ((int64_t)1 << 31);
+    cudaStream_t st = (cudaStream_t)stream;
+    if (mode == 0 && wf_ok) {
+        WfBuffers B;
+        char* p = (char*)ws;
+        B.qcount = (int64_t*)p;
+        p += 256;
+        const int64_t R = m_cap * x;
+        B.t = (double*)p;
+        p += R * sizeof(double);
+        B.queue = (int32_t*)p;
+        p += R * sizeof(int32_t);
+        B.facing = (uint8_t*)p;
+        cudaMemsetAsync(B.qcount, 0, sizeof(int64_t), st);
+        int64_t blocks = (R + WF_THREADS - 1) / WF_THREADS;
+        int64_t cap = (int64_t)num_sms() * 24;
+        wf_pass1_kernel<<<(unsigned)(blocks < cap ? blocks : cap), WF_THREADS, 0, st>>>(P, B);
+        wf_pass2_kernel<<<(unsigned)(num_sms() * 12), WF_THREADS, 0, st>>>(P, B);
+        int64_t ublocks = (m_cap + WF_THREADS - 1) / WF_THREADS;
+        wf_reduce_update_kernel<<<(unsigned)(ublocks < cap ? ublocks : cap), WF_THREADS, 0, st>>>(P, B);
+        count_launch(3);
+        return check_launch("sample_update");
+    }
+    if (mode == 2 && x >= 1 && x <= BIN_RAYS) {  // direction-binned path (experimental)
         static bool attr = false;
         const size_t smem = binned_smem_bytes(x);
         if (!attr) {

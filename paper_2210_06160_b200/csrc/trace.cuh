@@ -117,11 +117,15 @@ __device__ __forceinline__ bool tri_maybe(const FastTri& tr, float tx, float ty,
 }
 
 // Closest hit, brute-force equivalent.  `stack` is this thread's slot in a
-// shared-memory stack with `stride` (= blockDim) between entries.
+// shared-memory stack with `stride` (= blockDim) between entries.  budget > 0
+// bounds the number of internal-node visits: when it runs out the search is
+// abandoned and *complete is set false (the caller re-traces the ray later
+// with no budget); budget <= 0 = unbounded.
 __device__ __forceinline__ double trace_fast(const FastBvh& b, double ox, double oy, double oz,
                                              double dx, double dy, double dz, double t_max,
                                              int32_t* stack, int stride, int32_t& out_id,
-                                             int& out_facing) {
+                                             int& out_facing, int budget = 0,
+                                             bool* complete = nullptr) {
     RayF r;
     r.ix = clamp_inv(dx);
     r.iy = clamp_inv(dy);
@@ -136,8 +140,13 @@ __device__ __forceinline__ double trace_fast(const FastBvh& b, double ox, double
     float tb = t_max < 3.0e38 ? __double2float_ru(t_max) : RTSDF_FINF;
     int sp = 0;
     int32_t node = b.root;
+    if (complete) *complete = true;
     while (true) {
         if (node >= 0) {  // internal: test both children, descend into the nearer
+            if (budget > 0 && --budget == 0) {
+                if (complete) *complete = false;
+                break;
+            }
             const FastNode* nd = b.nodes + node;
             float4 a0 = __ldg((const float4*)&nd->lo0[0]);  // lo0 xyz, hi0 x
             float4 a1 = __ldg((const float4*)&nd->hi0[1]);  // hi0 yz, lo1 xy

@@ -154,20 +154,41 @@ def masked_indices(mask: torch.Tensor) -> torch.Tensor:
     return cb.idx[: int(cb.count.item())]
 
 
+_SWS: dict = {}
+
+
+def sample_workspace(m: int, x: int) -> torch.Tensor:
+    """Wavefront-sampler workspace for m texels x x rays (grow-only, per device)."""
+    need = int(_lib.lib().rtsdf_sample_ws_bytes(int(max(m, 1)), int(max(x, 1))))
+    dev = device()
+    ws = _SWS.get(dev.index)
+    if ws is None or ws.numel() < need:
+        ws = None
+        _SWS.pop(dev.index, None)
+        ws = torch.empty(int(need * 1.125) + 4096, dtype=torch.uint8, device=dev)
+        _SWS[dev.index] = ws
+    return ws
+
+
 def launch_sample_update(bvh: BvhIndex, g: _RsGeom, cb: CompactBuffers, params: SamplingParams,
                          frame: int, t_max: float, dirs=None, samp=None, prev=None,
                          accum: AccumulatorField | None = None, out=None, m_cap=None):
+    """m_cap: texel capacity; when None the masked count is read back (one
+    sync) so the wavefront workspace can be sized to the actual rays."""
     desc = g.desc()
     samp = samp or (None, None, None)
+    if m_cap is None:
+        m_cap = max(int(cb.count.item()), 1)
+    ws = sample_workspace(m_cap, params.rays_per_frame) if params.rays_per_frame > 0 else None
     _lib.check(_lib.lib().rtsdf_sample_update(
         _lib.ptr(bvh.search), bvh.search_nodes, bvh.num_tris, _lib.ptr(cb.idx), _lib.ptr(cb.count),
-        int(m_cap if m_cap is not None else cb.n), desc, int(params.rays_per_frame),
+        int(m_cap), desc, int(params.rays_per_frame),
         int(params.seed) & 0xFFFFFFFFFFFFFFFF, int(frame), float(t_max), _lib.ptr(dirs),
         _lib.ptr(samp[0]), _lib.ptr(samp[1]), _lib.ptr(samp[2]),
         _lib.ptr(prev), _lib.ptr(accum.mask if accum else None),
         _lib.ptr(accum.min_dist if accum else None), _lib.ptr(accum.front if accum else None),
         _lib.ptr(accum.back if accum else None), float(params.decay_alpha), _lib.ptr(out),
-        _lib.stream()), "sample_update")
+        _lib.ptr(ws), 0 if ws is None else ws.numel(), _lib.stream()), "sample_update")
 
 
 def sample_texel(bvh: BvhIndex, center, x: int, seed=0, stream=0, frame=0):
