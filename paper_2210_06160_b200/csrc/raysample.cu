@@ -151,12 +151,14 @@ struct WfBuffers {
 
 __device__ __forceinline__ void wf_ray(const SampleParams& P, int64_t r, double& ox, double& oy,
                                        double& oz, double& dx, double& dy, double& dz) {
-    const int x = P.x;
-    const int64_t n = r / x;
-    const int ray = (int)(r - n * x);
-    const int64_t nyz = (int64_t)P.fny * P.fnz;
-    const int64_t lin = __ldg(P.idx + n);
-    const int i = (int)(lin / nyz), j = (int)((lin / P.fnz) % P.fny), k = (int)(lin % P.fnz);
+    // 32-bit index math: rays < 2^31 (host-checked) and cells <= 1024^3
+    const unsigned x = (unsigned)P.x;
+    const unsigned n = (unsigned)r / x;
+    const int ray = (int)((unsigned)r - n * x);
+    const unsigned lin = (unsigned)__ldg(P.idx + n);
+    const unsigned nz = (unsigned)P.fnz, ny = (unsigned)P.fny;
+    const unsigned q = lin / nz;
+    const int k = (int)(lin - q * nz), j = (int)(q % ny), i = (int)(q / ny);
     ox = P.coarse.lox + ((double)i + 0.5) * P.fhx;  // raysample.py:167-169
     oy = P.coarse.loy + ((double)j + 0.5) * P.fhy;
     oz = P.coarse.loz + ((double)k + 0.5) * P.fhz;
