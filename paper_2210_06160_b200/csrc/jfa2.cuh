@@ -98,8 +98,13 @@ __global__ void __launch_bounds__(128) jfa_pass2_kernel(PlaneSrc src, int32_t* _
         const int32_t* pl = src.local;
         unsigned m = 0;
         if (pi >= 0 && pi < g.nx && a <= L) {
-            pl = SLAB ? plane_ptr(src, g, pi, plane) : src.local + (int64_t)pi * plane;
-            m = okmask;
+            // slab mode: the prefetch can run one plane past the last output's
+            // taps, which need not be resident -> treat as absent
+            const int32_t* q = SLAB ? plane_ptr(src, g, pi, plane) : src.local + (int64_t)pi * plane;
+            if (q != nullptr) {
+                pl = q;
+                m = okmask;
+            }
         }
 #pragma unroll
         for (int bt = 0; bt < RY + 2; ++bt)
