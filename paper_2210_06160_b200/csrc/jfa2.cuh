@@ -31,6 +31,25 @@ struct Jfa2Task {
     int nzb, jres, jgroups, ires, isegs, L;
 };
 
+// One candidate against one output's running (Km, W, tie): 3 predicate
+// compares, a min, a select and two predicated moves.  tie is set when a
+// DIFFERENT seed equals the running minimum and cleared by a strict
+// improvement, so at the end it is set iff >= 2 distinct seeds share the final
+// minimum key.
+__device__ __forceinline__ void jfa2_eval(int K, int32_t v, int& Km, int32_t& W, int& T) {
+    asm volatile(
+        "{\n\t.reg .pred plt, peq;\n\t"
+        "setp.lt.s32 plt, %3, %0;\n\t"
+        "setp.eq.s32 peq, %3, %0;\n\t"
+        "setp.ne.and.s32 peq, %4, %1, peq;\n\t"
+        "min.s32 %0, %0, %3;\n\t"
+        "selp.b32 %1, %4, %1, plt;\n\t"
+        "@peq mov.b32 %2, 1;\n\t"
+        "@plt mov.b32 %2, 0;\n\t}"
+        : "+r"(Km), "+r"(W), "+r"(T)
+        : "r"(K), "r"(v));
+}
+
 struct JfaFixList {
     int32_t* cells;  // local linear cell indices needing the exact rule
     int64_t* count;  // device counter
@@ -143,12 +162,7 @@ __global__ void __launch_bounds__(128) jfa_pass2_kernel(PlaneSrc src, int32_t* _
                         const int b = bt + db;
                         if (b < 0 || b >= RY) continue;  // compile-time
                         const int K = db == 0 ? Bs[s] : (db < 0 ? Bs[s] + Gy : Bs[s] - Gy);
-                        const bool lt = K < Km[s][b];
-                        const bool eq = (K == Km[s][b]) & (v != W[s][b]);
-                        Km[s][b] = min(Km[s][b], K);
-                        W[s][b] = lt ? v : W[s][b];
-                        if (eq) tie[s][b] = 1;
-                        if (lt) tie[s][b] = 0;
+                        jfa2_eval(K, v, Km[s][b], W[s][b], tie[s][b]);
                     }
                 }
             }

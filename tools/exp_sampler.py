@@ -42,3 +42,5 @@ for name, d in (("device-rng", None), ("table", dirs_d), ("device-rng", None), (
         torch.cuda.synchronize()
         ts.append(e0.elapsed_time(e1))
     print(name, "ms", [round(t, 3) for t in ts], flush=True)
+    ws = RS._SWS[torch.cuda.current_device()]
+    print("  queued long rays:", int(ws[:8].view(torch.int64).item()), "of", m * 32, flush=True)
