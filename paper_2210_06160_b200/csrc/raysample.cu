@@ -173,7 +173,7 @@ __device__ __forceinline__ void wf_ray(const SampleParams& P, int64_t r, double&
     }
 }
 
-__global__ void __launch_bounds__(WF_THREADS) wf_pass1_kernel(SampleParams P, WfBuffers B) {
+__global__ void __launch_bounds__(WF_THREADS, 8) wf_pass1_kernel(SampleParams P, WfBuffers B, int budget) {
     __shared__ int32_t stack_mem[RTSDF_FAST_STACK * WF_THREADS];
     const int lane = threadIdx.x & 31;
     const int64_t R = min(*P.count, P.m_cap) * P.x;
@@ -188,7 +188,7 @@ __global__ void __launch_bounds__(WF_THREADS) wf_pass1_kernel(SampleParams P, Wf
             int facing;
             bool done;
             double t = trace_fast(P.bvh, ox, oy, oz, dx, dy, dz, P.t_max,
-                                  stack_mem + threadIdx.x, WF_THREADS, id, facing, WF_BUDGET, &done);
+                                  stack_mem + threadIdx.x, WF_THREADS, id, facing, budget, &done);
             if (done) {
                 B.t[r] = id >= 0 ? t : -1.0;
                 B.facing[r] = (uint8_t)(id >= 0 ? facing : 0);
@@ -205,7 +205,7 @@ __global__ void __launch_bounds__(WF_THREADS) wf_pass1_kernel(SampleParams P, Wf
     }
 }
 
-__global__ void __launch_bounds__(WF_THREADS) wf_pass2_kernel(SampleParams P, WfBuffers B) {
+__global__ void __launch_bounds__(WF_THREADS, 8) wf_pass2_kernel(SampleParams P, WfBuffers B) {
     __shared__ int32_t stack_mem[RTSDF_FAST_STACK * WF_THREADS];
     const int64_t Q = *B.qcount;
     for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < Q;
@@ -501,7 +501,11 @@ extern "C" int rtsdf_sample_update(const void* bvh_packed, int64_t n_nodes, int6
         cudaMemsetAsync(B.qcount, 0, sizeof(int64_t), st);
         int64_t blocks = (R + WF_THREADS - 1) / WF_THREADS;
         int64_t cap = (int64_t)num_sms() * 24;
-        wf_pass1_kernel<<<(unsigned)(blocks < cap ? blocks : cap), WF_THREADS, 0, st>>>(P, B);
+        static const int budget = [] {
+            const char* e = getenv("RTSDF_WF_BUDGET");
+            return e ? atoi(e) : WF_BUDGET;
+        }();
+        wf_pass1_kernel<<<(unsigned)(blocks < cap ? blocks : cap), WF_THREADS, 0, st>>>(P, B, budget);
         wf_pass2_kernel<<<(unsigned)(num_sms() * 12), WF_THREADS, 0, st>>>(P, B);
         int64_t ublocks = (m_cap + WF_THREADS - 1) / WF_THREADS;
         wf_reduce_update_kernel<<<(unsigned)(ublocks < cap ? ublocks : cap), WF_THREADS, 0, st>>>(P, B);
