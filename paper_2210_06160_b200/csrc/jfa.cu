@@ -241,7 +241,15 @@ static int launch_step(PlaneSrc s, int32_t* dst, const JfaGeom& g, bool slab, vo
     dim3 block(32, 8, 1);
     dim3 grid((g.nz + 31) / 32, (g.ny + 7) / 8, g.nxl);
     bool int_mode = g.wx > 0 && g.wy > 0 && g.wz > 0;
-    if (int_mode) {
+    int mdim = g.nx > g.ny ? g.nx : g.ny;
+    if (g.nz > mdim) mdim = g.nz;
+    if (int_mode && 2 * g.offset >= mdim) {
+        // first pass: every lattice chain has <= 2 cells, v2's register tiles
+        // cannot amortise their setup -- the per-cell kernel is faster
+        if (slab) jfa_step_kernel<JFA_INT, true><<<grid, block, 0, st>>>(s, dst, g);
+        else jfa_step_kernel<JFA_INT, false><<<grid, block, 0, st>>>(s, dst, g);
+        count_launch();
+    } else if (int_mode) {
         if (slab) launch_pass2<false, true>(s, dst, nullptr, g, 0.0, nullptr, ws, st);
         else launch_pass2<false, false>(s, dst, nullptr, g, 0.0, nullptr, ws, st);
     } else {

@@ -140,7 +140,7 @@ __global__ void __launch_bounds__(SAMPLE_THREADS) sample_update_kernel(SamplePar
 // applies the Eq. 1 update.  The queue order varies run to run but every ray's
 // result is deterministic, and the per-texel reduction order is fixed.
 #define WF_THREADS 128
-#define WF_BUDGET 6
+#define WF_BUDGET 4
 
 struct WfBuffers {
     double* t;        // [R] hit t, or -1 (miss)
