@@ -157,6 +157,12 @@ int64_t rtsdf_bvh_build_host(const double* tri_lo, const double* tri_hi, int64_t
 int64_t rtsdf_bvh_build_sah_host(const double* tri_lo, const double* tri_hi, int64_t n_tris,
                                  int max_leaf, double* node_lo, double* node_hi,
                                  int32_t* node_left, int32_t* node_right, int32_t* order);
+/* Collapse a flat binary tree into 4-wide nodes (128 B: padded fp32 child
+ * boxes + child refs) for the K6 search; host in/out.  Returns node count or
+ * < 0 (capacity).                                                           */
+int64_t rtsdf_bvh4_collapse_host(const double* node_lo, const double* node_hi,
+                                 const int32_t* node_left, const int32_t* node_right,
+                                 int64_t n_nodes, void* out_nodes4, int64_t cap);
 /* Pack the flat BVH (device SoA as in BvhIndex, geometry.py:186-195) into the
  * device traversal layout: nodes (64 B each) and triangles (128 B each).    */
 size_t rtsdf_bvh_packed_bytes(int64_t n_nodes, int64_t n_tris);
@@ -203,7 +209,10 @@ typedef struct {
  * (t fp64, facing u8) and the long-ray queue.  With ws == NULL the sampler
  * falls back to the warp-per-texel kernel (same results).                   */
 size_t rtsdf_sample_ws_bytes(int64_t m_cap, int x);
-int rtsdf_sample_update(const void* bvh_packed, int64_t n_nodes, int64_t n_tris, const int64_t* idx,
+/* n_nodes4 > 0: the BVH4 collapse of the search tree (rtsdf_bvh4_collapse_host)
+ * is appended to bvh_packed at offset rtsdf_bvh_packed_bytes(n_nodes, n_tris). */
+int rtsdf_sample_update(const void* bvh_packed, int64_t n_nodes, int64_t n_tris, int64_t n_nodes4,
+                        const int64_t* idx,
                         const int64_t* count, int64_t m_cap, const rtsdf_resample_desc* rs,
                         int x, uint64_t seed, int64_t frame, double t_max, const double* dirs,
                         double* samp_min, int32_t* samp_front, int32_t* samp_back,

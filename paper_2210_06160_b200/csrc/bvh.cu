@@ -311,6 +311,23 @@ __global__ void __launch_bounds__(128) ray_query_fast_kernel(
     out_facing[q] = facing;
 }
 
+__global__ void __launch_bounds__(128) ray_query_fast4_kernel(
+    FastBvh4 b, const double* __restrict__ orig, const double* __restrict__ dirs, int64_t n,
+    double t_max, double* __restrict__ out_t, int32_t* __restrict__ out_id,
+    int32_t* __restrict__ out_facing) {
+    __shared__ int32_t stack_mem[RTSDF_FAST_STACK * 128];
+    int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (q >= n) return;
+    int32_t id;
+    int facing;
+    double t = trace_fast4(b, orig[3 * q], orig[3 * q + 1], orig[3 * q + 2], dirs[3 * q],
+                           dirs[3 * q + 1], dirs[3 * q + 2], t_max, stack_mem + threadIdx.x, 128,
+                           id, facing);
+    out_t[q] = t;
+    out_id[q] = id;
+    out_facing[q] = facing;
+}
+
 __global__ void ray_query_kernel(BvhView b, const double* __restrict__ orig,
                                  const double* __restrict__ dirs, int64_t n, double t_max,
                                  double* __restrict__ out_t, int32_t* __restrict__ out_id,
@@ -383,6 +400,111 @@ extern "C" int64_t rtsdf_bvh_build_sah_host(const double* tri_lo, const double* 
     return n;
 }
 
+// ---- BVH4 collapse (host) -------------------------------------------------
+namespace rtsdf {
+struct Collapse4 {
+    const double* lo;
+    const double* hi;
+    const int32_t* left;
+    const int32_t* right;
+    float pad;
+    std::vector<FastNode4> out;
+
+    static float down(double v, float pad) {
+        float f = (float)v;
+        if ((double)f > v) f = nextafterf(f, -INFINITY);
+        f = f - pad;
+        return nextafterf(f, -INFINITY);
+    }
+    static float up(double v, float pad) {
+        float f = (float)v;
+        if ((double)f < v) f = nextafterf(f, INFINITY);
+        f = f + pad;
+        return nextafterf(f, INFINITY);
+    }
+    double area(int32_t n) const {
+        double dx = hi[3 * n] - lo[3 * n], dy = hi[3 * n + 1] - lo[3 * n + 1],
+               dz = hi[3 * n + 2] - lo[3 * n + 2];
+        return dx * dy + dy * dz + dz * dx;
+    }
+    int32_t ref_of(int32_t n) {
+        if (left[n] < 0) return -(((-left[n] - 1) << 3) | right[n]) - 1;
+        return build(n);
+    }
+    int32_t build(int32_t n) {  // n: internal binary node, or a leaf root
+        int32_t me = (int32_t)out.size();
+        out.emplace_back();
+        std::vector<int32_t> kids;
+        if (left[n] < 0) {
+            kids.push_back(n);
+        } else {
+            kids.push_back(left[n]);
+            kids.push_back(right[n]);
+            while (kids.size() < 4) {
+                int best = -1;
+                double ba = -1.0;
+                for (size_t q = 0; q < kids.size(); ++q)
+                    if (left[kids[q]] >= 0 && area(kids[q]) > ba) {
+                        ba = area(kids[q]);
+                        best = (int)q;
+                    }
+                if (best < 0) break;
+                int32_t c = kids[best];
+                kids[best] = left[c];
+                kids.push_back(right[c]);
+            }
+        }
+        FastNode4 f;
+        for (int q = 0; q < 4; ++q) {
+            f.pad[q] = 0;
+            if (q < (int)kids.size()) {
+                int32_t c = kids[q];
+                f.lox[q] = down(lo[3 * c], pad);
+                f.loy[q] = down(lo[3 * c + 1], pad);
+                f.loz[q] = down(lo[3 * c + 2], pad);
+                f.hix[q] = up(hi[3 * c], pad);
+                f.hiy[q] = up(hi[3 * c + 1], pad);
+                f.hiz[q] = up(hi[3 * c + 2], pad);
+                f.child[q] = 0;  // filled below (recursion may reallocate `out`)
+            } else {  // empty slot: a degenerate box at 1e30 no ray reaches
+                f.lox[q] = f.loy[q] = f.loz[q] = f.hix[q] = f.hiy[q] = f.hiz[q] = 1e30f;
+                f.child[q] = 0x7fffffff;
+            }
+        }
+        out[me] = f;
+        for (int q = 0; q < (int)kids.size(); ++q) {
+            const int32_t ref = ref_of(kids[q]);  // may grow `out`: index, don't hold refs
+            out[me].child[q] = ref;
+        }
+        return me;
+    }
+};
+}  // namespace rtsdf
+
+extern "C" int64_t rtsdf_bvh4_collapse_host(const double* node_lo, const double* node_hi,
+                                            const int32_t* node_left, const int32_t* node_right,
+                                            int64_t n_nodes, void* out_nodes4, int64_t cap) {
+    if (n_nodes < 1) {
+        set_error("bvh4_collapse: empty tree");
+        return -1;
+    }
+    Collapse4 c;
+    c.lo = node_lo;
+    c.hi = node_hi;
+    c.left = node_left;
+    c.right = node_right;
+    double m = 1.0;
+    for (int a = 0; a < 3; ++a) m = fmax(m, fmax(fabs(node_lo[a]), fabs(node_hi[a])));
+    c.pad = (float)(1e-5 * m);
+    c.build(0);
+    if ((int64_t)c.out.size() > cap) {
+        set_error("bvh4_collapse: capacity %lld < %lld nodes", (long long)cap, (long long)c.out.size());
+        return -1;
+    }
+    memcpy(out_nodes4, c.out.data(), c.out.size() * sizeof(FastNode4));
+    return (int64_t)c.out.size();
+}
+
 extern "C" size_t rtsdf_bvh_packed_bytes(int64_t n_nodes, int64_t n_tris) {
     return fast_offset_tris(n_nodes, n_tris) + (size_t)n_tris * sizeof(FastTri);
 }
@@ -411,7 +533,11 @@ extern "C" int rtsdf_ray_query(const void* packed, int64_t n_nodes, int64_t n_tr
                                double t_max, double* out_t, int32_t* out_id,
                                int32_t* out_facing, void* stream) {
     if (n <= 0) return RTSDF_OK;
-    if (fast)
+    if (fast == 2)
+        ray_query_fast4_kernel<<<(unsigned)((n + 127) / 128), 128, 0, (cudaStream_t)stream>>>(
+            fast_bvh4_view(packed, n_nodes, n_tris), origins, dirs, n, t_max, out_t, out_id,
+            out_facing);
+    else if (fast)
         ray_query_fast_kernel<<<(unsigned)((n + 127) / 128), 128, 0, (cudaStream_t)stream>>>(
             fast_bvh_view(packed, n_nodes, n_tris), origins, dirs, n, t_max, out_t, out_id,
             out_facing);

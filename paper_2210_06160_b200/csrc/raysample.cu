@@ -17,6 +17,7 @@ namespace rtsdf {
 
 struct SampleParams {
     FastBvh bvh;
+    FastBvh4 bvh4;  // valid when n_nodes4 > 0
     const int64_t* idx;
     const int64_t* count;
     int64_t m_cap;
@@ -140,7 +141,8 @@ __global__ void __launch_bounds__(SAMPLE_THREADS) sample_update_kernel(SamplePar
 // applies the Eq. 1 update.  The queue order varies run to run but every ray's
 // result is deterministic, and the per-texel reduction order is fixed.
 #define WF_THREADS 128
-#define WF_BUDGET 4
+#define WF_BUDGET 4   // binary search tree: internal-node visits in pass 1
+#define WF_BUDGET4 3  // BVH4
 
 struct WfBuffers {
     double* t;        // [R] hit t, or -1 (miss)
@@ -173,6 +175,18 @@ __device__ __forceinline__ void wf_ray(const SampleParams& P, int64_t r, double&
     }
 }
 
+template <bool WIDE>
+__device__ __forceinline__ double wf_trace(const SampleParams& P, double ox, double oy, double oz,
+                                           double dx, double dy, double dz, int32_t* stack,
+                                           int32_t& id, int& facing, int budget, bool* done) {
+    if (WIDE)
+        return trace_fast4(P.bvh4, ox, oy, oz, dx, dy, dz, P.t_max, stack, WF_THREADS, id, facing,
+                           budget, done);
+    return trace_fast(P.bvh, ox, oy, oz, dx, dy, dz, P.t_max, stack, WF_THREADS, id, facing,
+                      budget, done);
+}
+
+template <bool WIDE>
 __global__ void __launch_bounds__(WF_THREADS, 8) wf_pass1_kernel(SampleParams P, WfBuffers B, int budget) {
     __shared__ int32_t stack_mem[RTSDF_FAST_STACK * WF_THREADS];
     const int lane = threadIdx.x & 31;
@@ -187,8 +201,8 @@ __global__ void __launch_bounds__(WF_THREADS, 8) wf_pass1_kernel(SampleParams P,
             int32_t id;
             int facing;
             bool done;
-            double t = trace_fast(P.bvh, ox, oy, oz, dx, dy, dz, P.t_max,
-                                  stack_mem + threadIdx.x, WF_THREADS, id, facing, budget, &done);
+            double t = wf_trace<WIDE>(P, ox, oy, oz, dx, dy, dz, stack_mem + threadIdx.x, id,
+                                      facing, budget, &done);
             if (done) {
                 B.t[r] = id >= 0 ? t : -1.0;
                 B.facing[r] = (uint8_t)(id >= 0 ? facing : 0);
@@ -205,6 +219,7 @@ __global__ void __launch_bounds__(WF_THREADS, 8) wf_pass1_kernel(SampleParams P,
     }
 }
 
+template <bool WIDE>
 __global__ void __launch_bounds__(WF_THREADS, 8) wf_pass2_kernel(SampleParams P, WfBuffers B) {
     __shared__ int32_t stack_mem[RTSDF_FAST_STACK * WF_THREADS];
     const int64_t Q = *B.qcount;
@@ -215,8 +230,8 @@ __global__ void __launch_bounds__(WF_THREADS, 8) wf_pass2_kernel(SampleParams P,
         wf_ray(P, r, ox, oy, oz, dx, dy, dz);
         int32_t id;
         int facing;
-        double t = trace_fast(P.bvh, ox, oy, oz, dx, dy, dz, P.t_max, stack_mem + threadIdx.x,
-                              WF_THREADS, id, facing);
+        double t = wf_trace<WIDE>(P, ox, oy, oz, dx, dy, dz, stack_mem + threadIdx.x, id, facing,
+                                  0, nullptr);
         B.t[r] = id >= 0 ? t : -1.0;
         B.facing[r] = (uint8_t)(id >= 0 ? facing : 0);
     }
@@ -432,6 +447,7 @@ using namespace rtsdf;
 extern "C" size_t rtsdf_sample_ws_bytes(int64_t m_cap, int x) { return wf_ws_bytes(m_cap, x); }
 
 extern "C" int rtsdf_sample_update(const void* bvh_packed, int64_t n_nodes, int64_t n_tris,
+                                   int64_t n_nodes4,
                                    const int64_t* idx,
                                    const int64_t* count, int64_t m_cap,
                                    const rtsdf_resample_desc* rs, int x, uint64_t seed,
@@ -501,12 +517,21 @@ extern "C" int rtsdf_sample_update(const void* bvh_packed, int64_t n_nodes, int6
         cudaMemsetAsync(B.qcount, 0, sizeof(int64_t), st);
         int64_t blocks = (R + WF_THREADS - 1) / WF_THREADS;
         int64_t cap = (int64_t)num_sms() * 24;
-        static const int budget = [] {
+        const bool wide = n_nodes4 > 0;
+        static const int budget_env = [] {
             const char* e = getenv("RTSDF_WF_BUDGET");
-            return e ? atoi(e) : WF_BUDGET;
+            return e ? atoi(e) : 0;
         }();
-        wf_pass1_kernel<<<(unsigned)(blocks < cap ? blocks : cap), WF_THREADS, 0, st>>>(P, B, budget);
-        wf_pass2_kernel<<<(unsigned)(num_sms() * 12), WF_THREADS, 0, st>>>(P, B);
+        const int budget = budget_env > 0 ? budget_env : (wide ? WF_BUDGET4 : WF_BUDGET);
+        const unsigned b1 = (unsigned)(blocks < cap ? blocks : cap), b2 = (unsigned)(num_sms() * 12);
+        if (wide) {
+            P.bvh4 = fast_bvh4_view(bvh_packed, n_nodes, n_tris);
+            wf_pass1_kernel<true><<<b1, WF_THREADS, 0, st>>>(P, B, budget);
+            wf_pass2_kernel<true><<<b2, WF_THREADS, 0, st>>>(P, B);
+        } else {
+            wf_pass1_kernel<false><<<b1, WF_THREADS, 0, st>>>(P, B, budget);
+            wf_pass2_kernel<false><<<b2, WF_THREADS, 0, st>>>(P, B);
+        }
         int64_t ublocks = (m_cap + WF_THREADS - 1) / WF_THREADS;
         wf_reduce_update_kernel<<<(unsigned)(ublocks < cap ? ublocks : cap), WF_THREADS, 0, st>>>(P, B);
         count_launch(3);

@@ -205,4 +205,138 @@ __device__ __forceinline__ double trace_fast(const FastBvh& b, double ox, double
     return best_id < 0 ? -1.0 : best_t;
 }
 
+// ---------------------------------------------------------------------------
+// 4-wide variant of the same search (BVH4 collapsed from the SAH binary tree):
+// half the depth, four independent slab tests per node fetch (more ILP, fewer
+// divergent loop trips).  Same conservative padding, same pre-test and exact
+// confirm, so the result is the same brute-force closest hit.
+struct __align__(128) FastNode4 {
+    float lox[4], loy[4], loz[4];
+    float hix[4], hiy[4], hiz[4];
+    int32_t child[4];  // >= 0 node4 index; < 0 leaf -(start * 8 + count) - 1; INT_MAX empty
+    int32_t pad[4];
+};
+static_assert(sizeof(FastNode4) == 128, "node4 layout");
+
+struct FastBvh4 {
+    const FastNode4* nodes;
+    const FastTri* tris;
+    const BvhTri* exact;
+};
+
+__host__ __device__ inline FastBvh4 fast_bvh4_view(const void* packed, int64_t n_nodes,
+                                                   int64_t n_tris) {
+    FastBvh4 f;
+    const char* p = (const char*)packed;
+    f.exact = (const BvhTri*)(p + (size_t)n_nodes * sizeof(BvhNode));
+    f.tris = (const FastTri*)(p + fast_offset_tris(n_nodes, n_tris));
+    f.nodes = (const FastNode4*)(p + fast_offset_tris(n_nodes, n_tris) +
+                                 (size_t)n_tris * sizeof(FastTri));
+    return f;
+}
+
+__device__ __forceinline__ bool leaf_tris(const FastTri* __restrict__ tris, const BvhTri* exact,
+                                          int32_t ref, double ox, double oy, double oz, double dx,
+                                          double dy, double dz, float fdx, float fdy, float fdz,
+                                          double& best_t, int32_t& best_id, int& best_facing,
+                                          float& tb) {
+    const int32_t code = -ref - 1;
+    const int start = code >> 3, count = code & 7;
+    bool improved = false;
+    for (int k = start; k < start + count; ++k) {
+        const FastTri* ft = tris + k;
+        float4 f0 = __ldg((const float4*)&ft->a[0]);
+        float4 f1 = __ldg((const float4*)&ft->e1[1]);
+        float4 f2 = __ldg((const float4*)&ft->e2[2]);
+        FastTri tr;
+        tr.e1[0] = f0.w; tr.e1[1] = f1.x; tr.e1[2] = f1.y;
+        tr.e2[0] = f1.z; tr.e2[1] = f1.w; tr.e2[2] = f2.x;
+        tr.scale = f2.y;
+        const BvhTri* ex = exact + k;
+        float tx = (float)(ox - __ldg(ex->a)), ty = (float)(oy - __ldg(ex->a + 1)),
+              tz = (float)(oz - __ldg(ex->a + 2));
+        if (!tri_maybe(tr, tx, ty, tz, fdx, fdy, fdz, tb)) continue;
+        double t = ray_tri(ox, oy, oz, dx, dy, dz, ex);
+        if (t >= 0.0 && t <= best_t) {
+            int32_t orig = __ldg(&ex->orig);
+            if (t < best_t || best_id < 0 || orig < best_id) {
+                best_t = t;
+                best_id = orig;
+                double dot = __dadd_rn(
+                    __dadd_rn(__dmul_rn(dx, __ldg(ex->n)), __dmul_rn(dy, __ldg(ex->n + 1))),
+                    __dmul_rn(dz, __ldg(ex->n + 2)));
+                best_facing = dot < 0.0 ? 1 : 2;
+                tb = __double2float_ru(best_t);
+                improved = true;
+            }
+        }
+    }
+    return improved;
+}
+
+__device__ __forceinline__ double trace_fast4(const FastBvh4& b, double ox, double oy, double oz,
+                                              double dx, double dy, double dz, double t_max,
+                                              int32_t* stack, int stride, int32_t& out_id,
+                                              int& out_facing, int budget = 0,
+                                              bool* complete = nullptr) {
+    RayF r;
+    r.ix = clamp_inv(dx);
+    r.iy = clamp_inv(dy);
+    r.iz = clamp_inv(dz);
+    r.oix = (float)ox * r.ix;
+    r.oiy = (float)oy * r.iy;
+    r.oiz = (float)oz * r.iz;
+    const float fdx = (float)dx, fdy = (float)dy, fdz = (float)dz;
+    double best_t = t_max;
+    int32_t best_id = -1;
+    int best_facing = 0;
+    float tb = t_max < 3.0e38 ? __double2float_ru(t_max) : RTSDF_FINF;
+    int sp = 0;
+    int32_t node = 0;
+    if (complete) *complete = true;
+    while (true) {
+        if (node >= 0) {
+            if (budget > 0 && --budget == 0) {
+                if (complete) *complete = false;
+                break;
+            }
+            const FastNode4* nd = b.nodes + node;
+            const float4 lx = __ldg((const float4*)nd->lox), ly = __ldg((const float4*)nd->loy),
+                         lz = __ldg((const float4*)nd->loz), hx = __ldg((const float4*)nd->hix),
+                         hy = __ldg((const float4*)nd->hiy), hz = __ldg((const float4*)nd->hiz);
+            const int4 ch = __ldg((const int4*)nd->child);
+            float t[4];
+            t[0] = box_entry(lx.x, ly.x, lz.x, hx.x, hy.x, hz.x, r, tb);
+            t[1] = box_entry(lx.y, ly.y, lz.y, hx.y, hy.y, hz.y, r, tb);
+            t[2] = box_entry(lx.z, ly.z, lz.z, hx.z, hy.z, hz.z, r, tb);
+            t[3] = box_entry(lx.w, ly.w, lz.w, hx.w, hy.w, hz.w, r, tb);
+            const int32_t c[4] = {ch.x, ch.y, ch.z, ch.w};
+            // nearest hit child is visited next; the other hits go on the stack
+            int nearest = -1;
+            float tn = RTSDF_FINF;
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+                if (t[q] < tn) {
+                    tn = t[q];
+                    nearest = q;
+                }
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+                if (q != nearest && t[q] != RTSDF_FINF) stack[(sp++) * stride] = c[q];
+            if (nearest >= 0) {
+                node = c[nearest];
+                continue;
+            }
+        } else {
+            leaf_tris(b.tris, b.exact, node, ox, oy, oz, dx, dy, dz, fdx, fdy, fdz, best_t,
+                      best_id, best_facing, tb);
+        }
+        if (sp == 0) break;
+        node = stack[(--sp) * stride];
+    }
+    out_id = best_id;
+    out_facing = best_facing;
+    return best_id < 0 ? -1.0 : best_t;
+}
+
 }  // namespace rtsdf

@@ -24,6 +24,7 @@ log = logging.getLogger(__name__)
 DEGENERATE_AREA = 1e-12
 # leaf size of the K6 search tree (binned SAH; csrc/bvh.cu)
 SAH_MAX_LEAF = int(os.environ.get("RTSDF_SAH_LEAF", "4"))
+USE_BVH4 = os.environ.get("RTSDF_BVH4", "1") != "0"
 FACING_NONE = 0
 FACING_FRONT = 1
 FACING_BACK = 2
@@ -177,6 +178,7 @@ class BvhIndex:
     # K6 search tree (binned SAH) in the packed device layout, and its node count
     search: torch.Tensor = dc_field(repr=False, compare=False, default=None)
     search_nodes: int = 0
+    search_nodes4: int = 0  # > 0: BVH4 collapse appended to `search`
 
     @property
     def num_nodes(self):
@@ -231,8 +233,30 @@ def build_bvh(mesh: TriangleMesh) -> BvhIndex:
     sa = np.ascontiguousarray(p0[so])
     search = upload_bvh(slo, shi, sl, sr, so, sa, np.ascontiguousarray(p1[so] - sa),
                         np.ascontiguousarray(p2[so] - sa), np.ascontiguousarray(mesh.normals[so]))
+    # 4-wide collapse of the search tree, appended after the packed layout
+    n4 = 0
+    if USE_BVH4:
+        slo_c, shi_c = np.ascontiguousarray(slo), np.ascontiguousarray(shi)
+        sl_c, sr_c = np.ascontiguousarray(sl), np.ascontiguousarray(sr)
+        nodes4 = np.empty((max(int(ns), 1), 128), dtype=np.uint8)
+        n4 = int(L.rtsdf_bvh4_collapse_host(*[_lib.host_ptr(x) for x in (slo_c, shi_c, sl_c, sr_c)],
+                                            int(ns), _lib.host_ptr(nodes4), nodes4.shape[0]))
+        if n4 > 0 and 3 * _depth4(nodes4[:n4]) < 40:  # RTSDF_FAST_STACK pushes
+            search = torch.cat([search, to_device(nodes4[:n4].reshape(-1))])
+        else:
+            n4 = 0
     return BvhIndex(mesh, node_lo, node_hi, left, right, order, a, e1, e2, tn, packed,
-                    to_device(mesh.normals), search, int(ns))
+                    to_device(mesh.normals), search, int(ns), n4)
+
+
+def _depth4(nodes4: np.ndarray) -> int:
+    child = nodes4.view(np.int32).reshape(-1, 32)[:, 24:28]
+    frontier, depth = np.array([0]), 0
+    while len(frontier):
+        depth += 1
+        c = child[frontier].reshape(-1)
+        frontier = c[(c >= 0) & (c != 0x7FFFFFFF)]
+    return depth
 
 
 def tree_depth(left: np.ndarray, right: np.ndarray) -> int:
@@ -280,8 +304,9 @@ def ray_query_many(bvh: BvhIndex, origins, directions, t_max=np.inf, fast=False)
     ids = torch.empty(n, dtype=torch.int32, device=o.device)
     fac = torch.empty(n, dtype=torch.int32, device=o.device)
     buf, nn = (bvh.search, bvh.search_nodes) if fast else (bvh.packed, bvh.num_nodes)
+    mode = (2 if bvh.search_nodes4 > 0 and fast != "binary" else 1) if fast else 0
     _lib.check(_lib.lib().rtsdf_ray_query(_lib.ptr(buf), nn, bvh.num_tris,
-                                          int(bool(fast)), _lib.ptr(o),
+                                          mode, _lib.ptr(o),
                                           _lib.ptr(d), n, float(t_max), _lib.ptr(t),
                                           _lib.ptr(ids), _lib.ptr(fac), _lib.stream()),
                "ray_query")

@@ -237,7 +237,11 @@ def test_fast_traversal_equals_brute_force(rt, name):
     # a slice of axis-aligned and grazing directions (degenerate slabs)
     d[:500] = np.eye(3)[rng.integers(0, 3, 500)] * rng.choice([-1.0, 1.0], (500, 1))
     t_max = float(np.linalg.norm(hi - lo))
-    tf, idf, ff = rt.ray_query_many(bvh, o, d, t_max, fast=True)
+    assert bvh.search_nodes4 > 0
+    tf, idf, ff = rt.ray_query_many(bvh, o, d, t_max, fast=True)  # BVH4 search
+    tb2, idb2, fb2 = rt.ray_query_many(bvh, o, d, t_max, fast="binary")
+    np.testing.assert_array_equal(idf, idb2)
+    np.testing.assert_array_equal(tf, tb2)
     te, ide, fe = rt.ray_query_many(bvh, o, d, t_max, fast=False)
     np.testing.assert_array_equal(idf, ide)
     np.testing.assert_array_equal(tf, te)
