@@ -187,6 +187,7 @@ __global__ void linear_to_packed_kernel(const int32_t* __restrict__ l, int32_t* 
 }  // namespace rtsdf
 
 #include "jfa2.cuh"
+#include "jfa3.cuh"
 
 namespace rtsdf {
 
@@ -226,7 +227,15 @@ static void launch_pass2(PlaneSrc s, int32_t* dst, float* dst_sdf, const JfaGeom
     cudaMemsetAsync(fix.count, 0, sizeof(int64_t), st);
     int64_t warps = (int64_t)T.nzb * T.jres * T.jgroups * T.ires * T.isegs;
     unsigned blocks = (unsigned)((warps + 3) / 4);
-    if (ry == 4)
+    static const bool v3_off = getenv("RTSDF_JFA_V2") != nullptr;
+    if (!v3_off && jfa3_ok(g)) {  // select-free 5-key pass (jfa3.cuh)
+        if (ry == 4)
+            jfa_pass3_kernel<4, FINAL, SLAB><<<blocks, 128, 0, st>>>(s, dst, dst_sdf, g, T, beta, empty_count, fix);
+        else if (ry == 2)
+            jfa_pass3_kernel<2, FINAL, SLAB><<<blocks, 128, 0, st>>>(s, dst, dst_sdf, g, T, beta, empty_count, fix);
+        else
+            jfa_pass3_kernel<1, FINAL, SLAB><<<blocks, 128, 0, st>>>(s, dst, dst_sdf, g, T, beta, empty_count, fix);
+    } else if (ry == 4)
         jfa_pass2_kernel<4, FINAL, SLAB><<<blocks, 128, 0, st>>>(s, dst, dst_sdf, g, T, beta, empty_count, fix);
     else if (ry == 2)
         jfa_pass2_kernel<2, FINAL, SLAB><<<blocks, 128, 0, st>>>(s, dst, dst_sdf, g, T, beta, empty_count, fix);
