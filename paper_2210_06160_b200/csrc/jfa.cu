@@ -214,7 +214,12 @@ static void launch_pass2(PlaneSrc s, int32_t* dst, float* dst_sdf, const JfaGeom
                          int64_t* empty_count, void* ws, cudaStream_t st) {
     const int k = g.offset;
     const int chain_y = (g.ny + k - 1) / k;  // longest j chain
-    const int ry = chain_y >= 4 ? 4 : (chain_y >= 2 ? 2 : 1);
+    static const int ry_max = [] {
+        const char* e = getenv("RTSDF_JFA_RY");
+        return e ? atoi(e) : 4;
+    }();
+    int ry = chain_y >= 4 ? 4 : (chain_y >= 2 ? 2 : 1);
+    if (ry > ry_max) ry = ry_max >= 2 ? 2 : 1;
     Jfa2Task T;
     T.L = 8;
     T.nzb = (g.nz + 31) / 32;
