@@ -232,8 +232,10 @@ static void launch_pass2(PlaneSrc s, int32_t* dst, float* dst_sdf, const JfaGeom
     cudaMemsetAsync(fix.count, 0, sizeof(int64_t), st);
     int64_t warps = (int64_t)T.nzb * T.jres * T.jgroups * T.ires * T.isegs;
     unsigned blocks = (unsigned)((warps + 3) / 4);
-    static const bool v3_off = getenv("RTSDF_JFA_V2") != nullptr;
-    if (!v3_off && jfa3_ok(g)) {  // select-free 5-key pass (jfa3.cuh)
+    // v3 (select-free 5-key pass, jfa3.cuh) is exact but measured slower than
+    // v2 on B200 (more instructions, 159 registers): opt-in only
+    static const bool v3_on = getenv("RTSDF_JFA_V3") != nullptr;
+    if (v3_on && jfa3_ok(g)) {
         if (ry == 4)
             jfa_pass3_kernel<4, FINAL, SLAB><<<blocks, 128, 0, st>>>(s, dst, dst_sdf, g, T, beta, empty_count, fix);
         else if (ry == 2)
