@@ -31,22 +31,23 @@ struct Jfa2Task {
     int nzb, jres, jgroups, ires, isegs, L;
 };
 
-// One candidate against one output's running (Km, W, tie): 3 predicate
-// compares, a min, a select and two predicated moves.  tie is set when a
-// DIFFERENT seed equals the running minimum and cleared by a strict
-// improvement, so at the end it is set iff >= 2 distinct seeds share the final
-// minimum key.
-__device__ __forceinline__ void jfa2_eval(int K, int32_t v, int& Km, int32_t& W, int& T) {
+// One candidate against one output's running (Km, W): 3 predicate compares, a
+// min, a select and a predicated OR.  The tie flag lives in bit 30 of W
+// (packed seeds are < 2^30): it is set when a DIFFERENT seed equals the running
+// minimum and cleared by a strict improvement (W = v), so at the end it is set
+// iff >= 2 distinct seeds share the final minimum key.  A W carrying the bit
+// compares unequal to every seed, which only re-sets the bit.
+#define JFA2_TIEBIT (1 << 30)
+__device__ __forceinline__ void jfa2_eval(int K, int32_t v, int& Km, int32_t& W) {
     asm volatile(
         "{\n\t.reg .pred plt, peq;\n\t"
-        "setp.lt.s32 plt, %3, %0;\n\t"
-        "setp.eq.s32 peq, %3, %0;\n\t"
-        "setp.ne.and.s32 peq, %4, %1, peq;\n\t"
-        "min.s32 %0, %0, %3;\n\t"
-        "selp.b32 %1, %4, %1, plt;\n\t"
-        "@peq mov.b32 %2, 1;\n\t"
-        "@plt mov.b32 %2, 0;\n\t}"
-        : "+r"(Km), "+r"(W), "+r"(T)
+        "setp.lt.s32 plt, %2, %0;\n\t"
+        "setp.eq.s32 peq, %2, %0;\n\t"
+        "setp.ne.and.s32 peq, %3, %1, peq;\n\t"
+        "min.s32 %0, %0, %2;\n\t"
+        "selp.b32 %1, %3, %1, plt;\n\t"
+        "@peq or.b32 %1, %1, 0x40000000;\n\t}"
+        : "+r"(Km), "+r"(W)
         : "r"(K), "r"(v));
 }
 
@@ -85,15 +86,13 @@ __global__ void __launch_bounds__(128) jfa_pass2_kernel(PlaneSrc src, int32_t* _
     const int gxk = 2 * g.wx * k, gyk = 2 * g.wy * k;
 
     int Km[3][RY];
-    int32_t W[3][RY];
-    int tie[3][RY];
+    int32_t W[3][RY];  // winner, tie flag in bit 30 (jfa2_eval)
 #pragma unroll
     for (int s = 0; s < 3; ++s)
 #pragma unroll
         for (int b = 0; b < RY; ++b) {
             Km[s][b] = 0x7fffffff;
             W[s][b] = RTSDF_EMPTY;
-            tie[s][b] = 0;
         }
 
     // the in-plane offsets of the (RY + 2) x 3 taps and their validity are
@@ -162,7 +161,7 @@ __global__ void __launch_bounds__(128) jfa_pass2_kernel(PlaneSrc src, int32_t* _
                         const int b = bt + db;
                         if (b < 0 || b >= RY) continue;  // compile-time
                         const int K = db == 0 ? Bs[s] : (db < 0 ? Bs[s] + Gy : Bs[s] - Gy);
-                        jfa2_eval(K, v, Km[s][b], W[s][b], tie[s][b]);
+                        jfa2_eval(K, v, Km[s][b], W[s][b]);
                     }
                 }
             }
@@ -176,7 +175,9 @@ __global__ void __launch_bounds__(128) jfa_pass2_kernel(PlaneSrc src, int32_t* _
                 const int oj = j_base + b * k;
                 const bool live = zok && oj < g.ny;
                 const int64_t cell = (int64_t)(oi - g.x0) * plane + (int64_t)oj * g.nz + z;
-                const int32_t w = W[0][b];
+                const int32_t wt = W[0][b];
+                const bool tie = wt != RTSDF_EMPTY && (wt & JFA2_TIEBIT);
+                const int32_t w = wt == RTSDF_EMPTY ? wt : (wt & ~JFA2_TIEBIT);
                 if (live) {
                     if (FINAL) {
                         empties += w == RTSDF_EMPTY;
@@ -188,7 +189,7 @@ __global__ void __launch_bounds__(128) jfa_pass2_kernel(PlaneSrc src, int32_t* _
                     }
                 }
                 // integer tie between distinct seeds: defer to the exact rule
-                const bool flag = live && tie[0][b];
+                const bool flag = live && tie;
                 const unsigned m = __ballot_sync(0xffffffffu, flag);
                 if (m) {
                     int64_t base = 0;
@@ -206,13 +207,10 @@ __global__ void __launch_bounds__(128) jfa_pass2_kernel(PlaneSrc src, int32_t* _
         for (int b = 0; b < RY; ++b) {
             Km[0][b] = Km[1][b];
             W[0][b] = W[1][b];
-            tie[0][b] = tie[1][b];
             Km[1][b] = Km[2][b];
             W[1][b] = W[2][b];
-            tie[1][b] = tie[2][b];
             Km[2][b] = 0x7fffffff;
             W[2][b] = RTSDF_EMPTY;
-            tie[2][b] = false;
         }
 #pragma unroll
         for (int bt = 0; bt < RY + 2; ++bt)
