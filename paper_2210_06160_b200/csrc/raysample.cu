@@ -237,6 +237,51 @@ __global__ void __launch_bounds__(WF_THREADS, 8) wf_pass2_kernel(SampleParams P,
     }
 }
 
+// Persistent tracer (default with the BVH4): every lane owns one ray at a time
+// and advances it one node visit / leaf per iteration; as soon as a lane's ray
+// completes it writes the per-ray result and the idle lanes of the warp fetch
+// the next rays from a global counter (one warp-aggregated atomic).  Short and
+// long rays no longer share a warp's lifetime, so lanes stay busy until the
+// whole ray set drains (the budgeted two-pass wavefront still left pass 2 at
+// 26 % SIMD efficiency).  Ray ids are fetched in order, so a warp keeps working
+// on neighbouring texels.
+__global__ void __launch_bounds__(WF_THREADS, 8) wf_persist4_kernel(SampleParams P, WfBuffers B) {
+    __shared__ int32_t stack_mem[RTSDF_FAST_STACK * WF_THREADS];
+    int32_t* stack = stack_mem + threadIdx.x;
+    const int lane = threadIdx.x & 31;
+    const int64_t R = min(*P.count, P.m_cap) * P.x;
+    int64_t r = -1;  // current ray; -1 idle, -2 drained
+    Trace4State s;
+    while (true) {
+        const bool idle = r == -1;
+        const unsigned m = __ballot_sync(0xffffffffu, idle);
+        if (m) {
+            int64_t base = 0;
+            if (lane == (__ffs(m) - 1))
+                base = (int64_t)atomicAdd((unsigned long long*)B.qcount, (unsigned long long)__popc(m));
+            base = __shfl_sync(0xffffffffu, base, __ffs(m) - 1);
+            if (idle) {
+                const int64_t rr = base + __popc(m & ((1u << lane) - 1));
+                if (rr < R) {
+                    double ox, oy, oz, dx, dy, dz;
+                    wf_ray(P, rr, ox, oy, oz, dx, dy, dz);
+                    trace4_init(s, ox, oy, oz, dx, dy, dz, P.t_max);
+                    r = rr;
+                } else {
+                    r = -2;
+                }
+            }
+        }
+        if (__all_sync(0xffffffffu, r == -2)) break;
+        if (r >= 0 && trace4_step(P.bvh4, s, stack, WF_THREADS)) {
+            const bool hit = s.best_id >= 0;
+            B.t[r] = hit ? s.best_t : -1.0;
+            B.facing[r] = (uint8_t)(hit ? s.best_facing : 0);
+            r = -1;
+        }
+    }
+}
+
 // raysample.py:140-152 (per-texel min / votes, in ray order) + :229-244 (Eq. 1)
 __global__ void __launch_bounds__(WF_THREADS) wf_reduce_update_kernel(SampleParams P, WfBuffers B) {
     const int64_t M = min(*P.count, P.m_cap);
@@ -524,7 +569,11 @@ extern "C" int rtsdf_sample_update(const void* bvh_packed, int64_t n_nodes, int6
         }();
         const int budget = budget_env > 0 ? budget_env : (wide ? WF_BUDGET4 : WF_BUDGET);
         const unsigned b1 = (unsigned)(blocks < cap ? blocks : cap), b2 = (unsigned)(num_sms() * 12);
-        if (wide) {
+        static const bool two_pass = getenv("RTSDF_WF_TWOPASS") != nullptr;
+        if (wide && !two_pass) {
+            P.bvh4 = fast_bvh4_view(bvh_packed, n_nodes, n_tris);
+            wf_persist4_kernel<<<(unsigned)(num_sms() * 8), WF_THREADS, 0, st>>>(P, B);
+        } else if (wide) {
             P.bvh4 = fast_bvh4_view(bvh_packed, n_nodes, n_tris);
             wf_pass1_kernel<true><<<b1, WF_THREADS, 0, st>>>(P, B, budget);
             wf_pass2_kernel<true><<<b2, WF_THREADS, 0, st>>>(P, B);
