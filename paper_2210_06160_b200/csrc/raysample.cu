@@ -569,8 +569,10 @@ extern "C" int rtsdf_sample_update(const void* bvh_packed, int64_t n_nodes, int6
         }();
         const int budget = budget_env > 0 ? budget_env : (wide ? WF_BUDGET4 : WF_BUDGET);
         const unsigned b1 = (unsigned)(blocks < cap ? blocks : cap), b2 = (unsigned)(num_sms() * 12);
-        static const bool two_pass = getenv("RTSDF_WF_TWOPASS") != nullptr;
-        if (wide && !two_pass) {
+        // persistent per-lane-refill tracer: exact, but measured slower than the
+        // two-pass wavefront on B200 (6.67 vs 6.32 ms at C3), so opt-in only
+        static const bool persist = getenv("RTSDF_WF_PERSIST") != nullptr;
+        if (wide && persist) {
             P.bvh4 = fast_bvh4_view(bvh_packed, n_nodes, n_tris);
             wf_persist4_kernel<<<(unsigned)(num_sms() * 8), WF_THREADS, 0, st>>>(P, B);
         } else if (wide) {
