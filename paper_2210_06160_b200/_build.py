@@ -47,7 +47,8 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     if not force and not needs_build():
         return LIB
     tmp = LIB.with_suffix(".so.tmp")
-    cmd = [nvcc(), *NVCC_FLAGS, "-I", str(ROOT / "include"), "-o", str(tmp),
+    extra = os.environ.get("RTSDF_NVCC_EXTRA", "").split()  # experiments, e.g. -DWF_MINB=6
+    cmd = [nvcc(), *NVCC_FLAGS, *extra, "-I", str(ROOT / "include"), "-o", str(tmp),
            *[str(CSRC / s) for s in SOURCES], "-lcudart"]
     res = subprocess.run(cmd, capture_output=True, text=True)
     log = (res.stdout or "") + (res.stderr or "")

@@ -316,13 +316,14 @@ __global__ void __launch_bounds__(128) ray_query_fast4_kernel(
     double t_max, double* __restrict__ out_t, int32_t* __restrict__ out_id,
     int32_t* __restrict__ out_facing) {
     __shared__ int32_t stack_mem[RTSDF_FAST_STACK * 128];
+    __shared__ __half tstack_mem[RTSDF_FAST_STACK * 128];
     int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (q >= n) return;
     int32_t id;
     int facing;
     double t = trace_fast4(b, orig[3 * q], orig[3 * q + 1], orig[3 * q + 2], dirs[3 * q],
-                           dirs[3 * q + 1], dirs[3 * q + 2], t_max, stack_mem + threadIdx.x, 128,
-                           id, facing);
+                           dirs[3 * q + 1], dirs[3 * q + 2], t_max, stack_mem + threadIdx.x,
+                           tstack_mem + threadIdx.x, 128, id, facing);
     out_t[q] = t;
     out_id[q] = id;
     out_facing[q] = facing;

@@ -224,39 +224,60 @@ __global__ void __launch_bounds__(128) jfa_pass2_kernel(PlaneSrc src, int32_t* _
 }
 
 // Re-decide the flagged cells with the reference's exact rule (jfa.py:108-124).
+// The 27 taps are gathered as independent loads first; the integer key then
+// pre-filters them: a strictly larger integer key is a strictly larger exact
+// d2, which fp64 rounding cannot invert (relative gap >= 2^-29), so the fp64
+// argmin lies among the taps at the minimum integer key -- only those pay fp64.
 template <bool FINAL, bool SLAB>
 __global__ void __launch_bounds__(128) jfa_fixup_kernel(PlaneSrc src, int32_t* __restrict__ dst,
                                                         float* __restrict__ dst_sdf, JfaGeom g,
                                                         double beta, JfaFixList fix) {
     const int64_t n = min(*fix.count, fix.cap);
     const int64_t plane = (int64_t)g.ny * g.nz;
+    const int k = g.offset;
     for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n;
          q += (int64_t)gridDim.x * blockDim.x) {
         const int32_t cell = fix.cells[q];
         const int il = (int)(cell / plane);
-        const int j = (int)((cell / g.nz) % g.ny), z = (int)(cell % g.nz);
+        const int rem = (int)(cell - (int64_t)il * plane);
+        const int j = rem / g.nz, z = rem - (rem / g.nz) * g.nz;
         const int i = g.x0 + il;
+        int32_t c[27];
+#pragma unroll
+        for (int di = 0; di < 3; ++di) {
+            const int qi = i + (di - 1) * k;
+            const int32_t* pl = nullptr;
+            if (qi >= 0 && qi < g.nx)
+                pl = SLAB ? plane_ptr(src, g, qi, plane) : src.local + (int64_t)qi * plane;
+#pragma unroll
+            for (int dj = 0; dj < 3; ++dj) {
+                const int qj = j + (dj - 1) * k;
+#pragma unroll
+                for (int dk = 0; dk < 3; ++dk) {
+                    const int qk = z + (dk - 1) * k;
+                    const bool ok = pl != nullptr && qj >= 0 && qj < g.ny && qk >= 0 && qk < g.nz;
+                    c[(di * 3 + dj) * 3 + dk] = ok ? __ldg(pl + (int64_t)qj * g.nz + qk) : RTSDF_EMPTY;
+                }
+            }
+        }
+        int key[27];
+        int km = 0x7fffffff;
+#pragma unroll
+        for (int t = 0; t < 27; ++t) {
+            const int dx = i - unpack_i(c[t]), dy = j - unpack_j(c[t]), dz = z - unpack_k(c[t]);
+            key[t] = c[t] == RTSDF_EMPTY ? 0x7fffffff : g.wx * dx * dx + g.wy * dy * dy + g.wz * dz * dz;
+            km = min(km, key[t]);
+        }
         int32_t best = RTSDF_EMPTY;
         double bd = 1e300;
-        for (int di = -1; di <= 1; ++di) {
-            const int qi = i + di * g.offset;
-            if (qi < 0 || qi >= g.nx) continue;
-            const int32_t* pl = SLAB ? plane_ptr(src, g, qi, plane) : src.local + (int64_t)qi * plane;
-            for (int dj = -1; dj <= 1; ++dj) {
-                const int qj = j + dj * g.offset;
-                if (qj < 0 || qj >= g.ny) continue;
-                for (int dk = -1; dk <= 1; ++dk) {
-                    const int qk = z + dk * g.offset;
-                    if (qk < 0 || qk >= g.nz) continue;
-                    const int32_t c = __ldg(pl + (int64_t)qj * g.nz + qk);
-                    if (c == RTSDF_EMPTY || c == best) continue;
-                    double d2 = center_d2(i - unpack_i(c), j - unpack_j(c), z - unpack_k(c), g.hx,
-                                          g.hy, g.hz);
-                    if (d2 < bd || (d2 == bd && best != RTSDF_EMPTY && c < best)) {
-                        best = c;
-                        bd = d2;
-                    }
-                }
+#pragma unroll
+        for (int t = 0; t < 27; ++t) {
+            if (key[t] != km || c[t] == RTSDF_EMPTY || c[t] == best) continue;
+            const double d2 = center_d2(i - unpack_i(c[t]), j - unpack_j(c[t]), z - unpack_k(c[t]),
+                                        g.hx, g.hy, g.hz);
+            if (d2 < bd || (d2 == bd && best != RTSDF_EMPTY && c[t] < best)) {
+                best = c[t];
+                bd = d2;
             }
         }
         if (FINAL)

@@ -25,6 +25,7 @@ struct SampleParams {
     int fnx, fny, fnz;
     double fhx, fhy, fhz;
     int x;
+    FastDiv div_x, div_ny, div_nz;  // wavefront ray-index decode
     uint64_t seed;
     int64_t frame;
     double t_max;
@@ -141,6 +142,9 @@ __global__ void __launch_bounds__(SAMPLE_THREADS) sample_update_kernel(SamplePar
 // applies the Eq. 1 update.  The queue order varies run to run but every ray's
 // result is deterministic, and the per-texel reduction order is fixed.
 #define WF_THREADS 128
+#ifndef WF_MINB
+#define WF_MINB 6  // resident blocks per SM the tracer kernels are compiled for
+#endif
 #define WF_BUDGET 4   // binary search tree: internal-node visits in pass 1
 #define WF_BUDGET4 3  // BVH4
 
@@ -154,13 +158,12 @@ struct WfBuffers {
 __device__ __forceinline__ void wf_ray(const SampleParams& P, int64_t r, double& ox, double& oy,
                                        double& oz, double& dx, double& dy, double& dz) {
     // 32-bit index math: rays < 2^31 (host-checked) and cells <= 1024^3
-    const unsigned x = (unsigned)P.x;
-    const unsigned n = (unsigned)r / x;
-    const int ray = (int)((unsigned)r - n * x);
+    const unsigned n = fdiv((unsigned)r, P.div_x);
+    const int ray = (int)((unsigned)r - n * P.div_x.d);
     const unsigned lin = (unsigned)__ldg(P.idx + n);
-    const unsigned nz = (unsigned)P.fnz, ny = (unsigned)P.fny;
-    const unsigned q = lin / nz;
-    const int k = (int)(lin - q * nz), j = (int)(q % ny), i = (int)(q / ny);
+    const unsigned q = fdiv(lin, P.div_nz);
+    const unsigned i = fdiv(q, P.div_ny);
+    const int k = (int)(lin - q * P.div_nz.d), j = (int)(q - i * P.div_ny.d);
     ox = P.coarse.lox + ((double)i + 0.5) * P.fhx;  // raysample.py:167-169
     oy = P.coarse.loy + ((double)j + 0.5) * P.fhy;
     oz = P.coarse.loz + ((double)k + 0.5) * P.fhz;
@@ -178,17 +181,19 @@ __device__ __forceinline__ void wf_ray(const SampleParams& P, int64_t r, double&
 template <bool WIDE>
 __device__ __forceinline__ double wf_trace(const SampleParams& P, double ox, double oy, double oz,
                                            double dx, double dy, double dz, int32_t* stack,
-                                           int32_t& id, int& facing, int budget, bool* done) {
+                                           __half* tstack, int32_t& id, int& facing, int budget,
+                                           bool* done) {
     if (WIDE)
-        return trace_fast4(P.bvh4, ox, oy, oz, dx, dy, dz, P.t_max, stack, WF_THREADS, id, facing,
-                           budget, done);
+        return trace_fast4(P.bvh4, ox, oy, oz, dx, dy, dz, P.t_max, stack, tstack, WF_THREADS, id,
+                           facing, budget, done);
     return trace_fast(P.bvh, ox, oy, oz, dx, dy, dz, P.t_max, stack, WF_THREADS, id, facing,
                       budget, done);
 }
 
 template <bool WIDE>
-__global__ void __launch_bounds__(WF_THREADS, 8) wf_pass1_kernel(SampleParams P, WfBuffers B, int budget) {
+__global__ void __launch_bounds__(WF_THREADS, WF_MINB) wf_pass1_kernel(SampleParams P, WfBuffers B, int budget) {
     __shared__ int32_t stack_mem[RTSDF_FAST_STACK * WF_THREADS];
+    __shared__ __half tstack_mem[WIDE ? RTSDF_FAST_STACK * WF_THREADS : 1];
     const int lane = threadIdx.x & 31;
     const int64_t R = min(*P.count, P.m_cap) * P.x;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -201,8 +206,8 @@ __global__ void __launch_bounds__(WF_THREADS, 8) wf_pass1_kernel(SampleParams P,
             int32_t id;
             int facing;
             bool done;
-            double t = wf_trace<WIDE>(P, ox, oy, oz, dx, dy, dz, stack_mem + threadIdx.x, id,
-                                      facing, budget, &done);
+            double t = wf_trace<WIDE>(P, ox, oy, oz, dx, dy, dz, stack_mem + threadIdx.x,
+                                      tstack_mem + threadIdx.x, id, facing, budget, &done);
             if (done) {
                 B.t[r] = id >= 0 ? t : -1.0;
                 B.facing[r] = (uint8_t)(id >= 0 ? facing : 0);
@@ -220,8 +225,9 @@ __global__ void __launch_bounds__(WF_THREADS, 8) wf_pass1_kernel(SampleParams P,
 }
 
 template <bool WIDE>
-__global__ void __launch_bounds__(WF_THREADS, 8) wf_pass2_kernel(SampleParams P, WfBuffers B) {
+__global__ void __launch_bounds__(WF_THREADS, WF_MINB) wf_pass2_kernel(SampleParams P, WfBuffers B) {
     __shared__ int32_t stack_mem[RTSDF_FAST_STACK * WF_THREADS];
+    __shared__ __half tstack_mem[WIDE ? RTSDF_FAST_STACK * WF_THREADS : 1];
     const int64_t Q = *B.qcount;
     for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < Q;
          q += (int64_t)gridDim.x * blockDim.x) {
@@ -230,14 +236,14 @@ __global__ void __launch_bounds__(WF_THREADS, 8) wf_pass2_kernel(SampleParams P,
         wf_ray(P, r, ox, oy, oz, dx, dy, dz);
         int32_t id;
         int facing;
-        double t = wf_trace<WIDE>(P, ox, oy, oz, dx, dy, dz, stack_mem + threadIdx.x, id, facing,
-                                  0, nullptr);
+        double t = wf_trace<WIDE>(P, ox, oy, oz, dx, dy, dz, stack_mem + threadIdx.x,
+                                  tstack_mem + threadIdx.x, id, facing, 0, nullptr);
         B.t[r] = id >= 0 ? t : -1.0;
         B.facing[r] = (uint8_t)(id >= 0 ? facing : 0);
     }
 }
 
-// Persistent tracer (default with the BVH4): every lane owns one ray at a time
+// Persistent tracer (opt-in, RTSDF_WF_PERSIST): every lane owns one ray at a time
 // and advances it one node visit / leaf per iteration; as soon as a lane's ray
 // completes it writes the per-ray result and the idle lanes of the warp fetch
 // the next rays from a global counter (one warp-aggregated atomic).  Short and
@@ -245,7 +251,7 @@ __global__ void __launch_bounds__(WF_THREADS, 8) wf_pass2_kernel(SampleParams P,
 // whole ray set drains (the budgeted two-pass wavefront still left pass 2 at
 // 26 % SIMD efficiency).  Ray ids are fetched in order, so a warp keeps working
 // on neighbouring texels.
-__global__ void __launch_bounds__(WF_THREADS, 8) wf_persist4_kernel(SampleParams P, WfBuffers B) {
+__global__ void __launch_bounds__(WF_THREADS, WF_MINB) wf_persist4_kernel(SampleParams P, WfBuffers B) {
     __shared__ int32_t stack_mem[RTSDF_FAST_STACK * WF_THREADS];
     int32_t* stack = stack_mem + threadIdx.x;
     const int lane = threadIdx.x & 31;
@@ -524,6 +530,9 @@ extern "C" int rtsdf_sample_update(const void* bvh_packed, int64_t n_nodes, int6
     P.fhy = rs->fh[1];
     P.fhz = rs->fh[2];
     P.x = x;
+    P.div_x = make_fastdiv((uint32_t)(x > 0 ? x : 1));
+    P.div_ny = make_fastdiv((uint32_t)rs->fny);
+    P.div_nz = make_fastdiv((uint32_t)rs->fnz);
     P.seed = seed;
     P.frame = frame;
     P.t_max = t_max;

@@ -16,6 +16,8 @@
 // Hence the visited set covers everything that can change the answer and
 // every accepted hit is the reference's bit-exact fp64 (t, id, facing).
 #pragma once
+#include <cuda_fp16.h>
+
 #include "common.cuh"
 
 #define RTSDF_FAST_STACK 40  // the host rejects search trees deeper than this
@@ -69,10 +71,16 @@ struct RayF {
     float oix, oiy, oiz;  // origin * reciprocal
 };
 
+// The reciprocal only steers the conservative box pre-test: MUFU.RCP's <= 1 ulp
+// error is far inside the 1e-5 * scene-scale box padding, and every hit is
+// confirmed in exact fp64, so the approximate reciprocal cannot change a result.
+// For a (near-)zero component the sign of the 1e30 stand-in is irrelevant: the
+// slab interval is [min, max] of the two planes either way.
 __device__ __forceinline__ float clamp_inv(double d) {
-    float f = (float)d;
-    if (fabsf(f) < 1e-30f) return d >= 0.0 ? 1e30f : -1e30f;
-    float r = 1.0f / f;
+    const float f = (float)d;
+    float r;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(f));
+    r = fabsf(f) < 1e-30f ? copysignf(1e30f, f) : r;
     return fminf(fmaxf(r, -1e30f), 1e30f);
 }
 
@@ -351,10 +359,14 @@ __device__ __forceinline__ bool trace4_step(const FastBvh4& b, Trace4State& s, i
     return false;
 }
 
+// Each stack entry carries its box entry distance (fp16, rounded down: a lower
+// bound), and a popped entry is skipped once it lies beyond the current best
+// hit's fp32 upper bound tb -- the same conservative test box_entry applied at
+// push time, with the tighter tb found since (ties at t == best_t survive).
 __device__ __forceinline__ double trace_fast4(const FastBvh4& b, double ox, double oy, double oz,
                                               double dx, double dy, double dz, double t_max,
-                                              int32_t* stack, int stride, int32_t& out_id,
-                                              int& out_facing, int budget = 0,
+                                              int32_t* stack, __half* tstack, int stride,
+                                              int32_t& out_id, int& out_facing, int budget = 0,
                                               bool* complete = nullptr) {
     RayF r;
     r.ix = clamp_inv(dx);
@@ -387,7 +399,28 @@ __device__ __forceinline__ double trace_fast4(const FastBvh4& b, double ox, doub
             t[1] = box_entry(lx.y, ly.y, lz.y, hx.y, hy.y, hz.y, r, tb);
             t[2] = box_entry(lx.z, ly.z, lz.z, hx.z, hy.z, hz.z, r, tb);
             t[3] = box_entry(lx.w, ly.w, lz.w, hx.w, hy.w, hz.w, r, tb);
-            const int32_t c[4] = {ch.x, ch.y, ch.z, ch.w};
+            int32_t c[4] = {ch.x, ch.y, ch.z, ch.w};
+#ifdef RTSDF_T4_SORT
+            // farthest first, so the nearest remaining hit is popped next
+#define T4_CE(a, b_)                                   \
+    if (t[a] < t[b_]) {                                \
+        const float tt = t[a];                         \
+        t[a] = t[b_];                                  \
+        t[b_] = tt;                                    \
+        const int32_t cc = c[a];                       \
+        c[a] = c[b_];                                  \
+        c[b_] = cc;                                    \
+    }
+            T4_CE(0, 1) T4_CE(2, 3) T4_CE(0, 2) T4_CE(1, 3) T4_CE(1, 2)
+#undef T4_CE
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+                if (t[q] != RTSDF_FINF) {
+                    stack[sp * stride] = c[q];
+                    tstack[sp * stride] = __float2half_rd(t[q]);
+                    ++sp;
+                }
+#else
             // nearest hit child is visited next; the other hits go on the stack
             int nearest = -1;
             float tn = RTSDF_FINF;
@@ -399,17 +432,30 @@ __device__ __forceinline__ double trace_fast4(const FastBvh4& b, double ox, doub
                 }
 #pragma unroll
             for (int q = 0; q < 4; ++q)
-                if (q != nearest && t[q] != RTSDF_FINF) stack[(sp++) * stride] = c[q];
+                if (q != nearest && t[q] != RTSDF_FINF) {
+                    stack[sp * stride] = c[q];
+                    tstack[sp * stride] = __float2half_rd(t[q]);
+                    ++sp;
+                }
             if (nearest >= 0) {
                 node = c[nearest];
                 continue;
             }
+#endif
         } else {
             leaf_tris(b.tris, b.exact, node, ox, oy, oz, dx, dy, dz, fdx, fdy, fdz, best_t,
                       best_id, best_facing, tb);
         }
-        if (sp == 0) break;
-        node = stack[(--sp) * stride];
+        bool more = false;
+        while (sp > 0) {
+            --sp;
+            if (__half2float(tstack[sp * stride]) <= tb) {
+                node = stack[sp * stride];
+                more = true;
+                break;
+            }
+        }
+        if (!more) break;
     }
     out_id = best_id;
     out_facing = best_facing;
