@@ -79,34 +79,37 @@ struct FieldView {
 __device__ __forceinline__ double dmin_(double a, double b) { return a < b ? a : b; }
 __device__ __forceinline__ double dmax_(double a, double b) { return a > b ? a : b; }
 
-__device__ __forceinline__ double trilinear(const FieldView& f, double px, double py,
-                                            double pz) {
-    double gx = __dsub_rn(__ddiv_rn(__dsub_rn(px, f.lox), f.hx), 0.5);
-    double gy = __dsub_rn(__ddiv_rn(__dsub_rn(py, f.loy), f.hy), 0.5);
-    double gz = __dsub_rn(__ddiv_rn(__dsub_rn(pz, f.loz), f.hz), 0.5);
-    gx = dmin_(dmax_(gx, 0.0), (double)f.nx - 1.0);
-    gy = dmin_(dmax_(gy, 0.0), (double)f.ny - 1.0);
-    gz = dmin_(dmax_(gz, 0.0), (double)f.nz - 1.0);
-    int ix = f.nx > 1 ? min((int)gx, f.nx - 2) : 0;
-    int iy = f.ny > 1 ? min((int)gy, f.ny - 2) : 0;
-    int iz = f.nz > 1 ? min((int)gz, f.nz - 2) : 0;
-    double fx = __dsub_rn(gx, (double)ix);
-    double fy = __dsub_rn(gy, (double)iy);
-    double fz = __dsub_rn(gz, (double)iz);
-    int jx = f.nx > 1 ? ix + 1 : ix;
-    int jy = f.ny > 1 ? iy + 1 : iy;
-    int jz = f.nz > 1 ? iz + 1 : iz;
+// One axis of the trilinear lookup: the lower corner index i, the upper j and
+// the fraction f (field.py:104-118 for a single coordinate).
+struct AxisW {
+    int i, j;
+    double f;
+};
+
+__device__ __forceinline__ AxisW axis_weight(double p, double lo, double h, int n) {
+    double g = __dsub_rn(__ddiv_rn(__dsub_rn(p, lo), h), 0.5);
+    g = dmin_(dmax_(g, 0.0), (double)n - 1.0);
+    AxisW w;
+    w.i = n > 1 ? min((int)g, n - 2) : 0;
+    w.f = __dsub_rn(g, (double)w.i);
+    w.j = n > 1 ? w.i + 1 : w.i;
+    return w;
+}
+
+__device__ __forceinline__ double trilinear_w(const FieldView& f, const AxisW& x, const AxisW& y,
+                                              const AxisW& z) {
     const int64_t sx = (int64_t)f.ny * f.nz, sy = f.nz;
     const float* d = f.data;
     const float b = f.bias;
-    double c000 = __fsub_rn(__ldg(d + ix * sx + iy * sy + iz), b);
-    double c100 = __fsub_rn(__ldg(d + jx * sx + iy * sy + iz), b);
-    double c010 = __fsub_rn(__ldg(d + ix * sx + jy * sy + iz), b);
-    double c110 = __fsub_rn(__ldg(d + jx * sx + jy * sy + iz), b);
-    double c001 = __fsub_rn(__ldg(d + ix * sx + iy * sy + jz), b);
-    double c101 = __fsub_rn(__ldg(d + jx * sx + iy * sy + jz), b);
-    double c011 = __fsub_rn(__ldg(d + ix * sx + jy * sy + jz), b);
-    double c111 = __fsub_rn(__ldg(d + jx * sx + jy * sy + jz), b);
+    double c000 = __fsub_rn(__ldg(d + x.i * sx + y.i * sy + z.i), b);
+    double c100 = __fsub_rn(__ldg(d + x.j * sx + y.i * sy + z.i), b);
+    double c010 = __fsub_rn(__ldg(d + x.i * sx + y.j * sy + z.i), b);
+    double c110 = __fsub_rn(__ldg(d + x.j * sx + y.j * sy + z.i), b);
+    double c001 = __fsub_rn(__ldg(d + x.i * sx + y.i * sy + z.j), b);
+    double c101 = __fsub_rn(__ldg(d + x.j * sx + y.i * sy + z.j), b);
+    double c011 = __fsub_rn(__ldg(d + x.i * sx + y.j * sy + z.j), b);
+    double c111 = __fsub_rn(__ldg(d + x.j * sx + y.j * sy + z.j), b);
+    const double fx = x.f, fy = y.f, fz = z.f;
     double ofx = __dsub_rn(1.0, fx), ofy = __dsub_rn(1.0, fy), ofz = __dsub_rn(1.0, fz);
     double c00 = __dadd_rn(__dmul_rn(c000, ofx), __dmul_rn(c100, fx));
     double c10 = __dadd_rn(__dmul_rn(c010, ofx), __dmul_rn(c110, fx));
@@ -115,6 +118,12 @@ __device__ __forceinline__ double trilinear(const FieldView& f, double px, doubl
     double c0 = __dadd_rn(__dmul_rn(c00, ofy), __dmul_rn(c10, fy));
     double c1 = __dadd_rn(__dmul_rn(c01, ofy), __dmul_rn(c11, fy));
     return __dadd_rn(__dmul_rn(c0, ofz), __dmul_rn(c1, fz));
+}
+
+__device__ __forceinline__ double trilinear(const FieldView& f, double px, double py,
+                                            double pz) {
+    return trilinear_w(f, axis_weight(px, f.lox, f.hx, f.nx), axis_weight(py, f.loy, f.hy, f.ny),
+                       axis_weight(pz, f.loz, f.hz, f.nz));
 }
 
 // ---- rng.py:18-53 counter-based SplitMix64 --------------------------------------

@@ -146,7 +146,7 @@ __global__ void __launch_bounds__(SAMPLE_THREADS) sample_update_kernel(SamplePar
 #define WF_MINB 6  // resident blocks per SM the tracer kernels are compiled for
 #endif
 #define WF_BUDGET 4   // binary search tree: internal-node visits in pass 1
-#define WF_BUDGET4 3  // BVH4
+#define WF_BUDGET4 2  // BVH4: root only (ground-plane leaves finish in pass 1)
 
 struct WfBuffers {
     double* t;        // [R] hit t, or -1 (miss)

@@ -11,8 +11,9 @@
 #include "common.cuh"
 
 #define RS_THREADS 256
-#define RS_PER_THREAD 8
+#define RS_PER_THREAD 16
 #define RS_CELLS_PER_BLOCK (RS_THREADS * RS_PER_THREAD)
+#define RS_TAB 1024  // per-axis weight table entries (dims <= 1024)
 
 namespace rtsdf {
 
@@ -22,34 +23,85 @@ struct RsParams {
     double fhx, fhy, fhz;
     double d;
     int64_t n_cells;
+    FastDiv div_ny, div_nz;
 };
 
-__device__ __forceinline__ double resample_at(const RsParams& P, int64_t c) {
-    const int64_t nyz = (int64_t)P.fny * P.fnz;
-    int i = (int)(c / nyz);
-    int64_t r = c - (int64_t)i * nyz;
-    int j = (int)(r / P.fnz);
-    int k = (int)(r - (int64_t)j * P.fnz);
-    // raysample.py:97-101: fine centres measured from the COARSE lo
-    double px = P.coarse.lox + ((double)i + 0.5) * P.fhx;
-    double py = P.coarse.loy + ((double)j + 0.5) * P.fhy;
-    double pz = P.coarse.loz + ((double)k + 0.5) * P.fhz;
-    return trilinear(P.coarse, px, py, pz);
+// raysample.py:97-101: fine centres measured from the COARSE lo, then the
+// trilinear axis weights (field.py:104-118) -- a function of one index only.
+__device__ __forceinline__ AxisW fine_axis(double clo, double fh, double ch, int cn, int idx) {
+    return axis_weight(clo + ((double)idx + 0.5) * fh, clo, ch, cn);
 }
 
+__device__ __forceinline__ void cell_ijk(const RsParams& P, uint32_t c, int& i, int& j, int& k) {
+    const uint32_t q = fdiv(c, P.div_nz);
+    k = (int)(c - q * P.div_nz.d);
+    i = (int)fdiv(q, P.div_ny);
+    j = (int)(q - (uint32_t)i * P.div_ny.d);
+}
+
+// Each block owns RS_CELLS_PER_BLOCK consecutive cells.  The axis weights of
+// the planes / rows / columns the block touches are computed once into shared
+// tables (3 fp64 divisions per table entry instead of per cell), so the cell
+// loop is 8 gathers + 7 fp64 lerps; identical arithmetic, identical bits.
 __global__ void __launch_bounds__(RS_THREADS) resample_mask_kernel(
     RsParams P, float* __restrict__ c_fine, float* __restrict__ out_unmasked,
     uint8_t* __restrict__ mask_new, int32_t* __restrict__ block_counts,
     const uint8_t* __restrict__ mask_old, float* __restrict__ run_min,
     int32_t* __restrict__ front, int32_t* __restrict__ back) {
     __shared__ int warp_sum[RS_THREADS / 32];
+    __shared__ double tf[3][RS_TAB];
+    __shared__ int ti[3][RS_TAB];
     const int64_t base = (int64_t)blockIdx.x * RS_CELLS_PER_BLOCK;
+    const int64_t last = min(base + RS_CELLS_PER_BLOCK, P.n_cells) - 1;
+    int i0, j0, k0, i1, j1, k1;
+    cell_ijk(P, (uint32_t)base, i0, j0, k0);
+    cell_ijk(P, (uint32_t)last, i1, j1, k1);
+    // index ranges touched by [base, last]
+    const int xs = i0, xn = i1 - i0 + 1;
+    const int ys = i0 == i1 ? j0 : 0, yn = i0 == i1 ? j1 - j0 + 1 : P.fny;
+    const int zs = (i0 == i1 && j0 == j1) ? k0 : 0, zn = (i0 == i1 && j0 == j1) ? k1 - k0 + 1 : P.fnz;
+    const bool tab = xn <= RS_TAB;  // yn, zn <= 1024 always
+    if (tab) {
+        const FieldView& f = P.coarse;
+        for (int t = threadIdx.x; t < xn + yn + zn; t += RS_THREADS) {
+            AxisW w;
+            int ax, e;
+            if (t < xn) {
+                ax = 0, e = t;
+                w = fine_axis(f.lox, P.fhx, f.hx, f.nx, xs + e);
+            } else if (t < xn + yn) {
+                ax = 1, e = t - xn;
+                w = fine_axis(f.loy, P.fhy, f.hy, f.ny, ys + e);
+            } else {
+                ax = 2, e = t - xn - yn;
+                w = fine_axis(f.loz, P.fhz, f.hz, f.nz, zs + e);
+            }
+            tf[ax][e] = w.f;
+            ti[ax][e] = w.i;
+        }
+        __syncthreads();
+    }
     int cnt = 0;
 #pragma unroll 2
     for (int r = 0; r < RS_PER_THREAD; ++r) {
-        int64_t c = base + r * RS_THREADS + threadIdx.x;
-        if (c >= P.n_cells) break;
-        double v = resample_at(P, c);
+        const int64_t c = base + r * RS_THREADS + threadIdx.x;
+        if (c > last) break;
+        int i, j, k;
+        cell_ijk(P, (uint32_t)c, i, j, k);
+        AxisW wx, wy, wz;
+        if (tab) {
+            wx.i = ti[0][i - xs], wx.f = tf[0][i - xs];
+            wy.i = ti[1][j - ys], wy.f = tf[1][j - ys];
+            wz.i = ti[2][k - zs], wz.f = tf[2][k - zs];
+            wx.j = P.coarse.nx > 1 ? wx.i + 1 : wx.i;
+            wy.j = P.coarse.ny > 1 ? wy.i + 1 : wy.i;
+            wz.j = P.coarse.nz > 1 ? wz.i + 1 : wz.i;
+        } else {
+            wx = fine_axis(P.coarse.lox, P.fhx, P.coarse.hx, P.coarse.nx, i);
+            wy = fine_axis(P.coarse.loy, P.fhy, P.coarse.hy, P.coarse.ny, j);
+            wz = fine_axis(P.coarse.loz, P.fhz, P.coarse.hz, P.coarse.nz, k);
+        }
+        const double v = trilinear_w(P.coarse, wx, wy, wz);
         bool m = v <= P.d;  // compared in fp64 (raysample.py:105)
         float vf = (float)v;
         if (c_fine) c_fine[c] = vf;
@@ -176,6 +228,8 @@ extern "C" int rtsdf_resample_mask(const float* coarse, int cnx, int cny, int cn
     P.fhz = fh[2];
     P.d = d;
     P.n_cells = (int64_t)fnx * fny * fnz;
+    P.div_ny = make_fastdiv((uint32_t)fny);
+    P.div_nz = make_fastdiv((uint32_t)fnz);
     int64_t nb = rtsdf_mask_blocks(P.n_cells);
     resample_mask_kernel<<<(unsigned)nb, RS_THREADS, 0, (cudaStream_t)stream>>>(
         P, c_fine, out_unmasked, mask_new, block_counts, mask_old, run_min, front, back);
