@@ -138,6 +138,42 @@ __global__ void __launch_bounds__(128) jfa_pass2_kernel(PlaneSrc src, int32_t* _
         if (a >= 1 && i_first + (a - 1) * k >= i_end) break;  // no further outputs (uniform)
         load_plane(a + 1, nxt);
         const int cx = -2 * g.wx * (i_first + a * k);
+        // Column-constant plane: every tap row holds the same seed in every lane
+        // (seeds constant along y, e.g. above a floor).  A candidate's key
+        // depends only on (seed, output), so the RY + 2 copies of a tap column
+        // are one candidate per output: 3 columns x 3 slots x RY rows instead
+        // of the 3 x 3 x 3 x RY tap/row pairs (repeats of a (key, seed) pair
+        // cannot change the running minimum, the winner or the tie flag).
+        // Only tried in the sparse early passes (k >= 64): after them, rows of
+        // different residue classes hold different provisional seeds and the
+        // test (15 compares + a vote per plane) almost never succeeds.
+        bool ycon = k >= 64;
+#pragma unroll
+        for (int bt = 1; bt < RY + 2; ++bt)
+#pragma unroll
+            for (int c = 0; c < 3; ++c) ycon = ycon && cur[bt][c] == cur[0][c];
+        if (k >= 64 && __all_sync(0xffffffffu, ycon)) {
+            const int cy = -2 * g.wy * (j_base - k);  // tap row bt = -1
+#pragma unroll
+            for (int c = -1; c <= 1; ++c) {
+                const int32_t v = cur[0][c + 1];
+                if (__all_sync(0xffffffffu, v == RTSDF_EMPTY)) continue;
+                const int sx = unpack_i(v), sy = unpack_j(v), sk = unpack_k(v);
+                const int B0 = sx * (g.wx * sx + cx) + sy * (g.wy * sy + cy) + sk * (g.wz * sk + cz);
+                const int B = v != RTSDF_EMPTY ? B0 : JFA2_EMPTY_KEY;
+                const int Gx = gxk * sx, Gy = gyk * sy;
+                const int Bs[3] = {B + Gx, B, B - Gx};
+#pragma unroll
+                for (int s = 0; s < 3; ++s) {
+                    int K = Bs[s];
+#pragma unroll
+                    for (int b = 0; b < RY; ++b) {
+                        K -= Gy;  // output row b = tap row -1 + (b + 1)
+                        jfa2_eval(K, v, Km[s][b], W[s][b]);
+                    }
+                }
+            }
+        } else
 #pragma unroll
         for (int bt = -1; bt <= RY; ++bt) {
             const int cy = -2 * g.wy * (j_base + bt * k);
