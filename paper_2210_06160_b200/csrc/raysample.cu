@@ -148,12 +148,35 @@ __global__ void __launch_bounds__(SAMPLE_THREADS) sample_update_kernel(SamplePar
 #define WF_BUDGET 4   // binary search tree: internal-node visits in pass 1
 #define WF_BUDGET4 2  // BVH4: root only (ground-plane leaves finish in pass 1)
 
+// Per-texel accumulators instead of per-ray results: the closest hit t as its
+// fp64 bit pattern (t >= 0, so unsigned integer order is fp64 order; ~0 = no
+// hit) merged with atomicMin, and the front / back votes packed in one word
+// (front | back << 16, x <= 65535) merged with atomicAdd.  min and integer sums
+// are exact and order-free, so the result does not depend on which pass or lane
+// delivers a ray -- deterministic without a per-ray buffer.
 struct WfBuffers {
-    double* t;        // [R] hit t, or -1 (miss)
-    uint8_t* facing;  // [R] 0 miss, 1 front, 2 back
-    int32_t* queue;   // [R] rays needing the full search
+    unsigned long long* tkey;  // [m_cap]
+    uint32_t* votes;           // [m_cap]
+    int32_t* queue;            // [R] rays needing the full search
     int64_t* qcount;
+    bool aligned;              // x divides 32: a warp of pass 1 holds whole texels
 };
+
+#define WF_NO_HIT 0xffffffffffffffffull
+
+__device__ __forceinline__ void wf_commit(const WfBuffers& B, uint32_t n, double t, int facing) {
+    atomicMin(&B.tkey[n], (unsigned long long)__double_as_longlong(t));
+    atomicAdd(&B.votes[n], facing == 1 ? 1u : 0x10000u);
+}
+
+__global__ void wf_init_kernel(SampleParams P, WfBuffers B) {
+    const int64_t M = min(*P.count, P.m_cap);
+    for (int64_t n = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; n < M;
+         n += (int64_t)gridDim.x * blockDim.x) {
+        B.tkey[n] = WF_NO_HIT;
+        B.votes[n] = 0;
+    }
+}
 
 __device__ __forceinline__ void wf_ray(const SampleParams& P, int64_t r, double& ox, double& oy,
                                        double& oz, double& dx, double& dy, double& dz) {
@@ -200,19 +223,65 @@ __global__ void __launch_bounds__(WF_THREADS, WF_MINB) wf_pass1_kernel(SamplePar
     for (int64_t r0 = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31); r0 < R; r0 += stride) {
         const int64_t r = r0 + lane;
         bool need = false;
+        unsigned long long key = WF_NO_HIT;
+        uint32_t inc = 0;
+        uint32_t n = 0xffffffffu;
         if (r < R) {
             double ox, oy, oz, dx, dy, dz;
             wf_ray(P, r, ox, oy, oz, dx, dy, dz);
+            n = fdiv((unsigned)r, P.div_x);
             int32_t id;
             int facing;
             bool done;
             double t = wf_trace<WIDE>(P, ox, oy, oz, dx, dy, dz, stack_mem + threadIdx.x,
                                       tstack_mem + threadIdx.x, id, facing, budget, &done);
-            if (done) {
-                B.t[r] = id >= 0 ? t : -1.0;
-                B.facing[r] = (uint8_t)(id >= 0 ? facing : 0);
+            if (done && id >= 0) {
+                key = (unsigned long long)__double_as_longlong(t);
+                inc = facing == 1 ? 1u : 0x10000u;
             }
             need = !done;
+        }
+        // merge the finished rays per texel (lanes of one texel are a contiguous
+        // run of consecutive ray ids)
+        if (P.x == 32) {
+            // one texel per warp: 64-bit min as two 32-bit warp reductions
+            const uint32_t hi = (uint32_t)(key >> 32), lo = (uint32_t)key;
+            const uint32_t hmin = __reduce_min_sync(0xffffffffu, hi);
+            const uint32_t lmin = __reduce_min_sync(0xffffffffu, hi == hmin ? lo : 0xffffffffu);
+            const uint32_t isum = __reduce_add_sync(0xffffffffu, inc);
+            if (lane == 0 && n != 0xffffffffu) {  // plain stores initialise the texel
+                B.tkey[n] = ((unsigned long long)hmin << 32) | lmin;
+                B.votes[n] = isum;
+            }
+        } else if (B.aligned) {
+            // x | 32: aligned groups of x lanes, butterfly within the group
+            for (int off = P.x >> 1; off; off >>= 1) {
+                const unsigned long long ok = __shfl_xor_sync(0xffffffffu, key, off);
+                key = ok < key ? ok : key;
+                inc += __shfl_xor_sync(0xffffffffu, inc, off);
+            }
+            if (n != 0xffffffffu && (lane & (P.x - 1)) == 0) {
+                B.tkey[n] = key;
+                B.votes[n] = inc;
+            }
+        } else {
+            // general x: shuffle-down min / sum clipped to the run leaves the
+            // run's total in its lowest lane; texels span warps -> atomics
+            const unsigned grp = __match_any_sync(0xffffffffu, n);
+            const int last = 31 - __clz(grp);
+#pragma unroll
+            for (int off = 16; off; off >>= 1) {
+                const unsigned long long ok = __shfl_down_sync(0xffffffffu, key, off);
+                const uint32_t oi = __shfl_down_sync(0xffffffffu, inc, off);
+                if (lane + off <= last) {
+                    key = ok < key ? ok : key;
+                    inc += oi;
+                }
+            }
+            if (n != 0xffffffffu && lane == __ffs(grp) - 1) {
+                if (key != WF_NO_HIT) atomicMin(&B.tkey[n], key);
+                if (inc) atomicAdd(&B.votes[n], inc);
+            }
         }
         const unsigned m = __ballot_sync(0xffffffffu, need);
         if (m) {
@@ -238,8 +307,7 @@ __global__ void __launch_bounds__(WF_THREADS, WF_MINB) wf_pass2_kernel(SamplePar
         int facing;
         double t = wf_trace<WIDE>(P, ox, oy, oz, dx, dy, dz, stack_mem + threadIdx.x,
                                   tstack_mem + threadIdx.x, id, facing, 0, nullptr);
-        B.t[r] = id >= 0 ? t : -1.0;
-        B.facing[r] = (uint8_t)(id >= 0 ? facing : 0);
+        if (id >= 0) wf_commit(B, fdiv((unsigned)r, P.div_x), t, facing);
     }
 }
 
@@ -253,7 +321,9 @@ __global__ void __launch_bounds__(WF_THREADS, WF_MINB) wf_pass2_kernel(SamplePar
 // on neighbouring texels.
 __global__ void __launch_bounds__(WF_THREADS, WF_MINB) wf_persist4_kernel(SampleParams P, WfBuffers B) {
     __shared__ int32_t stack_mem[RTSDF_FAST_STACK * WF_THREADS];
+    __shared__ __half tstack_mem[RTSDF_FAST_STACK * WF_THREADS];
     int32_t* stack = stack_mem + threadIdx.x;
+    __half* tstack = tstack_mem + threadIdx.x;
     const int lane = threadIdx.x & 31;
     const int64_t R = min(*P.count, P.m_cap) * P.x;
     int64_t r = -1;  // current ray; -1 idle, -2 drained
@@ -279,10 +349,8 @@ __global__ void __launch_bounds__(WF_THREADS, WF_MINB) wf_persist4_kernel(Sample
             }
         }
         if (__all_sync(0xffffffffu, r == -2)) break;
-        if (r >= 0 && trace4_step(P.bvh4, s, stack, WF_THREADS)) {
-            const bool hit = s.best_id >= 0;
-            B.t[r] = hit ? s.best_t : -1.0;
-            B.facing[r] = (uint8_t)(hit ? s.best_facing : 0);
+        if (r >= 0 && trace4_step(P.bvh4, s, stack, tstack, WF_THREADS)) {
+            if (s.best_id >= 0) wf_commit(B, fdiv((unsigned)r, P.div_x), s.best_t, s.best_facing);
             r = -1;
         }
     }
@@ -291,22 +359,14 @@ __global__ void __launch_bounds__(WF_THREADS, WF_MINB) wf_persist4_kernel(Sample
 // raysample.py:140-152 (per-texel min / votes, in ray order) + :229-244 (Eq. 1)
 __global__ void __launch_bounds__(WF_THREADS) wf_reduce_update_kernel(SampleParams P, WfBuffers B) {
     const int64_t M = min(*P.count, P.m_cap);
-    const int x = P.x;
     const int64_t nyz = (int64_t)P.fny * P.fnz;
     for (int64_t n = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; n < M;
          n += (int64_t)gridDim.x * blockDim.x) {
-        double best = __longlong_as_double(0x7ff0000000000000ll);
-        int fr = 0, bk = 0;
-        for (int ray = 0; ray < x; ++ray) {
-            const int64_t r = n * x + ray;
-            const int f = B.facing[r];
-            if (f) {
-                const double t = B.t[r];
-                if (t < best) best = t;
-                fr += f == 1;
-                bk += f == 2;
-            }
-        }
+        const unsigned long long key = B.tkey[n];
+        const uint32_t votes = B.votes[n];
+        const double best = key == WF_NO_HIT ? __longlong_as_double(0x7ff0000000000000ll)
+                                             : __longlong_as_double((long long)key);
+        const int fr = (int)(votes & 0xffffu), bk = (int)(votes >> 16);
         if (P.samp_min) P.samp_min[n] = best;
         if (P.samp_front) P.samp_front[n] = fr;
         if (P.samp_back) P.samp_back[n] = bk;
@@ -339,7 +399,8 @@ __global__ void __launch_bounds__(WF_THREADS) wf_reduce_update_kernel(SamplePara
 
 static size_t wf_ws_bytes(int64_t m_cap, int x) {
     const int64_t R = m_cap * (x > 0 ? x : 1);
-    return 256 + (size_t)R * (sizeof(double) + sizeof(int32_t) + 1) + 256;
+    return 256 + (size_t)m_cap * (sizeof(unsigned long long) + sizeof(uint32_t)) +
+           (size_t)R * sizeof(int32_t) + 256;
 }
 
 // ----------------------------------------------------------------------------
@@ -554,7 +615,7 @@ extern "C" int rtsdf_sample_update(const void* bvh_packed, int64_t n_nodes, int6
         if (!e) return 0;
         return e[0] == 'b' ? 2 : (e[0] == 'w' && e[1] == 'a' ? 1 : 0);
     }();
-    const bool wf_ok = x >= 1 && ws && ws_bytes >= wf_ws_bytes(m_cap, x) &&
+    const bool wf_ok = x >= 1 && x <= 65535 && ws && ws_bytes >= wf_ws_bytes(m_cap, x) &&
                        m_cap * (int64_t)x < ((int64_t)1 << 31);
     cudaStream_t st = (cudaStream_t)stream;
     if (mode == 0 && wf_ok) {
@@ -563,11 +624,12 @@ extern "C" int rtsdf_sample_update(const void* bvh_packed, int64_t n_nodes, int6
         B.qcount = (int64_t*)p;
         p += 256;
         const int64_t R = m_cap * x;
-        B.t = (double*)p;
-        p += R * sizeof(double);
+        B.tkey = (unsigned long long*)p;
+        p += m_cap * sizeof(unsigned long long);
+        B.votes = (uint32_t*)p;
+        p += m_cap * sizeof(uint32_t);
         B.queue = (int32_t*)p;
-        p += R * sizeof(int32_t);
-        B.facing = (uint8_t*)p;
+        B.aligned = 32 % x == 0;
         cudaMemsetAsync(B.qcount, 0, sizeof(int64_t), st);
         int64_t blocks = (R + WF_THREADS - 1) / WF_THREADS;
         int64_t cap = (int64_t)num_sms() * 24;
@@ -581,6 +643,11 @@ extern "C" int rtsdf_sample_update(const void* bvh_packed, int64_t n_nodes, int6
         // persistent per-lane-refill tracer: exact, but measured slower than the
         // two-pass wavefront on B200 (6.67 vs 6.32 ms at C3), so opt-in only
         static const bool persist = getenv("RTSDF_WF_PERSIST") != nullptr;
+        int launches = 3;
+        if (!B.aligned || (wide && persist)) {  // accumulators not initialised by pass 1
+            wf_init_kernel<<<(unsigned)cap, WF_THREADS, 0, st>>>(P, B);
+            ++launches;
+        }
         if (wide && persist) {
             P.bvh4 = fast_bvh4_view(bvh_packed, n_nodes, n_tris);
             wf_persist4_kernel<<<(unsigned)(num_sms() * 8), WF_THREADS, 0, st>>>(P, B);
@@ -594,7 +661,7 @@ extern "C" int rtsdf_sample_update(const void* bvh_packed, int64_t n_nodes, int6
         }
         int64_t ublocks = (m_cap + WF_THREADS - 1) / WF_THREADS;
         wf_reduce_update_kernel<<<(unsigned)(ublocks < cap ? ublocks : cap), WF_THREADS, 0, st>>>(P, B);
-        count_launch(3);
+        count_launch(launches);
         return check_launch("sample_update");
     }
     if (mode == 2 && x >= 1 && x <= BIN_RAYS) {  // direction-binned path (experimental)

@@ -321,8 +321,9 @@ __device__ __forceinline__ void trace4_init(Trace4State& s, double ox, double oy
 }
 
 // One node visit (4 slab tests) or one leaf; returns true when the ray is done.
+// Stack entries carry fp16 entry distances and are culled on pop (trace_fast4).
 __device__ __forceinline__ bool trace4_step(const FastBvh4& b, Trace4State& s, int32_t* stack,
-                                            int stride) {
+                                            __half* tstack, int stride) {
     if (s.node >= 0) {
         const FastNode4* nd = b.nodes + s.node;
         const float4 lx = __ldg((const float4*)nd->lox), ly = __ldg((const float4*)nd->loy),
@@ -345,7 +346,11 @@ __device__ __forceinline__ bool trace4_step(const FastBvh4& b, Trace4State& s, i
             }
 #pragma unroll
         for (int q = 0; q < 4; ++q)
-            if (q != nearest && t[q] != RTSDF_FINF) stack[(s.sp++) * stride] = c[q];
+            if (q != nearest && t[q] != RTSDF_FINF) {
+                stack[s.sp * stride] = c[q];
+                tstack[s.sp * stride] = __float2half_rd(t[q]);
+                ++s.sp;
+            }
         if (nearest >= 0) {
             s.node = c[nearest];
             return false;
@@ -354,9 +359,14 @@ __device__ __forceinline__ bool trace4_step(const FastBvh4& b, Trace4State& s, i
         leaf_tris(b.tris, b.exact, s.node, s.ox, s.oy, s.oz, s.dx, s.dy, s.dz, s.fdx, s.fdy, s.fdz,
                   s.best_t, s.best_id, s.best_facing, s.tb);
     }
-    if (s.sp == 0) return true;
-    s.node = stack[(--s.sp) * stride];
-    return false;
+    while (s.sp > 0) {
+        --s.sp;
+        if (__half2float(tstack[s.sp * stride]) <= s.tb) {
+            s.node = stack[s.sp * stride];
+            return false;
+        }
+    }
+    return true;
 }
 
 // Each stack entry carries its box entry distance (fp16, rounded down: a lower

@@ -265,6 +265,7 @@ def _c_setup(rt, name, dims):
 
 
 @pytest.mark.parametrize("name,dims,x", [("sphere", (64, 64, 64), 32), ("sphere", (64, 64, 64), 5),
+                                         ("sphere", (64, 64, 64), 8), ("sphere", (64, 64, 64), 64),
                                          ("sphere_plane", (400, 200, 400), 32),
                                          ("thin_plate", (96, 80, 112), 40)])
 def test_sample_hit_counts_bit_exact_host_table(rt, name, dims, x):
