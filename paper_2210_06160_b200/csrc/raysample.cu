@@ -160,6 +160,7 @@ struct WfBuffers {
     int32_t* queue;            // [R] rays needing the full search
     int64_t* qcount;
     bool aligned;              // x divides 32: a warp of pass 1 holds whole texels
+    double4* tex;              // [m_cap] per texel: origin xyz + RNG stream key (bits)
 };
 
 #define WF_NO_HIT 0xffffffffffffffffull
@@ -178,26 +179,45 @@ __global__ void wf_init_kernel(SampleParams P, WfBuffers B) {
     }
 }
 
-__device__ __forceinline__ void wf_ray(const SampleParams& P, int64_t r, double& ox, double& oy,
-                                       double& oz, double& dx, double& dy, double& dz) {
-    // 32-bit index math: rays < 2^31 (host-checked) and cells <= 1024^3
+// Per-texel ray setup, once per texel instead of once per ray: the fine-cell
+// centre (raysample.py:167-169) and the texel's SplitMix64 stream key
+// (raysample.py:170, rng.py:30-35).
+__global__ void __launch_bounds__(WF_THREADS) wf_setup_kernel(SampleParams P, WfBuffers B) {
+    const int64_t M = min(*P.count, P.m_cap);
+    for (int64_t n = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; n < M;
+         n += (int64_t)gridDim.x * blockDim.x) {
+        // 32-bit index math: cells <= 1024^3
+        const unsigned lin = (unsigned)__ldg(P.idx + n);
+        const unsigned q = fdiv(lin, P.div_nz);
+        const unsigned i = fdiv(q, P.div_ny);
+        const int k = (int)(lin - q * P.div_nz.d), j = (int)(q - i * P.div_ny.d);
+        double4 t;
+        t.x = P.coarse.lox + ((double)i + 0.5) * P.fhx;
+        t.y = P.coarse.loy + ((double)j + 0.5) * P.fhy;
+        t.z = P.coarse.loz + ((double)k + 0.5) * P.fhz;
+        t.w = __longlong_as_double((long long)stream_key(P.seed, (uint64_t)lin, (uint64_t)P.frame));
+        B.tex[n] = t;
+    }
+}
+
+__device__ __forceinline__ void wf_ray(const SampleParams& P, const WfBuffers& B, int64_t r,
+                                       double& ox, double& oy, double& oz, double& dx, double& dy,
+                                       double& dz) {
+    // rays < 2^31 (host-checked)
     const unsigned n = fdiv((unsigned)r, P.div_x);
     const int ray = (int)((unsigned)r - n * P.div_x.d);
-    const unsigned lin = (unsigned)__ldg(P.idx + n);
-    const unsigned q = fdiv(lin, P.div_nz);
-    const unsigned i = fdiv(q, P.div_ny);
-    const int k = (int)(lin - q * P.div_nz.d), j = (int)(q - i * P.div_ny.d);
-    ox = P.coarse.lox + ((double)i + 0.5) * P.fhx;  // raysample.py:167-169
-    oy = P.coarse.loy + ((double)j + 0.5) * P.fhy;
-    oz = P.coarse.loz + ((double)k + 0.5) * P.fhz;
+    const double2* tp = (const double2*)(B.tex + n);
+    const double2 a = __ldg(tp), b = __ldg(tp + 1);
+    ox = a.x;
+    oy = a.y;
+    oz = b.x;
     if (P.dirs) {
         const double* d = P.dirs + 3 * r;  // dirs[(n * x + ray) * 3 + c]
         dx = d[0];
         dy = d[1];
         dz = d[2];
     } else {
-        unit_sphere_dir(stream_key(P.seed, (uint64_t)lin, (uint64_t)P.frame), (uint64_t)ray, dx,
-                        dy, dz);
+        unit_sphere_dir((uint64_t)__double_as_longlong(b.y), (uint64_t)ray, dx, dy, dz);
     }
 }
 
@@ -228,7 +248,7 @@ __global__ void __launch_bounds__(WF_THREADS, WF_MINB) wf_pass1_kernel(SamplePar
         uint32_t n = 0xffffffffu;
         if (r < R) {
             double ox, oy, oz, dx, dy, dz;
-            wf_ray(P, r, ox, oy, oz, dx, dy, dz);
+            wf_ray(P, B, r, ox, oy, oz, dx, dy, dz);
             n = fdiv((unsigned)r, P.div_x);
             int32_t id;
             int facing;
@@ -302,7 +322,7 @@ __global__ void __launch_bounds__(WF_THREADS, WF_MINB) wf_pass2_kernel(SamplePar
          q += (int64_t)gridDim.x * blockDim.x) {
         const int64_t r = B.queue[q];
         double ox, oy, oz, dx, dy, dz;
-        wf_ray(P, r, ox, oy, oz, dx, dy, dz);
+        wf_ray(P, B, r, ox, oy, oz, dx, dy, dz);
         int32_t id;
         int facing;
         double t = wf_trace<WIDE>(P, ox, oy, oz, dx, dy, dz, stack_mem + threadIdx.x,
@@ -340,7 +360,7 @@ __global__ void __launch_bounds__(WF_THREADS, WF_MINB) wf_persist4_kernel(Sample
                 const int64_t rr = base + __popc(m & ((1u << lane) - 1));
                 if (rr < R) {
                     double ox, oy, oz, dx, dy, dz;
-                    wf_ray(P, rr, ox, oy, oz, dx, dy, dz);
+                    wf_ray(P, B, rr, ox, oy, oz, dx, dy, dz);
                     trace4_init(s, ox, oy, oz, dx, dy, dz, P.t_max);
                     r = rr;
                 } else {
@@ -399,7 +419,7 @@ __global__ void __launch_bounds__(WF_THREADS) wf_reduce_update_kernel(SamplePara
 
 static size_t wf_ws_bytes(int64_t m_cap, int x) {
     const int64_t R = m_cap * (x > 0 ? x : 1);
-    return 256 + (size_t)m_cap * (sizeof(unsigned long long) + sizeof(uint32_t)) +
+    return 256 + (size_t)m_cap * (sizeof(double4) + sizeof(unsigned long long) + sizeof(uint32_t)) +
            (size_t)R * sizeof(int32_t) + 256;
 }
 
@@ -624,6 +644,8 @@ extern "C" int rtsdf_sample_update(const void* bvh_packed, int64_t n_nodes, int6
         B.qcount = (int64_t*)p;
         p += 256;
         const int64_t R = m_cap * x;
+        B.tex = (double4*)p;
+        p += m_cap * sizeof(double4);
         B.tkey = (unsigned long long*)p;
         p += m_cap * sizeof(unsigned long long);
         B.votes = (uint32_t*)p;
@@ -643,7 +665,8 @@ extern "C" int rtsdf_sample_update(const void* bvh_packed, int64_t n_nodes, int6
         // persistent per-lane-refill tracer: exact, but measured slower than the
         // two-pass wavefront on B200 (6.67 vs 6.32 ms at C3), so opt-in only
         static const bool persist = getenv("RTSDF_WF_PERSIST") != nullptr;
-        int launches = 3;
+        int launches = 4;
+        wf_setup_kernel<<<(unsigned)cap, WF_THREADS, 0, st>>>(P, B);
         if (!B.aligned || (wide && persist)) {  // accumulators not initialised by pass 1
             wf_init_kernel<<<(unsigned)cap, WF_THREADS, 0, st>>>(P, B);
             ++launches;
@@ -691,3 +714,12 @@ extern "C" int rtsdf_sample_update(const void* bvh_packed, int64_t n_nodes, int6
     count_launch();
     return check_launch("sample_update");
 }
+
+#ifdef RTSDF_TRACE_STATS
+// experiment builds only: read and clear the traversal counters of this module
+extern "C" void rtsdf_debug_trace_stats(unsigned long long* out) {
+    cudaMemcpyFromSymbol(out, rtsdf::g_trace_stats, sizeof(unsigned long long) * 4);
+    static const unsigned long long zero[4] = {0, 0, 0, 0};
+    cudaMemcpyToSymbol(rtsdf::g_trace_stats, zero, sizeof(zero));
+}
+#endif

@@ -24,6 +24,15 @@
 
 namespace rtsdf {
 
+// Traversal counters for experiments (-DRTSDF_TRACE_STATS builds only):
+// [0] node visits, [1] leaf visits, [2] fp32 triangle pre-tests, [3] exact tests
+#ifdef RTSDF_TRACE_STATS
+static __device__ unsigned long long g_trace_stats[4];
+#define RTSDF_TSTAT(i, v) atomicAdd(&g_trace_stats[i], (unsigned long long)(v))
+#else
+#define RTSDF_TSTAT(i, v) ((void)0)
+#endif
+
 struct __align__(64) FastNode {
     float lo0[3], hi0[3];  // child 0 box (padded, outward rounded)
     float lo1[3], hi1[3];  // child 1 box
@@ -263,7 +272,9 @@ __device__ __forceinline__ bool leaf_tris(const FastTri* __restrict__ tris, cons
         const BvhTri* ex = exact + k;
         float tx = (float)(ox - __ldg(ex->a)), ty = (float)(oy - __ldg(ex->a + 1)),
               tz = (float)(oz - __ldg(ex->a + 2));
+        RTSDF_TSTAT(2, 1);
         if (!tri_maybe(tr, tx, ty, tz, fdx, fdy, fdz, tb)) continue;
+        RTSDF_TSTAT(3, 1);
         double t = ray_tri(ox, oy, oz, dx, dy, dz, ex);
         if (t >= 0.0 && t <= best_t) {
             int32_t orig = __ldg(&ex->orig);
@@ -400,6 +411,7 @@ __device__ __forceinline__ double trace_fast4(const FastBvh4& b, double ox, doub
                 break;
             }
             const FastNode4* nd = b.nodes + node;
+            RTSDF_TSTAT(0, 1);
             const float4 lx = __ldg((const float4*)nd->lox), ly = __ldg((const float4*)nd->loy),
                          lz = __ldg((const float4*)nd->loz), hx = __ldg((const float4*)nd->hix),
                          hy = __ldg((const float4*)nd->hiy), hz = __ldg((const float4*)nd->hiz);
@@ -453,6 +465,7 @@ __device__ __forceinline__ double trace_fast4(const FastBvh4& b, double ox, doub
             }
 #endif
         } else {
+            RTSDF_TSTAT(1, 1);
             leaf_tris(b.tris, b.exact, node, ox, oy, oz, dx, dy, dz, fdx, fdy, fdz, best_t,
                       best_id, best_facing, tb);
         }
