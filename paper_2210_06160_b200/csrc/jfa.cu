@@ -259,7 +259,8 @@ static void launch_pass2(PlaneSrc s, int32_t* dst, float* dst_sdf, const JfaGeom
         jfa_pass2_kernel<2, FINAL, SLAB><<<blocks, 128, 0, st>>>(s, dst, dst_sdf, g, T, beta, empty_count, fix);
     else
         jfa_pass2_kernel<1, FINAL, SLAB><<<blocks, 128, 0, st>>>(s, dst, dst_sdf, g, T, beta, empty_count, fix);
-    jfa_fixup_kernel<FINAL, SLAB><<<(unsigned)(num_sms() * 16), 128, 0, st>>>(s, dst, dst_sdf, g, beta, fix);
+    jfa_fixup_kernel<FINAL, SLAB><<<(unsigned)(num_sms() * 16), 128, 0, st>>>(
+        s, dst, dst_sdf, g, beta, fix, make_fastdiv((uint32_t)g.nz), make_fastdiv((uint32_t)g.ny));
     count_launch(2);
 }
 

@@ -267,35 +267,42 @@ __global__ void __launch_bounds__(128) jfa_pass2_kernel(PlaneSrc src, int32_t* _
 template <bool FINAL, bool SLAB>
 __global__ void __launch_bounds__(128) jfa_fixup_kernel(PlaneSrc src, int32_t* __restrict__ dst,
                                                         float* __restrict__ dst_sdf, JfaGeom g,
-                                                        double beta, JfaFixList fix) {
+                                                        double beta, JfaFixList fix, FastDiv dnz,
+                                                        FastDiv dny) {
     const int64_t n = min(*fix.count, fix.cap);
     const int64_t plane = (int64_t)g.ny * g.nz;
     const int k = g.offset;
     for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n;
          q += (int64_t)gridDim.x * blockDim.x) {
-        const int32_t cell = fix.cells[q];
-        const int il = (int)(cell / plane);
-        const int rem = (int)(cell - (int64_t)il * plane);
-        const int j = rem / g.nz, z = rem - (rem / g.nz) * g.nz;
-        const int i = g.x0 + il;
-        int32_t c[27];
+        // local linear cell -> (i, j, z); 32-bit (cells <= 1024^3)
+        const uint32_t cell = (uint32_t)fix.cells[q];
+        const uint32_t row = fdiv(cell, dnz);
+        const int z = (int)(cell - row * dnz.d);
+        const uint32_t il = fdiv(row, dny);
+        const int j = (int)(row - il * dny.d);
+        const int i = g.x0 + (int)il;
+        const int32_t* pl[3];
 #pragma unroll
         for (int di = 0; di < 3; ++di) {
             const int qi = i + (di - 1) * k;
-            const int32_t* pl = nullptr;
+            pl[di] = nullptr;
             if (qi >= 0 && qi < g.nx)
-                pl = SLAB ? plane_ptr(src, g, qi, plane) : src.local + (int64_t)qi * plane;
+                pl[di] = SLAB ? plane_ptr(src, g, qi, plane) : src.local + (int64_t)qi * plane;
+        }
+        const bool jok[3] = {j - k >= 0, true, j + k < g.ny};
+        const bool zok[3] = {z - k >= 0, true, z + k < g.nz};
+        // all 27 taps as independent loads, then the integer pre-filter
+        int32_t c[27];
 #pragma unroll
-            for (int dj = 0; dj < 3; ++dj) {
-                const int qj = j + (dj - 1) * k;
+        for (int di = 0; di < 3; ++di)
+#pragma unroll
+            for (int dj = 0; dj < 3; ++dj)
 #pragma unroll
                 for (int dk = 0; dk < 3; ++dk) {
-                    const int qk = z + (dk - 1) * k;
-                    const bool ok = pl != nullptr && qj >= 0 && qj < g.ny && qk >= 0 && qk < g.nz;
-                    c[(di * 3 + dj) * 3 + dk] = ok ? __ldg(pl + (int64_t)qj * g.nz + qk) : RTSDF_EMPTY;
+                    const bool ok = pl[di] != nullptr && jok[dj] && zok[dk];
+                    const int off = (j + (dj - 1) * k) * g.nz + z + (dk - 1) * k;
+                    c[(di * 3 + dj) * 3 + dk] = ok ? __ldg(pl[di] + off) : RTSDF_EMPTY;
                 }
-            }
-        }
         int key[27];
         int km = 0x7fffffff;
 #pragma unroll
