@@ -105,6 +105,19 @@ def peaks():
     return 6650.0, "fallback (B200_PROFILING.md)"
 
 
+def jfa_traffic():
+    """DRAM bytes (read + write) per dense JFA pass launch from the committed
+    ncu --set full capture (profiles/r1h_frame_kernels_summary.csv), or None."""
+    p = ROOT / "profiles" / "r1h_frame_kernels_summary.csv"
+    if not p.exists():
+        return None, None
+    rows = [ln.split(",") for ln in p.read_text().splitlines()[1:] if ln.startswith("jfa_pass2_kernel<4")]
+    if not rows:
+        return None, None
+    mb = [float(r[-5]) + float(r[-4]) for r in rows]  # dram_rd, dram_wr [MB] (name has commas)
+    return round(sum(mb) / len(mb) * 1e6), f"profiles/{p.name} (mean of {len(mb)} RY=4 pass launches, k = 64..1)"
+
+
 # ------------------------------------------------------------------ our arm
 def run_ours(args, rank, world, local_rank):
     import torch
@@ -238,6 +251,7 @@ def run_ours(args, rank, world, local_rank):
                "path": "pinned mesh H2D -> FramePipeline.advance(render=True) -> image + masked-count D2H"}
 
     kernels_ms = {"jfa_pass_total": jfa_ms, "sample_update": sample_ms}
+    traffic_b, traffic_src = jfa_traffic()
     dominant = "sample_update" if sample_ms > jfa_ms / len(offs) else "jfa_step"
     out = {
         "metric": METRIC, "value": round(value, 4), "unit": UNIT, "n_gpus": world,
@@ -256,7 +270,9 @@ def run_ours(args, rank, world, local_rank):
                      "achieved": round(n_cells * 8 / (float(np.mean(per_pass)) * 1e-3) / 1e9, 1),
                      "peak": hbm, "unit": "GB/s",
                      "frac": round(n_cells * 8 / (float(np.mean(per_pass)) * 1e-3) / 1e9 / hbm, 4),
-                     "traffic": None, "peak_source": hbm_src,
+                     "traffic": traffic_b, "traffic_unit": "bytes/launch (DRAM read+write, ncu)",
+                     "traffic_source": traffic_src,
+                     "algorithmic_bytes_per_launch": n_cells * 8, "peak_source": hbm_src,
                      "dominant_kernel": dominant,
                      "note": "sample_update (ray traversal) is issue/latency bound, not HBM or tensor "
                              "bound; see rays_per_s"},
