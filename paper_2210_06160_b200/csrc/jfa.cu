@@ -124,6 +124,101 @@ __global__ void __launch_bounds__(256) jfa_step_kernel(PlaneSrc src, int32_t* __
     dst[(int64_t)il * plane + (int64_t)j * g.nz + k] = b.p;
 }
 
+// ---- sparse early passes -----------------------------------------------------
+// The first passes (k >= 128 at C3) read grids that are > 99 % EMPTY (0.55 % of
+// cells hold a seed).  A byte per 32-cell z-segment records whether the
+// segment holds any seed; a warp owns one output segment, its lanes 0..26
+// test the 27 tap segments (k is a multiple of 32, so a tap segment is a whole
+// segment) and a warp whose taps are all empty writes EMPTY without loading a
+// single tap.  Other warps run the per-cell rule of jfa_step_kernel.  The
+// output bitmap for the next pass comes out of the same warp vote.
+
+__global__ void __launch_bounds__(256) jfa_seg_bitmap_kernel(const int32_t* __restrict__ src,
+                                                             uint8_t* __restrict__ bm, int ny,
+                                                             int nz, FastDiv dzb, uint32_t n_seg) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+    for (uint32_t seg = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; seg < n_seg; seg += nwarps) {
+        const uint32_t row = fdiv(seg, dzb);  // segments < 2^25
+        const int zb = (int)(seg - row * dzb.d);
+        const int z = zb * 32 + lane;
+        const bool on = z < nz && __ldg(src + (int64_t)row * nz + z) != RTSDF_EMPTY;
+        const unsigned m = __ballot_sync(0xffffffffu, on);
+        if (lane == 0) bm[seg] = m != 0;
+    }
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(256) jfa_sparse_kernel(const int32_t* __restrict__ src,
+                                                         int32_t* __restrict__ dst, JfaGeom g,
+                                                         const uint8_t* __restrict__ bm_in,
+                                                         uint8_t* __restrict__ bm_out,
+                                                         FastDiv dzb, FastDiv dny) {
+    const int nzb = (int)dzb.d;
+    const uint32_t n_seg = (uint32_t)g.nx * g.ny * nzb;
+    const int lane = threadIdx.x & 31;
+    const int off = g.offset, kz = off >> 5;
+    const int64_t plane = (int64_t)g.ny * g.nz;
+    // lane t < 27 owns tap segment t = (di, dj, dk) + 1
+    const int tdi = (lane / 9 - 1) * off, tdj = ((lane / 3) % 3 - 1) * off, tdz = (lane % 3 - 1) * kz;
+    const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+    // persistent warps: a ~1 M-segment grid of one-warp blocks is bound by
+    // block scheduling, not by the (mostly trivial) work
+    for (uint32_t seg = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; seg < n_seg; seg += nwarps) {
+        const uint32_t row = fdiv(seg, dzb);  // segments < 2^25
+        const int zb = (int)(seg - row * dzb.d);
+        const int i = (int)fdiv(row, dny), j = (int)(row - (uint32_t)i * dny.d);
+        bool tap = false;
+        if (lane < 27) {
+            const int qi = i + tdi, qj = j + tdj, qz = zb + tdz;
+            if (qi >= 0 && qi < g.nx && qj >= 0 && qj < g.ny && qz >= 0 && qz < nzb)
+                tap = __ldg(bm_in + ((int64_t)qi * g.ny + qj) * nzb + qz) != 0;
+        }
+        const int k = zb * 32 + lane;
+        const int64_t cell = (int64_t)i * plane + (int64_t)j * g.nz + k;
+        if (!__any_sync(0xffffffffu, tap)) {  // no seed can reach this segment
+            if (k < g.nz) dst[cell] = RTSDF_EMPTY;
+            if (bm_out && lane == 0) bm_out[seg] = 0;
+            continue;
+        }
+        int32_t out = RTSDF_EMPTY;
+        if (k < g.nz) {
+            Best<MODE> b;
+            b.p = __ldg(src + cell);
+            if (b.p != RTSDF_EMPTY) {
+                int dx = i - unpack_i(b.p), dy = j - unpack_j(b.p), dz = k - unpack_k(b.p);
+                if (MODE == JFA_INT) b.q = g.wx * dx * dx + g.wy * dy * dy + g.wz * dz * dz;
+                else b.d2 = center_d2(dx, dy, dz, g.hx, g.hy, g.hz);
+            } else {
+                b.q = 0x7fffffff;
+                b.d2 = 1e300;
+            }
+#pragma unroll
+            for (int di = -1; di <= 1; ++di) {
+                const int qi = i + di * off;
+                if (qi < 0 || qi >= g.nx) continue;
+#pragma unroll
+                for (int dj = -1; dj <= 1; ++dj) {
+                    const int qj = j + dj * off;
+                    if (qj < 0 || qj >= g.ny) continue;
+                    const int32_t* rw = src + (int64_t)qi * plane + (int64_t)qj * g.nz;
+#pragma unroll
+                    for (int dk = -1; dk <= 1; ++dk) {
+                        if (di == 0 && dj == 0 && dk == 0) continue;
+                        const int qk = k + dk * off;
+                        if (qk < 0 || qk >= g.nz) continue;
+                        consider<MODE>(b, __ldg(rw + qk), i, j, k, g);
+                    }
+                }
+            }
+            out = b.p;
+            dst[cell] = out;
+        }
+        const unsigned m = __ballot_sync(0xffffffffu, out != RTSDF_EMPTY);
+        if (bm_out && lane == 0) bm_out[seg] = m != 0;
+    }
+}
+
 __global__ void jfa_init_kernel(const uint8_t* __restrict__ occ, int ny, int nz, int64_t n,
                                 int32_t* __restrict__ seed, int64_t* __restrict__ count) {
     int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -310,8 +405,13 @@ static bool ws_ok(void* ws, size_t ws_bytes, int64_t n_cells) {
 
 using namespace rtsdf;
 
+// fix-up list (one int32 per cell) + two segment bitmaps for the sparse passes
+static size_t seg_bitmap_bytes(int nx, int ny, int nz) {
+    return (((size_t)nx * ny * ((nz + 31) / 32)) + 255) / 256 * 256;
+}
+
 extern "C" size_t rtsdf_jfa_ws_bytes(int nx, int ny, int nz) {
-    return 256 + (size_t)nx * ny * nz * sizeof(int32_t);
+    return 256 + (size_t)nx * ny * nz * sizeof(int32_t) + 2 * seg_bitmap_bytes(nx, ny, nz);
 }
 
 extern "C" int rtsdf_jfa_init(const uint8_t* occ, int nx, int ny, int nz, int32_t* seed,
@@ -354,28 +454,92 @@ extern "C" int rtsdf_jfa_step_slab(const int32_t* local, const int32_t* halo_lo,
     return launch_step(s, dst, g, true, ws, (cudaStream_t)stream);
 }
 
-extern "C" int rtsdf_jfa_run(int32_t* a, int32_t* b, int nx, int ny, int nz, double hx,
-                             double hy, double hz, int wx, int wy, int wz, int* which, void* ws,
-                             size_t ws_bytes, void* stream) {
-    if (!dims_ok(nx, ny, nz)) return RTSDF_ERR_DIMS;
+// The full schedule (jfa.py:140-145) on one device: sparse kernel for the
+// passes with k >= sparse_min_k (and k % 32 == 0) while the workspace has room
+// for the bitmaps, the v2 pass kernel (INT mode) or the per-cell kernel
+// otherwise; the last pass optionally writes the SDF (K3 fused, INT mode).
+static int run_schedule(int32_t* a, int32_t* b, float* sdf_out, int nx, int ny, int nz, double hx,
+                        double hy, double hz, int wx, int wy, int wz, double beta,
+                        int64_t* empty_count, int* which, void* ws, size_t ws_bytes,
+                        cudaStream_t st) {
+    const bool int_mode = wx > 0 && wy > 0 && wz > 0;
     int m = nx > ny ? nx : ny;
     if (nz > m) m = nz;
     int n = 1;
     while (n < m) n *= 2;  // jfa.py:58-68
+    static const int sparse_env = [] {
+        const char* e = getenv("RTSDF_JFA_SPARSE_K");
+        return e ? atoi(e) : -1;
+    }();
+    const int sparse_min_k = sparse_env >= 0 ? (sparse_env == 0 ? 1 << 30 : sparse_env) : 128;
+    const bool bm_room = ws_bytes >= rtsdf_jfa_ws_bytes(nx, ny, nz);
+    const int nzb = (nz + 31) / 32;
+    const int64_t n_seg = (int64_t)nx * ny * nzb;
+    uint8_t* bm[2] = {nullptr, nullptr};
+    if (bm_room) {
+        bm[0] = (uint8_t*)ws + 256 + (size_t)nx * ny * nz * sizeof(int32_t);
+        bm[1] = bm[0] + seg_bitmap_bytes(nx, ny, nz);
+    }
+    bool bm_valid = false;  // bm[0] describes src
     int32_t* src = a;
     int32_t* dst = b;
     int w = 0;
+    const int64_t seg_need = (n_seg * 32 + 255) / 256;
+    const unsigned seg_blocks = (unsigned)(seg_need < (int64_t)num_sms() * 16 ? seg_need : (int64_t)num_sms() * 16);
+    const FastDiv dzb = make_fastdiv((uint32_t)nzb), dny = make_fastdiv((uint32_t)ny);
     for (int off = n / 2; off >= 1; off /= 2) {
-        int rc = rtsdf_jfa_step(src, dst, nx, ny, nz, off, hx, hy, hz, wx, wy, wz, ws, ws_bytes,
-                                stream);
-        if (rc) return rc;
+        JfaGeom g{nx, ny, nz, 0, nx, 0, 0, 0, 0, off, hx, hy, hz, wx, wy, wz};
+        PlaneSrc s{src, nullptr, nullptr};
+        if (sdf_out && off == 1 && int_mode) {  // last pass writes the SDF directly
+            launch_pass2<true, false>(s, nullptr, sdf_out, g, beta, empty_count, ws, st);
+            return check_launch("jfa_run_sdf");
+        }
+        if (bm_room && off >= sparse_min_k && off % 32 == 0) {
+            if (!bm_valid) {
+                jfa_seg_bitmap_kernel<<<seg_blocks, 256, 0, st>>>(src, bm[0], ny, nz, dzb, (uint32_t)n_seg);
+                count_launch();
+            }
+            // the bitmap of this pass's output is only needed by a next sparse pass
+            const bool next_sparse = off / 2 >= sparse_min_k && (off / 2) % 32 == 0;
+            if (int_mode)
+                jfa_sparse_kernel<JFA_INT><<<seg_blocks, 256, 0, st>>>(
+                    src, dst, g, bm[0], next_sparse ? bm[1] : nullptr, dzb, dny);
+            else
+                jfa_sparse_kernel<JFA_FP64><<<seg_blocks, 256, 0, st>>>(
+                    src, dst, g, bm[0], next_sparse ? bm[1] : nullptr, dzb, dny);
+            count_launch();
+            uint8_t* t = bm[0];
+            bm[0] = bm[1];
+            bm[1] = t;
+            bm_valid = next_sparse;
+            int rc = check_launch("jfa_sparse");
+            if (rc) return rc;
+        } else {
+            int rc = launch_step(s, dst, g, false, ws, st);
+            if (rc) return rc;
+            bm_valid = false;
+        }
         int32_t* t = src;
         src = dst;
         dst = t;
         w ^= 1;
     }
     if (which) *which = w;
+    if (sdf_out) return rtsdf_seeds_to_sdf(src, sdf_out, nx, ny, nz, hx, hy, hz, beta, empty_count, st);
     return RTSDF_OK;
+}
+
+extern "C" int rtsdf_jfa_run(int32_t* a, int32_t* b, int nx, int ny, int nz, double hx,
+                             double hy, double hz, int wx, int wy, int wz, int* which, void* ws,
+                             size_t ws_bytes, void* stream) {
+    if (!dims_ok(nx, ny, nz)) return RTSDF_ERR_DIMS;
+    if (!weights_ok(nx, ny, nz, wx, wy, wz)) {
+        set_error("jfa_run: bad weights (%d,%d,%d)", wx, wy, wz);
+        return RTSDF_ERR_INVALID;
+    }
+    if (!ws_ok(ws, ws_bytes, (int64_t)nx * ny * nz)) return RTSDF_ERR_WORKSPACE;
+    return run_schedule(a, b, nullptr, nx, ny, nz, hx, hy, hz, wx, wy, wz, 0.0, nullptr, which, ws,
+                        ws_bytes, (cudaStream_t)stream);
 }
 
 extern "C" int rtsdf_jfa_run_sdf(int32_t* a, int32_t* b, float* out, int nx, int ny, int nz,
@@ -388,28 +552,12 @@ extern "C" int rtsdf_jfa_run_sdf(int32_t* a, int32_t* b, float* out, int nx, int
         return RTSDF_ERR_INVALID;
     }
     if (!ws_ok(ws, ws_bytes, (int64_t)nx * ny * nz)) return RTSDF_ERR_WORKSPACE;
-    const bool int_mode = wx > 0 && wy > 0 && wz > 0;
-    int m = nx > ny ? nx : ny;
-    if (nz > m) m = nz;
-    int n = 1;
-    while (n < m) n *= 2;
-    int32_t* src = a;
-    int32_t* dst = b;
-    cudaStream_t st = (cudaStream_t)stream;
-    for (int off = n / 2; off >= 1; off /= 2) {
-        JfaGeom g{nx, ny, nz, 0, nx, 0, 0, 0, 0, off, hx, hy, hz, wx, wy, wz};
-        PlaneSrc s{src, nullptr, nullptr};
-        if (off == 1 && int_mode) {  // last pass writes the SDF directly (K3 fused)
-            launch_pass2<true, false>(s, nullptr, out, g, beta, empty_count, ws, st);
-            return check_launch("jfa_run_sdf");
-        }
-        int rc = launch_step(s, dst, g, false, ws, st);
-        if (rc) return rc;
-        int32_t* t = src;
-        src = dst;
-        dst = t;
+    if (!out) {
+        set_error("jfa_run_sdf: out is null");
+        return RTSDF_ERR_INVALID;
     }
-    return rtsdf_seeds_to_sdf(src, out, nx, ny, nz, hx, hy, hz, beta, empty_count, stream);
+    return run_schedule(a, b, out, nx, ny, nz, hx, hy, hz, wx, wy, wz, beta, empty_count, nullptr,
+                        ws, ws_bytes, (cudaStream_t)stream);
 }
 
 extern "C" int rtsdf_seeds_to_sdf(const int32_t* seed, float* out, int nx, int ny, int nz,

@@ -10,6 +10,8 @@ a drop-in caller sees exactly the reference's array.
 
 from __future__ import annotations
 
+import ctypes
+
 from dataclasses import dataclass
 from fractions import Fraction
 from functools import lru_cache
@@ -173,14 +175,16 @@ def jfa_step(seeds: SeedGrid, offset: int) -> SeedGrid:
 
 
 def flood_inplace(a: torch.Tensor, b: torch.Tensor, h) -> torch.Tensor:
-    """Full schedule ping-ponging a (init seeds) <-> b; returns the result buffer."""
-    dims = tuple(int(n) for n in a.shape)
-    w = _weights(h, dims)
-    src, dst = a, b
-    for off in jfa_offsets(dims):
-        launch_step(src, dst, off, h, w)
-        src, dst = dst, src
-    return src
+    """Full schedule ping-ponging a (init seeds) <-> b (one C call: sparse early
+    passes, v2 pass kernel); returns the buffer holding the result."""
+    nx, ny, nz = (int(n) for n in a.shape)
+    w = _weights(h, (nx, ny, nz))
+    ws = workspace(nx, ny, nz)
+    which = ctypes.c_int(0)
+    _lib.check(_lib.lib().rtsdf_jfa_run(_lib.ptr(a), _lib.ptr(b), nx, ny, nz, float(h[0]),
+                                        float(h[1]), float(h[2]), *w, ctypes.byref(which),
+                                        _lib.ptr(ws), ws.numel(), _lib.stream()), "jfa_run")
+    return b if which.value else a
 
 
 def flood_to_sdf(a: torch.Tensor, b: torch.Tensor, out: torch.Tensor, h, beta=0.0,

@@ -36,3 +36,13 @@ for rep in range(3):
         for off, ms, n in rows:
             print(f"k={off:4d}  {ms:7.3f} ms  fix={n:9d} ({100.0 * n / np.prod(dims):.2f}%)")
 print("weights", w)
+ts = []
+for rep in range(5):
+    rt.voxelize_seeds(view.mesh, dims, scene.bounds, check=False, buffers=view.mesh_buffers(), out=a)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    J.flood_inplace(a, b, h)
+    e1.record()
+    torch.cuda.synchronize()
+    ts.append(e0.elapsed_time(e1))
+print("schedule (rtsdf_jfa_run) ms", [round(t, 3) for t in ts])
