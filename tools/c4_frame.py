@@ -1,0 +1,37 @@
+"""C4: 512^3 hybrid frame of the 1,310,720-triangle icosphere on
+one GPU -- host build times, per-stage frame times, masked / occupied counts."""
+import sys
+import time
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import paper_2210_06160_b200 as rt  # noqa: E402
+
+frames = int(sys.argv[1]) if len(sys.argv) > 1 else 4
+dims = (512, 512, 512)
+t0 = time.time()
+scene = rt.get_scene("big_sphere")
+print(f"scene build {time.time() - t0:.2f} s, tris {scene.instances[0].mesh.triangles.shape[0]}", flush=True)
+cfg = rt.PipelineConfig(coarse_dims=dims, fine_dims=dims, sampling=rt.SamplingParams(rays_per_frame=32))
+t0 = time.time()
+pipe = rt.FramePipeline(scene, cfg)
+view = scene.view(0)
+_ = view.bvh
+torch.cuda.synchronize()
+print(f"pipeline + BVH build {time.time() - t0:.2f} s", flush=True)
+for f in range(frames):
+    rec = pipe.advance(render=True, timing=True)
+    st = {k: round(v / 1e6, 3) for k, v in rec.durations_ns.items()}
+    print(f"frame {f}: masked {rec.masked_texels}  stages ms {st}  total {sum(st.values()):.2f}", flush=True)
+b = pipe._buffers()
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+e0.record()
+for _ in range(frames):
+    pipe.advance(render=True, timing=False)
+e1.record()
+torch.cuda.synchronize()
+print(f"C4 ms/frame {e0.elapsed_time(e1) / frames:.2f}  rays/frame {rec.masked_texels * 32}")
+print("max memory allocated GB", round(torch.cuda.max_memory_allocated() / 1e9, 2))
