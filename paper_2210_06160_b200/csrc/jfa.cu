@@ -13,6 +13,8 @@
 // relative gap is >= 1/q_max ~ 1e-7).  So the INT path orders by q and only
 // evaluates the reference's fp64 expression when q ties -- bit-exact, with
 // integer work on the common path.  (0,0,0) weights select the FP64 path.
+#include <cmath>
+
 #include "common.cuh"
 
 namespace rtsdf {
@@ -27,7 +29,48 @@ struct JfaGeom {
     int offset;
     double hx, hy, hz;
     int wx, wy, wz;
+    bool exact;  // fp64 d2 exact for these spacings (fp64_exact): ties resolve in the pass
 };
+
+// True when every fp64 operation of center_d2 (jfa.py:72-76) is exact for all
+// offsets |d| < n on each axis: h = m 2^e (m odd) with d*h and (d*h)^2
+// representable, and every partial sum of the three terms a multiple of the
+// smallest term granularity below 2^53.  Dyadic spacings such as 4/512 or
+// 2/1024 qualify (C1, C2, C4, C5); 3.2/400 (C3) does not.
+static bool fp64_exact(double hx, double hy, double hz, int nx, int ny, int nz) {
+    const double hs[3] = {hx, hy, hz};
+    const int ns[3] = {nx, ny, nz};
+    int64_t mant[3];
+    int ex[3], mb[3];
+    int gmin = 1 << 30;
+    for (int a = 0; a < 3; ++a) {
+        if (!(hs[a] > 0.0) || !std::isfinite(hs[a])) return false;
+        int e2;
+        const double f = std::frexp(hs[a], &e2);  // h = f 2^e2, f in [0.5, 1)
+        int64_t m = (int64_t)std::ldexp(f, 53);
+        int e = e2 - 53;
+        while ((m & 1) == 0) {
+            m >>= 1;
+            ++e;
+        }
+        mant[a] = m;
+        ex[a] = e;
+        mb[a] = 64 - __builtin_clzll((unsigned long long)m);
+        const int db = ns[a] > 1 ? 64 - __builtin_clzll((unsigned long long)(ns[a] - 1)) : 0;
+        if (2 * (mb[a] + db) > 53) return false;  // d h and (d h)^2 exact
+        if (ns[a] > 1 && 2 * e < gmin) gmin = 2 * e;
+    }
+    if (gmin == 1 << 30) return true;  // a single cell
+    unsigned __int128 sum = 0;
+    for (int a = 0; a < 3; ++a) {
+        if (ns[a] <= 1) continue;
+        const int sh = 2 * ex[a] - gmin;
+        if (sh > 60) return false;
+        const unsigned __int128 d = (unsigned __int128)(ns[a] - 1);
+        sum += d * d * (unsigned __int128)mant[a] * (unsigned __int128)mant[a] << sh;
+    }
+    return sum < ((unsigned __int128)1 << 53);
+}
 
 struct PlaneSrc {
     const int32_t* local;
@@ -341,6 +384,16 @@ static void launch_pass2(PlaneSrc s, int32_t* dst, float* dst_sdf, const JfaGeom
     // v3 (select-free 5-key pass, jfa3.cuh) is exact but measured slower than
     // v2 on B200 (more instructions, 159 registers): opt-in only
     static const bool v3_on = getenv("RTSDF_JFA_V3") != nullptr;
+    if (g.exact) {  // ties resolve inside the pass: no flags, no fix-up
+        if (ry == 4)
+            jfa_pass2_kernel<4, FINAL, SLAB, true><<<blocks, 128, 0, st>>>(s, dst, dst_sdf, g, T, beta, empty_count, fix);
+        else if (ry == 2)
+            jfa_pass2_kernel<2, FINAL, SLAB, true><<<blocks, 128, 0, st>>>(s, dst, dst_sdf, g, T, beta, empty_count, fix);
+        else
+            jfa_pass2_kernel<1, FINAL, SLAB, true><<<blocks, 128, 0, st>>>(s, dst, dst_sdf, g, T, beta, empty_count, fix);
+        count_launch(1);
+        return;
+    }
     if (v3_on && jfa3_ok(g)) {
         if (ry == 4)
             jfa_pass3_kernel<4, FINAL, SLAB><<<blocks, 128, 0, st>>>(s, dst, dst_sdf, g, T, beta, empty_count, fix);
@@ -349,11 +402,11 @@ static void launch_pass2(PlaneSrc s, int32_t* dst, float* dst_sdf, const JfaGeom
         else
             jfa_pass3_kernel<1, FINAL, SLAB><<<blocks, 128, 0, st>>>(s, dst, dst_sdf, g, T, beta, empty_count, fix);
     } else if (ry == 4)
-        jfa_pass2_kernel<4, FINAL, SLAB><<<blocks, 128, 0, st>>>(s, dst, dst_sdf, g, T, beta, empty_count, fix);
+        jfa_pass2_kernel<4, FINAL, SLAB, false><<<blocks, 128, 0, st>>>(s, dst, dst_sdf, g, T, beta, empty_count, fix);
     else if (ry == 2)
-        jfa_pass2_kernel<2, FINAL, SLAB><<<blocks, 128, 0, st>>>(s, dst, dst_sdf, g, T, beta, empty_count, fix);
+        jfa_pass2_kernel<2, FINAL, SLAB, false><<<blocks, 128, 0, st>>>(s, dst, dst_sdf, g, T, beta, empty_count, fix);
     else
-        jfa_pass2_kernel<1, FINAL, SLAB><<<blocks, 128, 0, st>>>(s, dst, dst_sdf, g, T, beta, empty_count, fix);
+        jfa_pass2_kernel<1, FINAL, SLAB, false><<<blocks, 128, 0, st>>>(s, dst, dst_sdf, g, T, beta, empty_count, fix);
     jfa_fixup_kernel<FINAL, SLAB><<<(unsigned)(num_sms() * 16), 128, 0, st>>>(
         s, dst, dst_sdf, g, beta, fix, make_fastdiv((uint32_t)g.nz), make_fastdiv((uint32_t)g.ny));
     count_launch(2);
@@ -433,7 +486,8 @@ extern "C" int rtsdf_jfa_step(const int32_t* src, int32_t* dst, int nx, int ny, 
         return RTSDF_ERR_INVALID;
     }
     if (!ws_ok(ws, ws_bytes, (int64_t)nx * ny * nz)) return RTSDF_ERR_WORKSPACE;
-    JfaGeom g{nx, ny, nz, 0, nx, 0, 0, 0, 0, offset, hx, hy, hz, wx, wy, wz};
+    JfaGeom g{nx, ny, nz, 0, nx, 0, 0, 0, 0, offset, hx, hy, hz, wx, wy, wz,
+              wx > 0 && fp64_exact(hx, hy, hz, nx, ny, nz)};
     PlaneSrc s{src, nullptr, nullptr};
     return launch_step(s, dst, g, false, ws, (cudaStream_t)stream);
 }
@@ -449,7 +503,8 @@ extern "C" int rtsdf_jfa_step_slab(const int32_t* local, const int32_t* halo_lo,
         return RTSDF_ERR_INVALID;
     }
     if (!ws_ok(ws, ws_bytes, (int64_t)nxl * ny * nz)) return RTSDF_ERR_WORKSPACE;
-    JfaGeom g{nx, ny, nz, x0, nxl, lo_first, n_lo, hi_first, n_hi, offset, hx, hy, hz, wx, wy, wz};
+    JfaGeom g{nx,     ny,    nz, x0, nxl, lo_first, n_lo, hi_first, n_hi, offset, hx, hy, hz,
+              wx,     wy,    wz, wx > 0 && fp64_exact(hx, hy, hz, nx, ny, nz)};
     PlaneSrc s{local, halo_lo, halo_hi};
     return launch_step(s, dst, g, true, ws, (cudaStream_t)stream);
 }
@@ -463,6 +518,7 @@ static int run_schedule(int32_t* a, int32_t* b, float* sdf_out, int nx, int ny, 
                         int64_t* empty_count, int* which, void* ws, size_t ws_bytes,
                         cudaStream_t st) {
     const bool int_mode = wx > 0 && wy > 0 && wz > 0;
+    const bool exact = int_mode && fp64_exact(hx, hy, hz, nx, ny, nz);
     int m = nx > ny ? nx : ny;
     if (nz > m) m = nz;
     int n = 1;
@@ -488,7 +544,7 @@ static int run_schedule(int32_t* a, int32_t* b, float* sdf_out, int nx, int ny, 
     const unsigned seg_blocks = (unsigned)(seg_need < (int64_t)num_sms() * 16 ? seg_need : (int64_t)num_sms() * 16);
     const FastDiv dzb = make_fastdiv((uint32_t)nzb), dny = make_fastdiv((uint32_t)ny);
     for (int off = n / 2; off >= 1; off /= 2) {
-        JfaGeom g{nx, ny, nz, 0, nx, 0, 0, 0, 0, off, hx, hy, hz, wx, wy, wz};
+        JfaGeom g{nx, ny, nz, 0, nx, 0, 0, 0, 0, off, hx, hy, hz, wx, wy, wz, exact};
         PlaneSrc s{src, nullptr, nullptr};
         if (sdf_out && off == 1 && int_mode) {  // last pass writes the SDF directly
             launch_pass2<true, false>(s, nullptr, sdf_out, g, beta, empty_count, ws, st);

@@ -51,13 +51,32 @@ __device__ __forceinline__ void jfa2_eval(int K, int32_t v, int& Km, int32_t& W)
         : "r"(K), "r"(v));
 }
 
+// EXACT mode (host-proven: every fp64 operation of center_d2 is exact for the
+// grid's spacings and extents, e.g. dyadic spacings such as 4/512): fp64 d2 is
+// then exactly proportional to the integer key, so the reference's rule
+// (fp64 d2, then lexicographic) IS the lexicographic order of (key, packed
+// seed) -- ties resolve in the hot loop, no flags, no fix-up.  (K, v) < (Km, W)
+// with the seed compared unsigned (EMPTY = 0xffffffff is the largest):
+// 3 predicate compares, a min and a select.
+__device__ __forceinline__ void jfa2_eval_exact(int K, int32_t v, int& Km, int32_t& W) {
+    asm volatile(
+        "{\n\t.reg .pred peq, pe, p;\n\t"
+        "setp.eq.s32 peq, %2, %0;\n\t"
+        "setp.lt.and.u32 pe, %3, %1, peq;\n\t"
+        "setp.lt.or.s32 p, %2, %0, pe;\n\t"
+        "min.s32 %0, %0, %2;\n\t"
+        "selp.b32 %1, %3, %1, p;\n\t}"
+        : "+r"(Km), "+r"(W)
+        : "r"(K), "r"(v));
+}
+
 struct JfaFixList {
     int32_t* cells;  // local linear cell indices needing the exact rule
     int64_t* count;  // device counter
     int64_t cap;
 };
 
-template <int RY, bool FINAL, bool SLAB>
+template <int RY, bool FINAL, bool SLAB, bool EXACT>
 __global__ void __launch_bounds__(128) jfa_pass2_kernel(PlaneSrc src, int32_t* __restrict__ dst,
                                                         float* __restrict__ dst_sdf, JfaGeom g,
                                                         Jfa2Task T, double beta,
@@ -169,7 +188,10 @@ __global__ void __launch_bounds__(128) jfa_pass2_kernel(PlaneSrc src, int32_t* _
 #pragma unroll
                     for (int b = 0; b < RY; ++b) {
                         K -= Gy;  // output row b = tap row -1 + (b + 1)
-                        jfa2_eval(K, v, Km[s][b], W[s][b]);
+                        if (EXACT)
+                            jfa2_eval_exact(K, v, Km[s][b], W[s][b]);
+                        else
+                            jfa2_eval(K, v, Km[s][b], W[s][b]);
                     }
                 }
             }
@@ -197,7 +219,10 @@ __global__ void __launch_bounds__(128) jfa_pass2_kernel(PlaneSrc src, int32_t* _
                         const int b = bt + db;
                         if (b < 0 || b >= RY) continue;  // compile-time
                         const int K = db == 0 ? Bs[s] : (db < 0 ? Bs[s] + Gy : Bs[s] - Gy);
-                        jfa2_eval(K, v, Km[s][b], W[s][b]);
+                        if (EXACT)
+                            jfa2_eval_exact(K, v, Km[s][b], W[s][b]);
+                        else
+                            jfa2_eval(K, v, Km[s][b], W[s][b]);
                     }
                 }
             }
@@ -212,8 +237,8 @@ __global__ void __launch_bounds__(128) jfa_pass2_kernel(PlaneSrc src, int32_t* _
                 const bool live = zok && oj < g.ny;
                 const int64_t cell = (int64_t)(oi - g.x0) * plane + (int64_t)oj * g.nz + z;
                 const int32_t wt = W[0][b];
-                const bool tie = wt != RTSDF_EMPTY && (wt & JFA2_TIEBIT);
-                const int32_t w = wt == RTSDF_EMPTY ? wt : (wt & ~JFA2_TIEBIT);
+                const bool tie = !EXACT && wt != RTSDF_EMPTY && (wt & JFA2_TIEBIT);
+                const int32_t w = EXACT || wt == RTSDF_EMPTY ? wt : (wt & ~JFA2_TIEBIT);
                 if (live) {
                     if (FINAL) {
                         empties += w == RTSDF_EMPTY;

@@ -13,8 +13,9 @@ import paper_2210_06160_b200 as rt  # noqa: E402
 from paper_2210_06160_b200 import _lib  # noqa: E402
 from paper_2210_06160_b200 import raysample as RS  # noqa: E402
 
-dims = (400, 200, 400)
-scene = rt.get_scene("sphere_plane")
+name = sys.argv[1] if len(sys.argv) > 1 else "sphere_plane"
+dims = tuple(int(v) for v in (sys.argv[2] if len(sys.argv) > 2 else "400,200,400").split(","))
+scene = rt.get_scene(name)
 cfg = rt.PipelineConfig(coarse_dims=dims, fine_dims=dims, sampling=rt.SamplingParams(rays_per_frame=32))
 pipe = rt.FramePipeline(scene, cfg)
 pipe.advance(render=False, timing=False)
