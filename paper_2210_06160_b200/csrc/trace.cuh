@@ -27,7 +27,9 @@ namespace rtsdf {
 // Traversal counters for experiments (-DRTSDF_TRACE_STATS builds only):
 // [0] node visits, [1] leaf visits, [2] fp32 triangle pre-tests, [3] exact tests
 #ifdef RTSDF_TRACE_STATS
-static __device__ unsigned long long g_trace_stats[4];
+// [4..11]: per-ray node-visit histogram of the long-ray traversal (bins 0-1,
+// 2-3, 4-7, 8-15, 16-31, 32-63, 64-127, 128+)
+static __device__ unsigned long long g_trace_stats[12];
 #define RTSDF_TSTAT(i, v) atomicAdd(&g_trace_stats[i], (unsigned long long)(v))
 #else
 #define RTSDF_TSTAT(i, v) ((void)0)
@@ -519,9 +521,15 @@ __device__ __forceinline__ double trace_fast4_ww(const FastBvh4& b, double ox, d
     };
     int32_t node = 0;  // >= 0 inner, < 0 leaf, T4_DONE finished
     int32_t leaf = 0;  // parked leaf (< 0) or 0
+#ifdef RTSDF_TRACE_STATS
+    int visits = 0;
+#endif
     while (true) {
         while (node >= 0) {
             RTSDF_TSTAT(0, 1);
+#ifdef RTSDF_TRACE_STATS
+            ++visits;
+#endif
             const FastNode4* nd = b.nodes + node;
             const float4 lx = __ldg((const float4*)nd->lox), ly = __ldg((const float4*)nd->loy),
                          lz = __ldg((const float4*)nd->loz), hx = __ldg((const float4*)nd->hix),
@@ -571,6 +579,9 @@ __device__ __forceinline__ double trace_fast4_ww(const FastBvh4& b, double ox, d
         }
         if (node == T4_DONE) break;
     }
+#ifdef RTSDF_TRACE_STATS
+    RTSDF_TSTAT(4 + min(7, 31 - __clz(visits | 1)), 1);
+#endif
     out_id = best_id;
     out_facing = best_facing;
     return best_id < 0 ? -1.0 : best_t;

@@ -30,12 +30,17 @@ sf = torch.empty(m, dtype=torch.int32, device="cuda")
 sb = torch.empty(m, dtype=torch.int32, device="cuda")
 fn = _lib.lib().rtsdf_debug_trace_stats
 fn.argtypes = [ctypes.POINTER(ctypes.c_ulonglong)]
-out = (ctypes.c_ulonglong * 4)()
+out = (ctypes.c_ulonglong * 12)()
 fn(out)
 RS.launch_sample_update(view.bvh, g, cb, cfg.sampling, 1, t_max, samp=(smin, sf, sb), m_cap=m)
 torch.cuda.synchronize()
 fn(out)
 rays = m * 32
 names = ["node visits", "leaf visits", "tri pre-tests", "exact tests"]
-for n, v in zip(names, out):
+for n, v in zip(names, out[:4]):
     print(f"{n:14s} {v:14d}  {v / rays:8.3f} per ray")
+hist = list(out[4:])
+if sum(hist):
+    labels = ["0-1", "2-3", "4-7", "8-15", "16-31", "32-63", "64-127", "128+"]
+    tot = sum(hist)
+    print("long-ray node visits:", ", ".join(f"{l}: {100.0 * h / tot:.1f}%" for l, h in zip(labels, hist)))
