@@ -721,8 +721,8 @@ extern "C" int rtsdf_sample_update(const void* bvh_packed, int64_t n_nodes, int6
 #ifdef RTSDF_TRACE_STATS
 // experiment builds only: read and clear the traversal counters of this module
 extern "C" void rtsdf_debug_trace_stats(unsigned long long* out) {
-    cudaMemcpyFromSymbol(out, rtsdf::g_trace_stats, sizeof(unsigned long long) * 4);
-    static const unsigned long long zero[4] = {0, 0, 0, 0};
+    cudaMemcpyFromSymbol(out, rtsdf::g_trace_stats, sizeof(unsigned long long) * 12);
+    static const unsigned long long zero[12] = {};
     cudaMemcpyToSymbol(rtsdf::g_trace_stats, zero, sizeof(zero));
 }
 #endif
