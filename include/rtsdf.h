@@ -107,10 +107,21 @@ int rtsdf_jfa_run_sdf(int32_t* buf_a, int32_t* buf_b, float* out, int nx, int ny
 
 /* Replaces jfa.py:224 (_seed_distance_kernel): out = f32(sqrt(d2_fp64) - beta).
  * empty_count (device int64, nullable) += EMPTY cells (NoSeedsError check,
- * jfa.py:176-177).  x0/nx_global: slab offset (0 / nx for a whole grid).    */
+ * jfa.py:176-177).                                                          */
 int rtsdf_seeds_to_sdf(const int32_t* seed_packed, float* out, int nx, int ny, int nz,
                        double hx, double hy, double hz, double beta, int64_t* empty_count,
                        void* stream);
+
+/* ------------------------------------------------- slab (range) forms
+ * For the z-slab sharded frame (paper_2210_06160_b200/shard.py).
+ * These calls address every buffer by GLOBAL cell index: pass a base pointer
+ * p such that p + c is the storage of global cell c for each cell the call
+ * touches (slab-local storage that starts at global cell c0 -> storage - c0).
+ * Only the range's cells are read or written -- plus, for the trilinear
+ * resample, coarse planes x0 - 1 .. x0 + nxl (a one-plane halo).           */
+int rtsdf_seeds_to_sdf_range(const int32_t* seed_packed, float* out, int nx, int ny, int nz,
+                             int x0, int nxl, double hx, double hy, double hz, double beta,
+                             int64_t* empty_count, void* stream);
 int rtsdf_seeds_packed_to_linear(const int32_t* packed, int32_t* linear, int nx, int ny, int nz,
                                  void* stream);
 int rtsdf_seeds_linear_to_packed(const int32_t* linear, int32_t* packed, int nx, int ny, int nz,
@@ -139,6 +150,18 @@ int rtsdf_resample_mask(const float* coarse, int cnx, int cny, int cnz,
 size_t rtsdf_compact_ws_bytes(int64_t n_cells);
 int rtsdf_compact_mask(const uint8_t* mask, int64_t n_cells, int32_t* block_counts,
                        int64_t* idx, int64_t* count, void* ws, size_t ws_bytes, void* stream);
+/* Range forms (global cell addressing, see the slab section above): cells
+ * [c0, c0 + n_range) of the fine grid; block_counts / the compaction
+ * workspace are sized for n_range; idx holds global indices.               */
+int rtsdf_resample_mask_range(const float* coarse, int cnx, int cny, int cnz,
+                              const double* clo /*host[3]*/, const double* ch /*host[3]*/,
+                              int fnx, int fny, int fnz, const double* fh /*host[3]*/, double d,
+                              int64_t c0, int64_t n_range, float* c_fine, float* out_unmasked,
+                              uint8_t* mask_new, int32_t* block_counts, const uint8_t* mask_old,
+                              float* run_min, int32_t* front, int32_t* back, void* stream);
+int rtsdf_compact_mask_range(const uint8_t* mask, int64_t c0, int64_t n_range,
+                             int32_t* block_counts, int64_t* idx, int64_t* count, void* ws,
+                             size_t ws_bytes, void* stream);
 
 /* --------------------------------------------------------------------- BVH */
 /* Replaces geometry.py:202-267 (build_bvh), on the host (plain C++, same
@@ -183,12 +206,16 @@ int rtsdf_ray_query(const void* bvh_packed, int64_t n_nodes, int64_t n_tris, int
 /* ---------------------------------------------- ray-sampled refine + Eq. 1 */
 /* Replaces raysample.py:277-299 (_sample_masked_kernel + band reset +
  * _update_masked_kernel).  Default (workspace given): wavefront -- every ray
- * traced with a small node budget, budget-exhausted rays re-traced from a
- * compacted queue, then one thread per texel reduces its rays in ray order
- * and applies Eq. 1 (results independent of the queue order).  Without a
- * workspace: one warp per texel, one lane per ray, warp-reduced.  Closest
- * hits are the brute-force ones the reference's BVH contract names
- * (geometry.py:3-6; trace.cuh).  No atomics touch results.  M is read from
+ * traced with a small node budget (its texel's finished rays merged by a warp
+ * reduction), budget-exhausted rays re-traced from a compacted queue and
+ * merged into per-texel accumulators (atomicMin on the fp64 bits of t, t >= 0;
+ * atomicAdd of packed front/back votes) -- min and integer sums are exact and
+ * order-free, so results are deterministic and independent of the queue
+ * order; then one thread per texel applies Eq. 1.  Without a workspace: one
+ * warp per texel, one lane per ray, warp-reduced.  Closest hits are the
+ * brute-force ones the reference's BVH contract names (geometry.py:3-6;
+ * trace.cuh).  Buffers indexed by texel (prev, out, mask_old, run_min,
+ * front, back) use the global fine cell index idx[n].  M is read from
  * device memory (*count from rtsdf_compact_mask) so no host sync is needed;
  * m_cap bounds the grid.
  *   dirs (nullable): host-supplied table dirs[(n*x + r)*3 + c] (parity mode);
@@ -205,9 +232,10 @@ typedef struct {
     double fh[3];
 } rtsdf_resample_desc;
 
-/* Workspace of the wavefront sampler for m_cap texels x rays: per-ray results
- * (t fp64, facing u8) and the long-ray queue.  With ws == NULL the sampler
- * falls back to the warp-per-texel kernel (same results).                   */
+/* Workspace of the wavefront sampler for m_cap texels x rays: per-texel ray
+ * setup (origin + stream key) and closest-hit / vote accumulators, and the
+ * long-ray queue.  With ws == NULL the sampler falls back to the
+ * warp-per-texel kernel (same results).                                     */
 size_t rtsdf_sample_ws_bytes(int64_t m_cap, int x);
 /* n_nodes4 > 0: the BVH4 collapse of the search tree (rtsdf_bvh4_collapse_host)
  * is appended to bvh_packed at offset rtsdf_bvh_packed_bytes(n_nodes, n_tris). */

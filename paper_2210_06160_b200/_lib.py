@@ -48,12 +48,16 @@ SIGNATURES = {
     "rtsdf_jfa_run": (I, [P, P, I, I, I, D, D, D, I, I, I, C.POINTER(I), P, SZ, P]),
     "rtsdf_jfa_run_sdf": (I, [P, P, P, I, I, I, D, D, D, I, I, I, D, P, P, SZ, P]),
     "rtsdf_seeds_to_sdf": (I, [P, P, I, I, I, D, D, D, D, P, P]),
+    "rtsdf_seeds_to_sdf_range": (I, [P, P, I, I, I, I, I, D, D, D, D, P, P]),
     "rtsdf_seeds_packed_to_linear": (I, [P, P, I, I, I, P]),
     "rtsdf_seeds_linear_to_packed": (I, [P, P, I, I, I, P]),
     "rtsdf_mask_blocks": (I64, [I64]),
     "rtsdf_resample_mask": (I, [P, I, I, I, DP, DP, I, I, I, DP, D, P, P, P, P, P, P, P, P, P]),
     "rtsdf_compact_ws_bytes": (SZ, [I64]),
     "rtsdf_compact_mask": (I, [P, I64, P, P, P, P, SZ, P]),
+    "rtsdf_resample_mask_range": (I, [P, I, I, I, DP, DP, I, I, I, DP, D, I64, I64, P, P, P, P, P,
+                                      P, P, P, P]),
+    "rtsdf_compact_mask_range": (I, [P, I64, I64, P, P, P, P, SZ, P]),
     "rtsdf_bvh_build_host": (I64, [P, P, I64, P, P, P, P, P]),
     "rtsdf_bvh_build_sah_host": (I64, [P, P, I64, I, P, P, P, P, P]),
     "rtsdf_bvh_packed_bytes": (SZ, [I64, I64]),

@@ -280,11 +280,11 @@ __global__ void jfa_init_kernel(const uint8_t* __restrict__ occ, int ny, int nz,
 
 // jfa.py:148-160: f32(sqrt(d2_fp64) - beta)
 __global__ void seeds_to_sdf_kernel(const int32_t* __restrict__ seed, float* __restrict__ out,
-                                    int nx, int ny, int nz, double hx, double hy, double hz,
+                                    int x0, int ny, int nz, double hx, double hy, double hz,
                                     double beta, int64_t* __restrict__ empty_count) {
     const int k = blockIdx.x * 32 + threadIdx.x;
     const int j = blockIdx.y * 8 + threadIdx.y;
-    const int i = blockIdx.z;
+    const int i = x0 + blockIdx.z;  // global plane (buffers are global-indexed)
     bool empty = false;
     if (k < nz && j < ny) {
         int64_t c = ((int64_t)i * ny + j) * nz + k;
@@ -616,16 +616,28 @@ extern "C" int rtsdf_jfa_run_sdf(int32_t* a, int32_t* b, float* out, int nx, int
                         ws, ws_bytes, (cudaStream_t)stream);
 }
 
-extern "C" int rtsdf_seeds_to_sdf(const int32_t* seed, float* out, int nx, int ny, int nz,
-                                  double hx, double hy, double hz, double beta,
-                                  int64_t* empty_count, void* stream) {
+extern "C" int rtsdf_seeds_to_sdf_range(const int32_t* seed, float* out, int nx, int ny, int nz,
+                                        int x0, int nxl, double hx, double hy, double hz,
+                                        double beta, int64_t* empty_count, void* stream) {
     if (!dims_ok(nx, ny, nz)) return RTSDF_ERR_DIMS;
+    if (x0 < 0 || nxl < 0 || x0 + nxl > nx) {
+        set_error("seeds_to_sdf_range: planes [%d, %d) outside 0..%d", x0, x0 + nxl, nx);
+        return RTSDF_ERR_INVALID;
+    }
+    if (nxl == 0) return RTSDF_OK;
     dim3 block(32, 8, 1);
-    dim3 grid((nz + 31) / 32, (ny + 7) / 8, nx);
-    seeds_to_sdf_kernel<<<grid, block, 0, (cudaStream_t)stream>>>(seed, out, nx, ny, nz, hx, hy,
+    dim3 grid((nz + 31) / 32, (ny + 7) / 8, nxl);
+    seeds_to_sdf_kernel<<<grid, block, 0, (cudaStream_t)stream>>>(seed, out, x0, ny, nz, hx, hy,
                                                                   hz, beta, empty_count);
     count_launch();
     return check_launch("seeds_to_sdf");
+}
+
+extern "C" int rtsdf_seeds_to_sdf(const int32_t* seed, float* out, int nx, int ny, int nz,
+                                  double hx, double hy, double hz, double beta,
+                                  int64_t* empty_count, void* stream) {
+    return rtsdf_seeds_to_sdf_range(seed, out, nx, ny, nz, 0, nx, hx, hy, hz, beta, empty_count,
+                                    stream);
 }
 
 extern "C" int rtsdf_seeds_packed_to_linear(const int32_t* p, int32_t* l, int nx, int ny, int nz,

@@ -22,7 +22,7 @@ struct RsParams {
     int fnx, fny, fnz;
     double fhx, fhy, fhz;
     double d;
-    int64_t n_cells;
+    int64_t c0, n_cells;  // global cells [c0, c0 + n_cells); buffers global-indexed
     FastDiv div_ny, div_nz;
 };
 
@@ -51,8 +51,8 @@ __global__ void __launch_bounds__(RS_THREADS) resample_mask_kernel(
     __shared__ int warp_sum[RS_THREADS / 32];
     __shared__ double tf[3][RS_TAB];
     __shared__ int ti[3][RS_TAB];
-    const int64_t base = (int64_t)blockIdx.x * RS_CELLS_PER_BLOCK;
-    const int64_t last = min(base + RS_CELLS_PER_BLOCK, P.n_cells) - 1;
+    const int64_t base = P.c0 + (int64_t)blockIdx.x * RS_CELLS_PER_BLOCK;
+    const int64_t last = min(base + RS_CELLS_PER_BLOCK, P.c0 + P.n_cells) - 1;
     int i0, j0, k0, i1, j1, k1;
     cell_ijk(P, (uint32_t)base, i0, j0, k0);
     cell_ijk(P, (uint32_t)last, i1, j1, k1);
@@ -127,13 +127,14 @@ __global__ void __launch_bounds__(RS_THREADS) resample_mask_kernel(
 }
 
 __global__ void __launch_bounds__(RS_THREADS) count_mask_kernel(const uint8_t* __restrict__ mask,
-                                                               int64_t n, int32_t* __restrict__ block_counts) {
+                                                               int64_t c0, int64_t n,
+                                                               int32_t* __restrict__ block_counts) {
     __shared__ int warp_sum[RS_THREADS / 32];
     const int64_t base = (int64_t)blockIdx.x * RS_CELLS_PER_BLOCK;
     int cnt = 0;
     for (int r = 0; r < RS_PER_THREAD; ++r) {
         int64_t c = base + r * RS_THREADS + threadIdx.x;
-        if (c < n) cnt += mask[c] != 0;
+        if (c < n) cnt += mask[c0 + c] != 0;
     }
     for (int o = 16; o; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
     if ((threadIdx.x & 31) == 0) warp_sum[threadIdx.x >> 5] = cnt;
@@ -171,7 +172,7 @@ __global__ void __launch_bounds__(1024) scan_blocks_kernel(const int32_t* __rest
 }
 
 __global__ void __launch_bounds__(RS_THREADS) compact_kernel(const uint8_t* __restrict__ mask,
-                                                            int64_t n,
+                                                            int64_t c0, int64_t n,
                                                             const int64_t* __restrict__ offsets,
                                                             int64_t* __restrict__ idx) {
     __shared__ int warp_cnt[RS_THREADS / 32];
@@ -180,7 +181,7 @@ __global__ void __launch_bounds__(RS_THREADS) compact_kernel(const uint8_t* __re
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     for (int r = 0; r < RS_PER_THREAD; ++r) {
         int64_t c = base + r * RS_THREADS + threadIdx.x;
-        bool m = c < n && mask[c] != 0;
+        bool m = c < n && mask[c0 + c] != 0;
         unsigned bal = __ballot_sync(0xffffffffu, m);
         if (lane == 0) warp_cnt[wid] = __popc(bal);
         __syncthreads();
@@ -190,7 +191,7 @@ __global__ void __launch_bounds__(RS_THREADS) compact_kernel(const uint8_t* __re
             before += w < wid ? v : 0;
             all += v;
         }
-        if (m) idx[run + before + __popc(bal & ((1u << lane) - 1))] = c;
+        if (m) idx[run + before + __popc(bal & ((1u << lane) - 1))] = c0 + c;
         run += all;
         __syncthreads();
     }
@@ -204,20 +205,28 @@ extern "C" int64_t rtsdf_mask_blocks(int64_t n_cells) {
     return (n_cells + RS_CELLS_PER_BLOCK - 1) / RS_CELLS_PER_BLOCK;
 }
 
-extern "C" int rtsdf_resample_mask(const float* coarse, int cnx, int cny, int cnz,
-                                   const double* clo, const double* ch, int fnx, int fny, int fnz,
-                                   const double* fh, double d, float* c_fine, float* out_unmasked,
-                                   uint8_t* mask_new, int32_t* block_counts,
-                                   const uint8_t* mask_old, float* run_min, int32_t* front,
-                                   int32_t* back, void* stream) {
+extern "C" int rtsdf_resample_mask_range(const float* coarse, int cnx, int cny, int cnz,
+                                         const double* clo, const double* ch, int fnx, int fny,
+                                         int fnz, const double* fh, double d, int64_t c0,
+                                         int64_t n_range, float* c_fine, float* out_unmasked,
+                                         uint8_t* mask_new, int32_t* block_counts,
+                                         const uint8_t* mask_old, float* run_min, int32_t* front,
+                                         int32_t* back, void* stream) {
     if (cnx < 1 || cny < 1 || cnz < 1 || fnx < 1 || fny < 1 || fnz < 1) {
         set_error("resample_mask: bad dims");
+        return RTSDF_ERR_INVALID;
+    }
+    const int64_t n_fine = (int64_t)fnx * fny * fnz;
+    if (c0 < 0 || n_range < 0 || c0 + n_range > n_fine || n_fine >= ((int64_t)1 << 31)) {
+        set_error("resample_mask: cell range [%lld, %lld) outside the fine grid", (long long)c0,
+                  (long long)(c0 + n_range));
         return RTSDF_ERR_INVALID;
     }
     if (mask_old && (!run_min || !front || !back)) {
         set_error("resample_mask: mask_old needs run_min/front/back");
         return RTSDF_ERR_INVALID;
     }
+    if (n_range == 0) return RTSDF_OK;
     RsParams P;
     P.coarse = FieldView{coarse, cnx, cny, cnz, clo[0], clo[1], clo[2], ch[0], ch[1], ch[2], 0.0f};
     P.fnx = fnx;
@@ -227,14 +236,26 @@ extern "C" int rtsdf_resample_mask(const float* coarse, int cnx, int cny, int cn
     P.fhy = fh[1];
     P.fhz = fh[2];
     P.d = d;
-    P.n_cells = (int64_t)fnx * fny * fnz;
+    P.c0 = c0;
+    P.n_cells = n_range;
     P.div_ny = make_fastdiv((uint32_t)fny);
     P.div_nz = make_fastdiv((uint32_t)fnz);
-    int64_t nb = rtsdf_mask_blocks(P.n_cells);
+    int64_t nb = rtsdf_mask_blocks(n_range);
     resample_mask_kernel<<<(unsigned)nb, RS_THREADS, 0, (cudaStream_t)stream>>>(
         P, c_fine, out_unmasked, mask_new, block_counts, mask_old, run_min, front, back);
     count_launch();
     return check_launch("resample_mask");
+}
+
+extern "C" int rtsdf_resample_mask(const float* coarse, int cnx, int cny, int cnz,
+                                   const double* clo, const double* ch, int fnx, int fny, int fnz,
+                                   const double* fh, double d, float* c_fine, float* out_unmasked,
+                                   uint8_t* mask_new, int32_t* block_counts,
+                                   const uint8_t* mask_old, float* run_min, int32_t* front,
+                                   int32_t* back, void* stream) {
+    return rtsdf_resample_mask_range(coarse, cnx, cny, cnz, clo, ch, fnx, fny, fnz, fh, d, 0,
+                                     (int64_t)fnx * fny * fnz, c_fine, out_unmasked, mask_new,
+                                     block_counts, mask_old, run_min, front, back, stream);
 }
 
 extern "C" size_t rtsdf_compact_ws_bytes(int64_t n_cells) {
@@ -242,23 +263,33 @@ extern "C" size_t rtsdf_compact_ws_bytes(int64_t n_cells) {
     return (size_t)nb * (sizeof(int64_t) + sizeof(int32_t)) + 256;
 }
 
-extern "C" int rtsdf_compact_mask(const uint8_t* mask, int64_t n, int32_t* block_counts,
-                                  int64_t* idx, int64_t* count, void* ws, size_t ws_bytes,
-                                  void* stream_) {
+extern "C" int rtsdf_compact_mask_range(const uint8_t* mask, int64_t c0, int64_t n,
+                                        int32_t* block_counts, int64_t* idx, int64_t* count,
+                                        void* ws, size_t ws_bytes, void* stream_) {
     cudaStream_t stream = (cudaStream_t)stream_;
     int64_t nb = rtsdf_mask_blocks(n);
     if (ws_bytes < rtsdf_compact_ws_bytes(n)) {
         set_error("compact_mask: workspace too small");
         return RTSDF_ERR_WORKSPACE;
     }
+    if (n <= 0) {
+        cudaMemsetAsync(count, 0, sizeof(int64_t), stream);
+        return check_launch("compact_mask");
+    }
     int64_t* offsets = (int64_t*)ws;
     if (!block_counts) {
         block_counts = (int32_t*)((char*)ws + nb * sizeof(int64_t));
-        count_mask_kernel<<<(unsigned)nb, RS_THREADS, 0, stream>>>(mask, n, block_counts);
+        count_mask_kernel<<<(unsigned)nb, RS_THREADS, 0, stream>>>(mask, c0, n, block_counts);
         count_launch();
     }
     scan_blocks_kernel<<<1, 1024, 0, stream>>>(block_counts, nb, offsets, count);
-    compact_kernel<<<(unsigned)nb, RS_THREADS, 0, stream>>>(mask, n, offsets, idx);
+    compact_kernel<<<(unsigned)nb, RS_THREADS, 0, stream>>>(mask, c0, n, offsets, idx);
     count_launch(2);
     return check_launch("compact_mask");
+}
+
+extern "C" int rtsdf_compact_mask(const uint8_t* mask, int64_t n, int32_t* block_counts,
+                                  int64_t* idx, int64_t* count, void* ws, size_t ws_bytes,
+                                  void* stream_) {
+    return rtsdf_compact_mask_range(mask, 0, n, block_counts, idx, count, ws, ws_bytes, stream_);
 }

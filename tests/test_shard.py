@@ -1,0 +1,80 @@
+"""z-slab sharded hybrid frame: the slab exchanges on a real
+world-size-2 gloo group (CPU), and -- on the GPU -- W slab ranks in one
+process (exchanges by copies) against the single-GPU FramePipeline, bit for
+bit (fine field, masked count, shaded image)."""
+
+import os
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2210_06160_b200 import slab as S
+
+
+def _halo_worker(rank, world, port, ret):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2210_06160_b200.shard import exchange_coarse_halo, gather_slabs
+
+    nx, ny, nz = 10, 3, 4
+    full = torch.arange(nx * ny * nz, dtype=torch.float32).reshape(nx, ny, nz)
+    bounds = S.slab_bounds(nx, world)
+    x0, nxl = bounds[rank]
+    h = torch.full((nxl + 2, ny, nz), -1.0)
+    h[1:nxl + 1] = full[x0:x0 + nxl]
+    exchange_coarse_halo(h, rank, world)
+    ok = True
+    if rank > 0:
+        ok &= torch.equal(h[0], full[x0 - 1])
+    if rank < world - 1:
+        ok &= torch.equal(h[nxl + 1], full[x0 + nxl])
+    got = gather_slabs(h[1:nxl + 1], bounds, rank)
+    if rank == 0:
+        ok &= torch.equal(got, full)
+    ret.put((rank, bool(ok)))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_gloo_coarse_halo_and_gather(world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 29700 + os.getpid() % 1000 + world
+    procs = [ctx.Process(target=_halo_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=300) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert all(res.values()), res
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("scene_name,dims,frames,world", [
+    ("sphere", (64, 64, 64), 3, 2),
+    ("sphere", (64, 64, 64), 2, 3),
+    ("sphere_plane", (400, 200, 400), 2, 2),
+    ("sphere_plane", (400, 200, 400), 1, 8),
+])
+def test_loopback_sharded_frame_equals_single_gpu(scene_name, dims, frames, world):
+    import paper_2210_06160_b200 as rt
+    from paper_2210_06160_b200.shard import LoopbackCluster
+
+    cfg = rt.PipelineConfig(coarse_dims=dims, fine_dims=dims,
+                            sampling=rt.SamplingParams(rays_per_frame=32))
+    ref = rt.FramePipeline(rt.get_scene(scene_name), cfg)
+    cl = LoopbackCluster(rt.get_scene(scene_name), cfg, world)
+    for f in range(frames):
+        last = f == frames - 1
+        rec = ref.advance(render=last, timing=False)
+        m = cl.advance(render=last)
+        assert m == rec.masked_texels
+        assert torch.equal(cl.fine, ref.fine.data), f
+    assert torch.equal(cl.last_image, ref.last_image)
+    np.testing.assert_array_equal(cl.ranks[0].coarse_owned().cpu().numpy(),
+                                  ref.coarse.data[:cl.ranks[0].nxl].cpu().numpy())
