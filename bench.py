@@ -8,8 +8,10 @@ soft-shadow march 240x180 -> compose, all on the device.
 
     python bench.py [--gpus N --steps K --warmup W] [--impl ours|reference]
 
-N > 1 (torchrun, one rank per GPU): every rank runs its own frames
-(replicas, "scaling": "weak"); value = max-over-ranks time / all frames.
+N > 1 (torchrun, one rank per GPU): the z-slab sharded frame (shard.py: each
+frame split over the N GPUs, NCCL P2P halo planes per JFA pass, fine slabs
+gathered on rank 0 for the shading; "scaling": "strong"), value = max-over-
+ranks time / frames; --replicas runs N independent frames instead ("weak").
 --impl reference times the reference algorithm's CPU implementation (the
 oracle port in oracle/, OpenMP over all host cores) on a bounded sample of
 the same frame per step.
@@ -46,6 +48,10 @@ def parse():
     ap.add_argument("--rays", type=int, default=32)
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--parts", type=int, default=8, help="reference arm: sample = 1/parts")
+    ap.add_argument("--replicas", action="store_true",
+                    help="N > 1: N independent frames instead of the z-slab sharded frame")
+    ap.add_argument("--sharded", action="store_true",
+                    help="use the sharded frame even at N = 1 (under torchrun; tests the glue)")
     return ap.parse_args()
 
 
@@ -140,10 +146,22 @@ def run_ours(args, rank, world, local_rank):
     cfg = rt.PipelineConfig(coarse_dims=DIMS, fine_dims=DIMS,
                             sampling=rt.SamplingParams(rays_per_frame=args.rays, mask_distance=0.1,
                                                        decay_alpha=0.95, seed=0))
-    pipe = rt.FramePipeline(scene, cfg)
+    # N > 1: the z-slab sharded frame (each frame split over the N GPUs, NCCL
+    # P2P halos per JFA pass, fine slabs gathered for the shading on rank 0);
+    # --replicas: N independent frames instead
+    sharded = (dist or args.sharded) and not args.replicas
+    if sharded:
+        from paper_2210_06160_b200.shard import ShardedFramePipeline
 
-    def step():
-        pipe.advance(render=True, timing=False)
+        sp = ShardedFramePipeline(scene, cfg, rank, world)
+
+        def step():
+            sp.advance(render=True)
+    else:
+        pipe = rt.FramePipeline(scene, cfg)
+
+        def step():
+            pipe.advance(render=True, timing=False)
 
     for _ in range(max(3, args.warmup)):
         step()
@@ -165,9 +183,58 @@ def run_ours(args, rank, world, local_rank):
         t = torch.tensor([ms_total], device="cuda")
         tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
         ms_total = float(t.item())
-    frames = args.steps * world
+    frames = args.steps if sharded else args.steps * world
     value = ms_total / frames
     ms_per_step = ms_total / args.steps
+
+    # ---- e2e through the public API with host buffers
+    view = scene.view(0)
+    mb = view.mesh_buffers()
+    hv = torch.from_numpy(view.mesh.vertices.copy()).pin_memory()
+    ht = torch.from_numpy(view.mesh.triangles.copy()).pin_memory()
+    img_host = torch.empty((scene.camera.height, scene.camera.width, 3), dtype=torch.float32).pin_memory()
+    cnt_host = torch.empty(1, dtype=torch.int64).pin_memory()
+    h2d = hv.numel() * 8 + ht.numel() * 4
+    d2h = img_host.numel() * 4 + 8
+
+    def e2e_step():
+        mb.verts.copy_(hv, non_blocking=True)
+        mb.tris.copy_(ht, non_blocking=True)
+        if sharded:
+            cnt, img = sp.advance(render=True)
+            if img is not None:
+                img_host.copy_(img, non_blocking=True)
+            cnt_host.copy_(cnt, non_blocking=True)
+        else:
+            r = pipe.advance(render=True, timing=False)
+            img_host.copy_(pipe.last_image, non_blocking=True)
+            cnt_host.copy_(r._masked_dev, non_blocking=True)
+
+    for _ in range(2):
+        e2e_step()
+    barrier()
+    a, z = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(args.steps):
+        e2e_step()
+    z.record()
+    barrier()
+    e_ms = a.elapsed_time(z)
+    if dist:
+        t = torch.tensor([e_ms], device="cuda")
+        tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+        e_ms = float(t.item())
+    e2e = {"value": e_ms / frames, "unit": UNIT, "h2d_bytes_per_step": h2d,
+           "d2h_bytes_per_step": d2h,
+           "path": ("pinned mesh H2D -> ShardedFramePipeline.advance(render=True) on every rank -> "
+                    "image (rank 0) + masked-count D2H") if sharded else
+                   "pinned mesh H2D -> FramePipeline.advance(render=True) -> image + masked-count D2H"}
+    if sharded:  # kernel-level detail below runs on a single-GPU pipeline per rank
+        del sp
+        torch.cuda.empty_cache()
+        pipe = rt.FramePipeline(scene, cfg)
+        for _ in range(2):
+            pipe.advance(render=True, timing=False)
 
     # ---- per-stage breakdown on this rank (one instrumented frame + standalone kernels)
     rec = pipe.advance(render=True, timing=True)
@@ -177,7 +244,6 @@ def run_ours(args, rank, world, local_rank):
     h = (scene.hi - scene.lo) / np.array(DIMS, dtype=np.float64)
     w = J.integer_weights(*map(float, h), DIMS)
     offs = J.jfa_offsets(DIMS)
-    view = scene.view(0)
     # JFA: re-run the schedule from fresh seeds, one event pair per pass
     per_pass = []
     for rep in range(3):
@@ -227,52 +293,19 @@ def run_ours(args, rank, world, local_rank):
     sample_ms = ev[0].elapsed_time(ev[1])
     rays = masked * args.rays
 
-    # ---- e2e through the public API with host buffers
-    e2e = None
-    if True:
-        mb = view.mesh_buffers()
-        hv = torch.from_numpy(view.mesh.vertices.copy()).pin_memory()
-        ht = torch.from_numpy(view.mesh.triangles.copy()).pin_memory()
-        img_host = torch.empty(pipe.last_image.shape if pipe.last_image is not None else (180, 240, 3),
-                               dtype=torch.float32).pin_memory()
-        cnt_host = torch.empty(1, dtype=torch.int64).pin_memory()
-        h2d = hv.numel() * 8 + ht.numel() * 4
-        d2h = img_host.numel() * 4 + 8
-
-        def e2e_step():
-            mb.verts.copy_(hv, non_blocking=True)
-            mb.tris.copy_(ht, non_blocking=True)
-            r = pipe.advance(render=True, timing=False)
-            img_host.copy_(pipe.last_image, non_blocking=True)
-            cnt_host.copy_(r._masked_dev, non_blocking=True)
-
-        for _ in range(2):
-            e2e_step()
-        barrier()
-        a, z = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record()
-        for _ in range(args.steps):
-            e2e_step()
-        z.record()
-        barrier()
-        e_ms = a.elapsed_time(z)
-        if dist:
-            t = torch.tensor([e_ms], device="cuda")
-            tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
-            e_ms = float(t.item())
-        e2e = {"value": e_ms / (args.steps * world), "unit": UNIT, "h2d_bytes_per_step": h2d,
-               "d2h_bytes_per_step": d2h,
-               "path": "pinned mesh H2D -> FramePipeline.advance(render=True) -> image + masked-count D2H"}
-
     kernels_ms = {"jfa_pass_total": jfa_ms, "sample_update": sample_ms}
     traffic_b, traffic_src = jfa_traffic()
     dominant = "sample_update" if sample_ms > jfa_ms / len(offs) else "jfa_step"
     out = {
         "metric": METRIC, "value": round(value, 4), "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": round(ms_per_step, 4),
-        "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f64+i32",
+        "higher_is_better": False, "scaling": "strong" if sharded else "weak", "vs_baseline": None,
+        "dtype": "f64+i32",
         "data": "synthetic: reference-identical procedural sphere_plane scene (1,282 triangles)",
-        "config": dict(workload(args.rays), parallelism=f"replicas x{world}" if world > 1 else "1 GPU"),
+        "config": dict(workload(args.rays),
+                       parallelism=(f"z-slab x{world} (NCCL P2P halos per JFA pass, coarse 1-plane "
+                                    "halo, fine slabs gathered for DL)") if sharded else
+                       (f"replicas x{world}" if world > 1 else "1 GPU")),
         "frame_stages_ms": {k: round(v, 4) for k, v in stages_ms.items()},
         "masked_texels": masked, "rays_per_frame": rays,
         "rays_per_s": round(rays / (sample_ms * 1e-3), 1),
@@ -374,18 +407,19 @@ def main():
         if rank == 0:
             print(json.dumps(run_reference(args)), flush=True)
         return
-    if world > 1:
+    group = world > 1 or args.sharded
+    if group:
         import torch
         import torch.distributed as tdist
 
         torch.cuda.set_device(local_rank)
-        tdist.init_process_group("nccl")
+        tdist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     out = run_ours(args, rank, world, local_rank)
     if rank == 0:
         if world == 1 and not args.no_cpu:
             out["cpu_baseline"] = run_cpu_baseline()
         print(json.dumps(out), flush=True)
-    if world > 1:
+    if group:
         import torch.distributed as tdist
 
         tdist.barrier()
