@@ -327,7 +327,10 @@ class HybridOracle:
     """FramePipeline.advance (pipeline.py:109-160) on the CPU oracle."""
 
     def __init__(self, verts, tris, normals, bounds, coarse_dims, fine_dims, x=32, d=0.1,
-                 alpha=0.95, seed=0, beta=0.0):
+                 alpha=0.95, seed=0, beta=0.0, mesh_fn=None):
+        # mesh_fn(frame) -> (verts, tris, normals): animated scenes re-voxelize
+        # and rebuild the BVH every frame (pipeline.py:116-119, scenes.py:56-93)
+        self.mesh_fn = mesh_fn
         self.verts, self.tris, self.normals = verts, tris, normals
         self.lo = np.asarray(bounds[0], np.float64)
         self.hi = np.asarray(bounds[1], np.float64)
@@ -340,6 +343,9 @@ class HybridOracle:
         self.frame = 0
 
     def advance(self, dirs_fn=None):
+        if self.mesh_fn is not None:
+            self.verts, self.tris, self.normals = self.mesh_fn(self.frame)
+            self.bvh = bvh_build(self.verts, self.tris, self.normals)
         occ = voxelize(self.verts, self.tris, self.coarse_dims, (self.lo, self.hi))
         h = (self.hi - self.lo) / np.array(self.coarse_dims, dtype=np.float64)
         seeds = jfa_run(occ, h)
