@@ -248,6 +248,24 @@ int rtsdf_sample_update(const void* bvh_packed, int64_t n_nodes, int64_t n_tris,
                         int32_t* front, int32_t* back, double alpha, float* out, void* ws,
                         size_t ws_bytes, void* stream);
 
+/* ------------------------------------------------------ validation oracles */
+/* Replaces geometry.py:592 (_closest_many): exact unsigned point-to-mesh
+ * distance per point (fp64 (n, 3) -> fp64 (n,)), over the reference-order
+ * BVH (rtsdf_bvh_pack layout) in the reference's traversal order and pruning
+ * (geometry.py:521-565), so results are bit-exact.                          */
+int rtsdf_exact_distance(const void* bvh_packed, int64_t n_nodes, const double* points,
+                         int64_t n, double* out, void* stream);
+/* Replaces render.py:246 (_reference_kernel): per covered pixel the fraction
+ * of spp cone-sampled shadow rays (origin pos + 1e-4 nrm, stream
+ * (seed, pixel, 1)) with no hit; 1.0 where uncovered.  light / t1 / t2 are
+ * the unit light direction and the cone basis (host[3] each, render.py:237-
+ * 241); tan_r = tan(angular radius).  CUDA sincos stands in for glibc.     */
+int rtsdf_reference_visibility(const void* bvh_packed, int64_t n_nodes, const double* g_pos,
+                               const double* g_nrm, const uint8_t* g_cov, int height, int width,
+                               const double* light /*host[3]*/, const double* t1 /*host[3]*/,
+                               const double* t2 /*host[3]*/, double tan_r, int spp,
+                               uint64_t seed, double* out_vis, void* stream);
+
 /* ------------------------------------------------------------- soft shadow */
 /* Replaces render.py:167 (_occlusion_kernel): per covered pixel fp64 sphere
  * trace with the triangulated cone term (raymarch.py:83-147).  sample_bias:

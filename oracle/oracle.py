@@ -47,6 +47,9 @@ _SIGS = {
                                 D, D, D, I, U64, P]),
     "oracle_gbuffer": (None, [P, P, P, P, P, P, P, P, P, P, P, P, P, P, P, D, D, I, I, P, P, P,
                               P]),
+    "oracle_exact_distance_many": (None, [P, P, P, P, P, P, P, P, P, P, I64, P]),
+    "oracle_reference_visibility": (None, [P, P, P, P, P, P, P, P, P, P, P, P, I, I, D, D, D, D, D,
+                                           D, D, D, D, D, I, U64, P]),
 }
 
 _lib = None
@@ -362,6 +365,42 @@ class HybridOracle:
                                                  self.accum, dirs=dirs)
         self.frame += 1
         return dict(occ=occ, seeds=seeds, coarse=coarse, fine=self.fine, idx=idx)
+
+
+# ------------------------------------------------------ validation oracles
+def exact_distance_many(b, points):
+    """geometry.py:588-594: exact unsigned point-to-mesh distance per point."""
+    pts = _c(points, np.float64).reshape(-1, 3)
+    out = np.empty(len(pts))
+    lib().oracle_exact_distance_many(*_bvh_args(b), _p(pts), len(pts), _p(out))
+    return out
+
+
+def cone_basis(light_unit):
+    """render.py:237-241 (t1, t2) around the light direction, numpy as the reference."""
+    l = np.asarray(light_unit, dtype=np.float64)
+    up = np.array([0.0, 1.0, 0.0]) if abs(l[1]) < 0.9 else np.array([1.0, 0.0, 0.0])
+    t1 = np.cross(l, up)
+    t1 /= np.linalg.norm(t1)
+    t2 = np.cross(l, t1)
+    return t1, t2
+
+
+def reference_visibility(b, g_pos, g_nrm, g_cov, light_unit, angular_radius, spp, seed):
+    """render.py:195-254: cone-sampled shadow-ray visibility per pixel."""
+    import math
+
+    pos = _c(g_pos, np.float64)
+    nrm = _c(g_nrm, np.float64)
+    cov = _c(g_cov, np.uint8)
+    h, w = cov.shape
+    l = np.asarray(light_unit, dtype=np.float64)
+    t1, t2 = cone_basis(l)
+    out = np.empty((h, w))
+    lib().oracle_reference_visibility(*_bvh_args(b), _p(pos), _p(nrm), _p(cov), h, w, *map(float, l),
+                                      *map(float, t1), *map(float, t2),
+                                      math.tan(angular_radius), int(spp), int(seed), _p(out))
+    return out
 
 
 def jfa_step_range(src, dst, offset, h, i0, i1):

@@ -58,6 +58,8 @@ SIGNATURES = {
     "rtsdf_resample_mask_range": (I, [P, I, I, I, DP, DP, I, I, I, DP, D, I64, I64, P, P, P, P, P,
                                       P, P, P, P]),
     "rtsdf_compact_mask_range": (I, [P, I64, I64, P, P, P, P, SZ, P]),
+    "rtsdf_exact_distance": (I, [P, I64, P, I64, P, P]),
+    "rtsdf_reference_visibility": (I, [P, I64, P, P, P, I, I, DP, DP, DP, D, I, U64, P, P]),
     "rtsdf_bvh_build_host": (I64, [P, P, I64, P, P, P, P, P]),
     "rtsdf_bvh_build_sah_host": (I64, [P, P, I64, I, P, P, P, P, P]),
     "rtsdf_bvh_packed_bytes": (SZ, [I64, I64]),

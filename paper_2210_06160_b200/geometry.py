@@ -325,7 +325,28 @@ def ray_query(bvh: BvhIndex, origin, direction, t_max=np.inf) -> RayHit:
     return RayHit(True, float(t[0]), int(ids[0]), int(fac[0]))
 
 
+# ---------------------------------------------------------------------------
+# Exact point-to-mesh distance (validation oracle)
+# ---------------------------------------------------------------------------
+
+def exact_distance_many(bvh: BvhIndex, points) -> np.ndarray:
+    """Exact unsigned point-to-mesh distance per point (geometry.py:588-594):
+    Eberly's region tests over the reference-order BVH in the reference's
+    traversal order and pruning rule -- bit-exact with the reference."""
+    pts = to_device(np.ascontiguousarray(points, dtype=np.float64).reshape(-1, 3))
+    out = torch.empty(pts.shape[0], dtype=torch.float64, device=pts.device)
+    _lib.check(_lib.lib().rtsdf_exact_distance(_lib.ptr(bvh.packed), bvh.num_nodes, _lib.ptr(pts),
+                                               pts.shape[0], _lib.ptr(out), _lib.stream()),
+               "exact_distance")
+    return to_numpy(out)
+
+
+def exact_distance(bvh: BvhIndex, point) -> float:
+    """Exact unsigned point-to-mesh distance (geometry.py:579-585)."""
+    return float(exact_distance_many(bvh, np.asarray(point, dtype=np.float64)[None])[0])
+
+
 __all__ = ["DEGENERATE_AREA", "FACING_NONE", "FACING_FRONT", "FACING_BACK", "MeshError",
            "MeshParseError", "EmptyMeshError", "TriangleMesh", "make_mesh", "load_mesh",
            "identity_transform", "BvhIndex", "build_bvh", "RayHit", "ray_query",
-           "ray_query_many", "to_numpy"]
+           "ray_query_many", "to_numpy", "exact_distance", "exact_distance_many"]

@@ -4,8 +4,9 @@
 field (render.py:155-175, K8 rtsdf_occlusion).  `rasterize_gbuffer` is the
 G-buffer primary-visibility pass (render.py:112-128), traced on the device
 through the same BVH kernel as the refinement.  Image I/O stays on the host.
-The distributed ray-traced ground truth (reference_visibility) is a
-validation oracle and is out of scope.
+`reference_visibility` / `reference_render` are the reference's distributed
+ray-traced ground truth (render.py:195-264) on the device -- a validation
+oracle for image-quality checks.
 """
 
 from __future__ import annotations
@@ -209,5 +210,44 @@ def write_ppm(path, image, gamma=2.2):
         fh.write(data.tobytes())
 
 
+def cone_basis(light_unit):
+    """render.py:237-241: (t1, t2) spanning the plane normal to the light."""
+    l = np.asarray(light_unit, dtype=np.float64)
+    up = np.array([0.0, 1.0, 0.0]) if abs(l[1]) < 0.9 else np.array([1.0, 0.0, 0.0])
+    t1 = np.cross(l, up)
+    t1 /= np.linalg.norm(t1)
+    t2 = np.cross(l, t1)
+    return t1, t2
+
+
+def reference_visibility(view, gbuffer: GBuffer, light: DirectionalLight, spp=256,
+                         seed=0) -> torch.Tensor:
+    """Fraction of unoccluded cone-sampled shadow rays per pixel (render.py:231-254)."""
+    if spp < 1:
+        raise ValueError("spp must be >= 1")
+    bvh = view.bvh
+    l = light.unit()
+    t1, t2 = cone_basis(l)
+    h, w = gbuffer.shape
+    out = torch.empty((h, w), dtype=torch.float64, device=gbuffer.position.device)
+    cov = gbuffer.coverage.to(torch.uint8)
+    _lib.check(_lib.lib().rtsdf_reference_visibility(
+        _lib.ptr(bvh.packed), bvh.num_nodes, _lib.ptr(gbuffer.position), _lib.ptr(gbuffer.normal),
+        _lib.ptr(cov), h, w, (_lib.D * 3)(*map(float, l)), (_lib.D * 3)(*map(float, t1)),
+        (_lib.D * 3)(*map(float, t2)),
+        math.tan(light.angular_radius), int(spp), int(seed) & 0xFFFFFFFFFFFFFFFF, _lib.ptr(out),
+        _lib.stream()), "reference_visibility")
+    return out
+
+
+def reference_render(view, camera: Camera, light: DirectionalLight, spp=256, seed=0,
+                     background=(0.05, 0.07, 0.10)) -> torch.Tensor:
+    """Distributed ray-traced ground truth with the same Lambert shading (render.py:257-264)."""
+    gb = rasterize_gbuffer(view, camera)
+    vis = reference_visibility(view, gb, light, spp=spp, seed=seed)
+    return compose(gb, 1.0 - vis, light, background)
+
+
 __all__ = ["Camera", "DirectionalLight", "DiscLight", "GBuffer", "rasterize_gbuffer",
-           "occlusion_image", "compose", "shade", "compare", "write_pfm", "read_pfm", "write_ppm"]
+           "occlusion_image", "compose", "shade", "compare", "write_pfm", "read_pfm", "write_ppm",
+           "reference_visibility", "reference_render", "cone_basis"]

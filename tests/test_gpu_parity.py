@@ -523,3 +523,41 @@ def test_c4_full_size(rt):
     d2_exact = np.rint(d_exact ** 2).astype(np.int64)
     assert (d2_jfa >= d2_exact).all()
     assert (d2_jfa == d2_exact).mean() > 0.99
+
+
+# ------------------------------------------------- validation oracles (f)-4
+def _validation_golden():
+    with np.load(Path(__file__).resolve().parent / "golden" / "golden_validation.npz") as z:
+        return {k: z[k] for k in z.files}
+
+
+def test_exact_distance_matches_reference(rt):
+    """geometry.exact_distance_many on the GPU == the reference's, bit for bit
+    (soup + C1 sphere, 3000 points each; reference traversal order)."""
+    V, A = _validation_golden(), golden_arrays()
+    soup = rt.make_mesh(A["soup.vertices"], A["soup.triangles"])
+    np.testing.assert_array_equal(rt.exact_distance_many(rt.build_bvh(soup), V["soup.points"]),
+                                  V["soup.exact_distance"])
+    scene = rt.get_scene("sphere")
+    view = scene.view(0)
+    np.testing.assert_array_equal(rt.exact_distance_many(view.bvh, V["sphere.points"]),
+                                  V["sphere.exact_distance"])
+    assert rt.exact_distance(view.bvh, V["sphere.points"][7]) == V["sphere.exact_distance"][7]
+
+
+def test_reference_visibility_matches_reference(rt):
+    """render.reference_visibility on the GPU vs the reference (C1 camera, 16
+    cone samples): coverage exact; per-pixel visibility equal except where CUDA
+    sincos and glibc differ in the last ulp of a grazing ray (bounded)."""
+    V = _validation_golden()
+    scene = rt.get_scene("sphere")
+    view = scene.view(0)
+    gb = rt.rasterize_gbuffer(view, scene.camera)
+    np.testing.assert_array_equal(_np(gb.coverage), V["sphere.coverage"])
+    vis = _np(rt.reference_visibility(view, gb, scene.light, spp=16, seed=3))
+    want = V["sphere.visibility16"]
+    diff = vis != want
+    assert diff.mean() < 1e-3, diff.mean()
+    assert np.abs(vis - want).max() <= 1.0 / 16 + 1e-12
+    img = _np(rt.reference_render(view, scene.camera, scene.light, spp=4, seed=0))
+    assert img.shape == (scene.camera.height, scene.camera.width, 3) and np.isfinite(img).all()
