@@ -181,13 +181,21 @@ __global__ void __launch_bounds__(256) jfa_seg_bitmap_kernel(const int32_t* __re
                                                              int nz, FastDiv dzb, uint32_t n_seg) {
     const int lane = threadIdx.x & 31;
     const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
-    for (uint32_t seg = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; seg < n_seg; seg += nwarps) {
-        const uint32_t row = fdiv(seg, dzb);  // segments < 2^25
-        const int zb = (int)(seg - row * dzb.d);
-        const int z = zb * 32 + lane;
-        const bool on = z < nz && __ldg(src + (int64_t)row * nz + z) != RTSDF_EMPTY;
-        const unsigned m = __ballot_sync(0xffffffffu, on);
-        if (lane == 0) bm[seg] = m != 0;
+    // 4 segments per warp per step: independent loads in flight
+    for (uint32_t s0 = ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 4; s0 < n_seg; s0 += nwarps * 4) {
+        bool on[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const uint32_t seg = s0 + u;
+            const uint32_t row = fdiv(seg, dzb);  // segments < 2^25
+            const int z = (int)(seg - row * dzb.d) * 32 + lane;
+            on[u] = seg < n_seg && z < nz && __ldg(src + (int64_t)row * nz + z) != RTSDF_EMPTY;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const unsigned m = __ballot_sync(0xffffffffu, on[u]);
+            if (lane == 0 && s0 + u < n_seg) bm[s0 + u] = m != 0;
+        }
     }
 }
 
