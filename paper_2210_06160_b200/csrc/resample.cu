@@ -171,29 +171,47 @@ __global__ void __launch_bounds__(1024) scan_blocks_kernel(const int32_t* __rest
     if (threadIdx.x == 1023) *total = part[1023];
 }
 
+// One thread owns RS_PER_THREAD (16) consecutive cells: the mask bytes (0/1)
+// are read as one 16-byte vector where aligned, turned into a 16-bit set
+// ((w & 0x01010101) * 0x01020408 >> 24 gathers the four byte flags of a word),
+// one block-wide exclusive scan of the per-thread counts places them, and
+// each thread writes its indices in ascending order -- the same block
+// partition as the resample kernel's block_counts.
 __global__ void __launch_bounds__(RS_THREADS) compact_kernel(const uint8_t* __restrict__ mask,
                                                             int64_t c0, int64_t n,
                                                             const int64_t* __restrict__ offsets,
                                                             int64_t* __restrict__ idx) {
-    __shared__ int warp_cnt[RS_THREADS / 32];
-    const int64_t base = (int64_t)blockIdx.x * RS_CELLS_PER_BLOCK;
-    int64_t run = offsets[blockIdx.x];
+    __shared__ int warp_tot[RS_THREADS / 32];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    for (int r = 0; r < RS_PER_THREAD; ++r) {
-        int64_t c = base + r * RS_THREADS + threadIdx.x;
-        bool m = c < n && mask[c0 + c] != 0;
-        unsigned bal = __ballot_sync(0xffffffffu, m);
-        if (lane == 0) warp_cnt[wid] = __popc(bal);
-        __syncthreads();
-        int before = 0, all = 0;
-        for (int w = 0; w < RS_THREADS / 32; ++w) {
-            int v = warp_cnt[w];
-            before += w < wid ? v : 0;
-            all += v;
-        }
-        if (m) idx[run + before + __popc(bal & ((1u << lane) - 1))] = c0 + c;
-        run += all;
-        __syncthreads();
+    const int64_t base = (int64_t)blockIdx.x * RS_CELLS_PER_BLOCK + (int64_t)threadIdx.x * RS_PER_THREAD;
+    const uint8_t* m = mask + c0 + base;
+    uint32_t bits = 0;
+    if (base + RS_PER_THREAD <= n && ((uintptr_t)m & 15) == 0) {
+        const uint4 v = __ldg((const uint4*)m);
+        const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int q = 0; q < 4; ++q) bits |= (((w[q] & 0x01010101u) * 0x01020408u) >> 24 & 0xFu) << (4 * q);
+    } else {
+        for (int r = 0; r < RS_PER_THREAD; ++r)
+            if (base + r < n && m[r] != 0) bits |= 1u << r;
+    }
+    const int cnt = __popc(bits);
+    int incl = cnt;  // warp inclusive scan
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += v;
+    }
+    if (lane == 31) warp_tot[wid] = incl;
+    __syncthreads();
+    int before = 0;
+#pragma unroll
+    for (int w = 0; w < RS_THREADS / 32; ++w) before += w < wid ? warp_tot[w] : 0;
+    int64_t out = offsets[blockIdx.x] + before + incl - cnt;
+    while (bits) {
+        const int r = __ffs(bits) - 1;
+        idx[out++] = c0 + base + r;
+        bits &= bits - 1;
     }
 }
 

@@ -199,6 +199,28 @@ def test_resample_mask_compaction(rt, coarse_dims, fine_dims):
     np.testing.assert_array_equal(_np(idx), np.flatnonzero(want_m.ravel()))
 
 
+def test_compaction_random_odd_sizes_and_ranges(rt):
+    """Ordered compaction == np.flatnonzero on random masks of odd sizes, and
+    the range form (global cell addressing, unaligned c0) == the slice."""
+    import torch
+    from paper_2210_06160_b200 import _lib
+
+    rng = np.random.default_rng(5)
+    for n in (1, 15, 17, 4095, 4097, 100003):
+        m = rng.random(n) < 0.3
+        got = _np(rt.raysample.masked_indices(torch.from_numpy(m).cuda()))
+        np.testing.assert_array_equal(got, np.flatnonzero(m))
+    m = rng.random(200_000) < 0.1
+    md = torch.from_numpy(m).cuda()
+    for c0, cnt in ((0, 200_000), (7, 123_457), (4096 * 3 + 5, 50_001)):
+        cb = rt.raysample.CompactBuffers(cnt)
+        _lib.check(_lib.lib().rtsdf_compact_mask_range(
+            _lib.ptr(md), c0, cnt, None, _lib.ptr(cb.idx), _lib.ptr(cb.count), _lib.ptr(cb.ws),
+            cb.ws.numel(), _lib.stream()), "compact_mask_range")
+        k = int(cb.count.item())
+        np.testing.assert_array_equal(_np(cb.idx[:k]), c0 + np.flatnonzero(m[c0:c0 + cnt]))
+
+
 def test_bvh_closest_hits_match_reference(rt):
     G, A = golden(), golden_arrays()
     mesh = rt.make_mesh(A["soup.vertices"], A["soup.triangles"])
