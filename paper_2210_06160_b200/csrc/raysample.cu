@@ -29,6 +29,7 @@ struct SampleParams {
     uint64_t seed;
     int64_t frame;
     double t_max;
+    float tb;  // tmax_bound(t_max), computed once on the host
     const double* dirs;
     double* samp_min;
     int32_t* samp_front;
@@ -228,7 +229,7 @@ __device__ __forceinline__ double wf_trace(const SampleParams& P, double ox, dou
                                            bool* done) {
     if (WIDE)
         return trace_fast4(P.bvh4, ox, oy, oz, dx, dy, dz, P.t_max, stack, tstack, WF_THREADS, id,
-                           facing, budget, done);
+                           facing, budget, done, P.tb);
     return trace_fast(P.bvh, ox, oy, oz, dx, dy, dz, P.t_max, stack, WF_THREADS, id, facing,
                       budget, done);
 }
@@ -327,7 +328,7 @@ __global__ void __launch_bounds__(WF_THREADS, WF_MINB) wf_pass2_kernel(SamplePar
         int facing;
         // long rays: speculative while-while traversal (BVH4)
         double t = WIDE ? trace_fast4_ww(P.bvh4, ox, oy, oz, dx, dy, dz, P.t_max, stack_mem + threadIdx.x,
-                                         tstack_mem + threadIdx.x, WF_THREADS, id, facing)
+                                         tstack_mem + threadIdx.x, WF_THREADS, id, facing, P.tb)
                         : wf_trace<WIDE>(P, ox, oy, oz, dx, dy, dz, stack_mem + threadIdx.x,
                                          tstack_mem + threadIdx.x, id, facing, 0, nullptr);
         if (id >= 0) wf_commit(B, fdiv((unsigned)r, P.div_x), t, facing);
@@ -620,6 +621,7 @@ extern "C" int rtsdf_sample_update(const void* bvh_packed, int64_t n_nodes, int6
     P.seed = seed;
     P.frame = frame;
     P.t_max = t_max;
+    P.tb = tmax_bound(t_max);
     P.dirs = dirs;
     P.samp_min = samp_min;
     P.samp_front = samp_front;

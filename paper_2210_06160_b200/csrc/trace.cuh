@@ -91,11 +91,21 @@ __device__ __forceinline__ float clamp_inv(double d) {
     const float f = (float)d;
     float r;
     asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(f));
-    r = fabsf(f) < 1e-30f ? copysignf(1e30f, f) : r;
-    return fminf(fmaxf(r, -1e30f), 1e30f);
+    return fabsf(f) < 1e-30f ? copysignf(1e30f, f) : r;  // |1/f| <= ~1e30 otherwise
 }
 
 #define RTSDF_FINF __int_as_float(0x7f800000)
+
+// fp32 upper bound of t_max for the box tests (+inf beyond fp32 range)
+__host__ __device__ inline float tmax_bound(double t_max) {
+#ifdef __CUDA_ARCH__
+    return t_max < 3.0e38 ? __double2float_ru(t_max) : __int_as_float(0x7f800000);
+#else
+    if (!(t_max < 3.0e38)) return INFINITY;
+    float f = (float)t_max;
+    return (double)f < t_max ? nextafterf(f, INFINITY) : f;
+#endif
+}
 
 // Padded child box slab test: entry t (>= 0) or +inf if missed / beyond t_best.
 __device__ __forceinline__ float box_entry(float lx, float ly, float lz, float hx, float hy,
@@ -390,7 +400,7 @@ __device__ __forceinline__ double trace_fast4(const FastBvh4& b, double ox, doub
                                               double dx, double dy, double dz, double t_max,
                                               int32_t* stack, __half* tstack, int stride,
                                               int32_t& out_id, int& out_facing, int budget = 0,
-                                              bool* complete = nullptr) {
+                                              bool* complete = nullptr, float tb0 = -1.0f) {
     RayF r;
     r.ix = clamp_inv(dx);
     r.iy = clamp_inv(dy);
@@ -402,7 +412,7 @@ __device__ __forceinline__ double trace_fast4(const FastBvh4& b, double ox, doub
     double best_t = t_max;
     int32_t best_id = -1;
     int best_facing = 0;
-    float tb = t_max < 3.0e38 ? __double2float_ru(t_max) : RTSDF_FINF;
+    float tb = tb0 >= 0.0f ? tb0 : tmax_bound(t_max);
     int sp = 0;
     int32_t node = 0;
     if (complete) *complete = true;
@@ -498,7 +508,8 @@ __device__ __forceinline__ double trace_fast4(const FastBvh4& b, double ox, doub
 __device__ __forceinline__ double trace_fast4_ww(const FastBvh4& b, double ox, double oy,
                                                  double oz, double dx, double dy, double dz,
                                                  double t_max, int32_t* stack, __half* tstack,
-                                                 int stride, int32_t& out_id, int& out_facing) {
+                                                 int stride, int32_t& out_id, int& out_facing,
+                                                 float tb0 = -1.0f) {
     RayF r;
     r.ix = clamp_inv(dx);
     r.iy = clamp_inv(dy);
@@ -510,7 +521,7 @@ __device__ __forceinline__ double trace_fast4_ww(const FastBvh4& b, double ox, d
     double best_t = t_max;
     int32_t best_id = -1;
     int best_facing = 0;
-    float tb = t_max < 3.0e38 ? __double2float_ru(t_max) : RTSDF_FINF;
+    float tb = tb0 >= 0.0f ? tb0 : tmax_bound(t_max);
     int sp = 0;
     auto pop = [&]() -> int32_t {
         while (sp > 0) {
