@@ -14,6 +14,9 @@
 // evaluates the reference's fp64 expression when q ties -- bit-exact, with
 // integer work on the common path.  (0,0,0) weights select the FP64 path.
 #include <cmath>
+#include <map>
+#include <mutex>
+#include <tuple>
 
 #include "common.cuh"
 
@@ -178,7 +181,9 @@ __global__ void __launch_bounds__(256) jfa_step_kernel(PlaneSrc src, int32_t* __
 
 __global__ void __launch_bounds__(256) jfa_seg_bitmap_kernel(const int32_t* __restrict__ src,
                                                              uint8_t* __restrict__ bm, int ny,
-                                                             int nz, FastDiv dzb, uint32_t n_seg) {
+                                                             int nz, FastDiv dzb, uint32_t n_seg,
+                                                             unsigned long long* __restrict__ n_on) {
+    unsigned on_count = 0;
     const int lane = threadIdx.x & 31;
     const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
     // 4 segments per warp per step: independent loads in flight
@@ -195,8 +200,11 @@ __global__ void __launch_bounds__(256) jfa_seg_bitmap_kernel(const int32_t* __re
         for (int u = 0; u < 4; ++u) {
             const unsigned m = __ballot_sync(0xffffffffu, on[u]);
             if (lane == 0 && s0 + u < n_seg) bm[s0 + u] = m != 0;
+            on_count += m != 0;
         }
     }
+    if (lane == 0 && on_count) atomicAdd(n_on, (unsigned long long)on_count);
+    if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(n_on, 1ull);  // "measured" (+1)
 }
 
 template <int MODE>
@@ -204,7 +212,9 @@ __global__ void __launch_bounds__(256) jfa_sparse_kernel(const int32_t* __restri
                                                          int32_t* __restrict__ dst, JfaGeom g,
                                                          const uint8_t* __restrict__ bm_in,
                                                          uint8_t* __restrict__ bm_out,
-                                                         FastDiv dzb, FastDiv dny) {
+                                                         FastDiv dzb, FastDiv dny,
+                                                         unsigned long long* __restrict__ n_on) {
+    unsigned on_count = 0;
     const int nzb = (int)dzb.d;
     const uint32_t n_seg = (uint32_t)g.nx * g.ny * nzb;
     const int lane = threadIdx.x & 31;
@@ -267,7 +277,10 @@ __global__ void __launch_bounds__(256) jfa_sparse_kernel(const int32_t* __restri
         }
         const unsigned m = __ballot_sync(0xffffffffu, out != RTSDF_EMPTY);
         if (bm_out && lane == 0) bm_out[seg] = m != 0;
+        on_count += m != 0;
     }
+    if (n_on && lane == 0 && on_count) atomicAdd(n_on, (unsigned long long)on_count);
+    if (n_on && blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(n_on, 1ull);  // "measured" (+1)
 }
 
 __global__ void jfa_init_kernel(const uint8_t* __restrict__ occ, int ny, int nz, int64_t n,
@@ -466,13 +479,13 @@ static bool ws_ok(void* ws, size_t ws_bytes, int64_t n_cells) {
 
 using namespace rtsdf;
 
-// fix-up list (one int32 per cell) + two segment bitmaps for the sparse passes
 static size_t seg_bitmap_bytes(int nx, int ny, int nz) {
     return (((size_t)nx * ny * ((nz + 31) / 32)) + 255) / 256 * 256;
 }
 
+// fix-up list, two segment bitmaps, 32 per-pass segment-count slots
 extern "C" size_t rtsdf_jfa_ws_bytes(int nx, int ny, int nz) {
-    return 256 + (size_t)nx * ny * nz * sizeof(int32_t) + 2 * seg_bitmap_bytes(nx, ny, nz);
+    return 256 + (size_t)nx * ny * nz * sizeof(int32_t) + 2 * seg_bitmap_bytes(nx, ny, nz) + 256;
 }
 
 extern "C" int rtsdf_jfa_init(const uint8_t* occ, int nx, int ny, int nz, int32_t* seed,
@@ -517,6 +530,55 @@ extern "C" int rtsdf_jfa_step_slab(const int32_t* local, const int32_t* halo_lo,
     return launch_step(s, dst, g, true, ws, (cudaStream_t)stream);
 }
 
+// Per (device, dims) history of the sparse-pass input densities: the counts
+// of one call are copied (async, pinned) for the next call with the same grid,
+// which then decides its sparse passes without a host sync; the first call for
+// a grid syncs once per sparse-eligible pass.  A stale prediction (the scene
+// changed) costs speed only, never results, and is corrected by the next call.
+struct SparseHistory {
+    unsigned long long* counts = nullptr;  // pinned [32]: pass p's input: 0 unknown, else 1 + count
+    cudaEvent_t ready = nullptr;           // compute stream -> side stream
+    cudaEvent_t done = nullptr;            // counts landed
+    cudaStream_t side = nullptr;           // off-critical-path copy stream
+    bool valid = false;                    // a copy was published
+    unsigned long long last[32];           // the newest counts that have landed
+    bool have_last = false;
+};
+
+static SparseHistory* sparse_history(int nx, int ny, int nz) {
+    static std::mutex mu;
+    static std::map<std::tuple<int, int, int, int>, SparseHistory> hist;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lock(mu);
+    SparseHistory& h = hist[std::make_tuple(dev, nx, ny, nz)];
+    if (!h.counts) {
+        if (cudaMallocHost(&h.counts, 32 * sizeof(unsigned long long)) != cudaSuccess) {
+            h.counts = nullptr;
+            return nullptr;
+        }
+        for (int i = 0; i < 32; ++i) h.counts[i] = 0;
+        cudaEventCreateWithFlags(&h.ready, cudaEventDisableTiming);
+        cudaEventCreateWithFlags(&h.done, cudaEventDisableTiming);
+        cudaStreamCreateWithFlags(&h.side, cudaStreamNonBlocking);
+    }
+    return &h;
+}
+
+// Copy this call's per-pass counts to the pinned history on the side stream
+// (after the compute stream's counting kernels; off the critical path).
+static void publish_counts(SparseHistory* h, const unsigned long long* slots, cudaStream_t st) {
+    if (!h || !slots) return;
+    // the side stream's previous copy must finish before the pinned buffer is reused
+    if (h->valid && cudaEventQuery(h->done) != cudaSuccess) return;
+    cudaEventRecord(h->ready, st);
+    cudaStreamWaitEvent(h->side, h->ready, 0);
+    cudaMemcpyAsync(h->counts, slots, 32 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                    h->side);
+    cudaEventRecord(h->done, h->side);
+    h->valid = true;
+}
+
 // The full schedule (jfa.py:140-145) on one device: sparse kernel for the
 // passes with k >= sparse_min_k (and k % 32 == 0) while the workspace has room
 // for the bitmaps, the v2 pass kernel (INT mode) or the per-cell kernel
@@ -531,11 +593,23 @@ static int run_schedule(int32_t* a, int32_t* b, float* sdf_out, int nx, int ny, 
     if (nz > m) m = nz;
     int n = 1;
     while (n < m) n *= 2;  // jfa.py:58-68
+    // Sparse passes while the pass input is sparse (< 5 % of its 32-cell
+    // segments hold a seed): a sparse pass only pays off while few segments
+    // are active, since its active warps run the per-cell rule instead of the
+    // register-tiled pass (C3: 1.1 % for the first two inputs, then 11.7 %;
+    // C5: 14 % already before the second pass).  The bitmap kernels count the
+    // non-empty segments of each pass input; the first call for a grid reads
+    // them back at once (a small sync per eligible pass), later calls decide
+    // from the previous call's counts (SparseHistory) without a sync.
     static const int sparse_env = [] {
         const char* e = getenv("RTSDF_JFA_SPARSE_K");
         return e ? atoi(e) : -1;
     }();
-    const int sparse_min_k = sparse_env >= 0 ? (sparse_env == 0 ? 1 << 30 : sparse_env) : 128;
+    static const double sparse_frac = [] {
+        const char* e = getenv("RTSDF_JFA_SPARSE_FRAC");
+        return e ? atof(e) : 0.05;
+    }();
+    const int sparse_min_k = sparse_env >= 0 ? (sparse_env == 0 ? 1 << 30 : sparse_env) : 64;
     const bool bm_room = ws_bytes >= rtsdf_jfa_ws_bytes(nx, ny, nz);
     const int nzb = (nz + 31) / 32;
     const int64_t n_seg = (int64_t)nx * ny * nzb;
@@ -543,6 +617,30 @@ static int run_schedule(int32_t* a, int32_t* b, float* sdf_out, int nx, int ny, 
     if (bm_room) {
         bm[0] = (uint8_t*)ws + 256 + (size_t)nx * ny * nz * sizeof(int32_t);
         bm[1] = bm[0] + seg_bitmap_bytes(nx, ny, nz);
+    }
+    bool sparse_on = true;  // until the first dense input
+    SparseHistory* hist = bm_room ? sparse_history(nx, ny, nz) : nullptr;
+    unsigned long long pred[32];
+    bool predicted = false;
+    if (hist) {
+        // never wait for the previous call: use its counts if they have landed,
+        // else the ones before (one call staler)
+        if (hist->valid && cudaEventQuery(hist->done) == cudaSuccess) {
+            for (int i = 0; i < 32; ++i) hist->last[i] = hist->counts[i];
+            hist->have_last = true;
+        }
+        if (hist->have_last) {
+            for (int i = 0; i < 32; ++i) pred[i] = hist->last[i];
+            predicted = true;
+        }
+    }
+    const bool big = (int64_t)nx * ny * nz >= ((int64_t)1 << 28);
+    if (predicted && big) predicted = false;  // large grids: the sync is noise, measure every call
+    int pass = 0;
+    unsigned long long* slots = nullptr;  // per-pass input counts (1 + n), device
+    if (bm_room) {
+        slots = (unsigned long long*)(bm[1] + seg_bitmap_bytes(nx, ny, nz));
+        cudaMemsetAsync(slots, 0, 32 * sizeof(unsigned long long), st);
     }
     bool bm_valid = false;  // bm[0] describes src
     int32_t* src = a;
@@ -556,21 +654,39 @@ static int run_schedule(int32_t* a, int32_t* b, float* sdf_out, int nx, int ny, 
         PlaneSrc s{src, nullptr, nullptr};
         if (sdf_out && off == 1 && int_mode) {  // last pass writes the SDF directly
             launch_pass2<true, false>(s, nullptr, sdf_out, g, beta, empty_count, ws, st);
+            publish_counts(hist, slots, st);
             return check_launch("jfa_run_sdf");
         }
-        if (bm_room && off >= sparse_min_k && off % 32 == 0) {
-            if (!bm_valid) {
-                jfa_seg_bitmap_kernel<<<seg_blocks, 256, 0, st>>>(src, bm[0], ny, nz, dzb, (uint32_t)n_seg);
+        bool sparse = false;
+        if (bm_room && sparse_on && off >= sparse_min_k && off % 32 == 0 && pass < 32) {
+            const bool need_bm = !bm_valid;
+            if (predicted) {
+                const unsigned long long v = pred[pass];
+                sparse = v != 0 && (double)(v - 1) < sparse_frac * (double)n_seg;
+            }
+            if (need_bm && (sparse || !predicted)) {
+                jfa_seg_bitmap_kernel<<<seg_blocks, 256, 0, st>>>(src, bm[0], ny, nz, dzb,
+                                                                  (uint32_t)n_seg, slots + pass);
                 count_launch();
             }
-            // the bitmap of this pass's output is only needed by a next sparse pass
-            const bool next_sparse = off / 2 >= sparse_min_k && (off / 2) % 32 == 0;
+            if (!predicted) {  // first call for this grid (or a big grid): measure now
+                unsigned long long v = 0;
+                cudaMemcpyAsync(&v, slots + pass, sizeof(v), cudaMemcpyDeviceToHost, st);
+                cudaStreamSynchronize(st);
+                sparse = v != 0 && (double)(v - 1) < sparse_frac * (double)n_seg;
+            }
+            sparse_on = sparse;
+        }
+        if (sparse) {
+            // this pass's output bitmap (+ count) feeds the next pass's decision
+            const bool next_sparse = off / 2 >= sparse_min_k && (off / 2) % 32 == 0 && pass + 1 < 32;
+            unsigned long long* next_slot = next_sparse ? slots + pass + 1 : nullptr;
             if (int_mode)
                 jfa_sparse_kernel<JFA_INT><<<seg_blocks, 256, 0, st>>>(
-                    src, dst, g, bm[0], next_sparse ? bm[1] : nullptr, dzb, dny);
+                    src, dst, g, bm[0], next_sparse ? bm[1] : nullptr, dzb, dny, next_slot);
             else
                 jfa_sparse_kernel<JFA_FP64><<<seg_blocks, 256, 0, st>>>(
-                    src, dst, g, bm[0], next_sparse ? bm[1] : nullptr, dzb, dny);
+                    src, dst, g, bm[0], next_sparse ? bm[1] : nullptr, dzb, dny, next_slot);
             count_launch();
             uint8_t* t = bm[0];
             bm[0] = bm[1];
@@ -587,7 +703,9 @@ static int run_schedule(int32_t* a, int32_t* b, float* sdf_out, int nx, int ny, 
         src = dst;
         dst = t;
         w ^= 1;
+        ++pass;
     }
+    publish_counts(hist, slots, st);
     if (which) *which = w;
     if (sdf_out) return rtsdf_seeds_to_sdf(src, sdf_out, nx, ny, nz, hx, hy, hz, beta, empty_count, st);
     return RTSDF_OK;

@@ -9,8 +9,8 @@ import torch  # noqa: E402
 import paper_2210_06160_b200 as rt  # noqa: E402
 from paper_2210_06160_b200 import jfa as J  # noqa: E402
 
-dims = (400, 200, 400)
-scene = rt.get_scene("sphere_plane")
+dims = tuple(int(v) for v in (sys.argv[1] if len(sys.argv) > 1 else "400,200,400").split(","))
+scene = rt.get_scene(sys.argv[2] if len(sys.argv) > 2 else "sphere_plane")
 view = scene.view(0)
 h = (scene.hi - scene.lo) / np.array(dims, dtype=np.float64)
 w = J.integer_weights(*map(float, h), dims)
