@@ -8,12 +8,15 @@ taken from torch tensors (torch is only the allocator/stream provider).
 from __future__ import annotations
 
 import ctypes as C
+import os
 from pathlib import Path
 
 import numpy as np
 
 _PKG = Path(__file__).resolve().parent
 LIB_PATH = _PKG / "librtsdf.so"
+if os.environ.get("RTSDF_LIB"):  # experiments: an alternative build of the same ABI
+    LIB_PATH = Path(os.environ["RTSDF_LIB"])
 
 P = C.c_void_p
 I = C.c_int

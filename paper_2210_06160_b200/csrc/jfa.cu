@@ -387,6 +387,8 @@ static void launch_pass2(PlaneSrc s, int32_t* dst, float* dst_sdf, const JfaGeom
     // longer is cheaper (measured at C3: L = 24 is ~8 % faster than 8) as long
     // as the grid still fills the GPU for two waves (~16 resident warps / SM).
     Jfa2Task T;
+    T.one = 1;
+    T.zero = 0;
     T.nzb = (g.nz + 31) / 32;
     T.jres = k < g.ny ? k : g.ny;
     T.jgroups = (chain_y + ry - 1) / ry;
@@ -461,10 +463,11 @@ static bool weights_ok(int nx, int ny, int nz, int wx, int wy, int wz) {
     if (wx == 0 && wy == 0 && wz == 0) return true;
     if (wx <= 0 || wy <= 0 || wz <= 0) return false;
     if (wx > 16 || wy > 16 || wz > 16) return false;  // EMPTY-key bound in jfa2.cuh
-    // keys relative to |x|^2 span about 2 qmax plus the increments: keep 2 bits spare
+    // keys relative to |x|^2 span about 2 qmax plus the increments, and the
+    // non-EXACT pass doubles them (jfa2_eval's tie mark): keep 3 bits spare
     double qmax = (double)wx * (nx - 1) * (nx - 1) + (double)wy * (ny - 1) * (ny - 1) +
                   (double)wz * (nz - 1) * (nz - 1);
-    return qmax < 536870912.0;
+    return qmax < 268435456.0;
 }
 
 static bool ws_ok(void* ws, size_t ws_bytes, int64_t n_cells) {

@@ -16,39 +16,42 @@
 // computed once per value: every candidate costs one IADD plus a compare and
 // two selects.  The minimum integer key is the reference's fp64 minimum.  An
 // integer tie between two DIFFERENT seeds (a few % of cells in the late
-// passes) only sets a per-output flag; flagged cells are appended to a list
+// passes) only marks the output (odd running key, jfa2_eval); flagged cells are appended to a list
 // and re-decided by jfa_fixup_kernel with the reference's own rule
 // (fp64 d2, then lexicographic; jfa.py:108-124), so the hot loop has no fp64
 // and no divergent branch.
 #pragma once
 #include "common.cuh"
 
-#define JFA2_EMPTY_KEY (1 << 30)  // larger than any real key (|key| < 2^29)
+#define JFA2_EMPTY_KEY (1 << 30)  // larger than any real (doubled) key: |key| < 2^29
 
 namespace rtsdf {
 
 struct Jfa2Task {
     int nzb, jres, jgroups, ires, isegs, L;
+    int one, zero;  // = 1, 0 (opaque to ptxas, see jfa2_eval)
 };
 
-// One candidate against one output's running (Km, W): 3 predicate compares, a
-// min, a select and a predicated OR.  The tie flag lives in bit 30 of W
-// (packed seeds are < 2^30): it is set when a DIFFERENT seed equals the running
-// minimum and cleared by a strict improvement (W = v), so at the end it is set
-// iff >= 2 distinct seeds share the final minimum key.  A W carrying the bit
-// compares unequal to every seed, which only re-sets the bit.
-#define JFA2_TIEBIT (1 << 30)
-__device__ __forceinline__ void jfa2_eval(int K, int32_t v, int& Km, int32_t& W) {
+// One candidate against one output's running (Km, W).  Keys are even (the
+// non-EXACT pass doubles the weights); an integer tie between a DIFFERENT seed
+// and the running minimum marks Km odd by subtracting 1.  An odd Km = 2m - 1
+// orders exactly like 2m against every (even) key, so later equal keys are
+// neither smaller nor equal (already tied) and a strictly smaller key clears
+// the mark: at the end Km is odd iff >= 2 distinct seeds share the minimum.
+// 4 ALU ops (3 predicate compares, a min) + 2 predicated IMADs on the FMA pipe
+// (`one`/`zero` are opaque to ptxas, which would otherwise fold the moves
+// into ALU selects; the ALU pipe is the pass's bottleneck).
+__device__ __forceinline__ void jfa2_eval(int K, int32_t v, int& Km, int32_t& W, int one, int zero) {
     asm volatile(
-        "{\n\t.reg .pred plt, peq;\n\t"
+        "{\n\t.reg .pred plt, peq, pt;\n\t"
         "setp.lt.s32 plt, %2, %0;\n\t"
         "setp.eq.s32 peq, %2, %0;\n\t"
-        "setp.ne.and.s32 peq, %3, %1, peq;\n\t"
+        "setp.ne.and.s32 pt, %3, %1, peq;\n\t"
         "min.s32 %0, %0, %2;\n\t"
-        "selp.b32 %1, %3, %1, plt;\n\t"
-        "@peq or.b32 %1, %1, 0x40000000;\n\t}"
+        "@plt mad.lo.s32 %1, %1, %5, %3;\n\t"
+        "@pt mad.lo.s32 %0, %0, %4, -1;\n\t}"
         : "+r"(Km), "+r"(W)
-        : "r"(K), "r"(v));
+        : "r"(K), "r"(v), "r"(one), "r"(zero));
 }
 
 // EXACT mode (host-proven: every fp64 operation of center_d2 is exact for the
@@ -101,11 +104,15 @@ __global__ void __launch_bounds__(128) jfa_pass2_kernel(PlaneSrc src, int32_t* _
     const bool zok = z < g.nz;
     const int64_t plane = (int64_t)g.ny * g.nz;
     const int j_base = rj + gj * RY * k;  // row of output b = 0
-    const int cz = -2 * g.wz * z;
-    const int gxk = 2 * g.wx * k, gyk = 2 * g.wy * k;
+    // non-EXACT: doubled weights, so every real key is even (jfa2_eval's tie mark)
+    const int wsc = EXACT ? 1 : 2;
+    const int wx = wsc * g.wx, wy = wsc * g.wy, wz = wsc * g.wz;
+    const int one = T.one, zero = T.zero;
+    const int cz = -2 * wz * z;
+    const int gxk = 2 * wx * k, gyk = 2 * wy * k;
 
     int Km[3][RY];
-    int32_t W[3][RY];  // winner, tie flag in bit 30 (jfa2_eval)
+    int32_t W[3][RY];  // winner (non-EXACT: Km odd = integer tie, jfa2_eval)
 #pragma unroll
     for (int s = 0; s < 3; ++s)
 #pragma unroll
@@ -156,7 +163,7 @@ __global__ void __launch_bounds__(128) jfa_pass2_kernel(PlaneSrc src, int32_t* _
     for (int a = -1; a <= L; ++a) {
         if (a >= 1 && i_first + (a - 1) * k >= i_end) break;  // no further outputs (uniform)
         load_plane(a + 1, nxt);
-        const int cx = -2 * g.wx * (i_first + a * k);
+        const int cx = -2 * wx * (i_first + a * k);
         // Column-constant plane: every tap row holds the same seed in every lane
         // (seeds constant along y, e.g. above a floor).  A candidate's key
         // depends only on (seed, output), so the RY + 2 copies of a tap column
@@ -172,13 +179,13 @@ __global__ void __launch_bounds__(128) jfa_pass2_kernel(PlaneSrc src, int32_t* _
 #pragma unroll
             for (int c = 0; c < 3; ++c) ycon = ycon && cur[bt][c] == cur[0][c];
         if (k >= 64 && __all_sync(0xffffffffu, ycon)) {
-            const int cy = -2 * g.wy * (j_base - k);  // tap row bt = -1
+            const int cy = -2 * wy * (j_base - k);  // tap row bt = -1
 #pragma unroll
             for (int c = -1; c <= 1; ++c) {
                 const int32_t v = cur[0][c + 1];
                 if (__all_sync(0xffffffffu, v == RTSDF_EMPTY)) continue;
                 const int sx = unpack_i(v), sy = unpack_j(v), sk = unpack_k(v);
-                const int B0 = sx * (g.wx * sx + cx) + sy * (g.wy * sy + cy) + sk * (g.wz * sk + cz);
+                const int B0 = sx * (wx * sx + cx) + sy * (wy * sy + cy) + sk * (wz * sk + cz);
                 const int B = v != RTSDF_EMPTY ? B0 : JFA2_EMPTY_KEY;
                 const int Gx = gxk * sx, Gy = gyk * sy;
                 const int Bs[3] = {B + Gx, B, B - Gx};
@@ -191,20 +198,20 @@ __global__ void __launch_bounds__(128) jfa_pass2_kernel(PlaneSrc src, int32_t* _
                         if (EXACT)
                             jfa2_eval_exact(K, v, Km[s][b], W[s][b]);
                         else
-                            jfa2_eval(K, v, Km[s][b], W[s][b]);
+                            jfa2_eval(K, v, Km[s][b], W[s][b], one, zero);
                     }
                 }
             }
         } else
 #pragma unroll
         for (int bt = -1; bt <= RY; ++bt) {
-            const int cy = -2 * g.wy * (j_base + bt * k);
+            const int cy = -2 * wy * (j_base + bt * k);
 #pragma unroll
             for (int c = -1; c <= 1; ++c) {
                 const int32_t v = cur[bt + 1][c + 1];
                 if (__all_sync(0xffffffffu, v == RTSDF_EMPTY)) continue;  // warp-uniform skip
                 const int sx = unpack_i(v), sy = unpack_j(v), sk = unpack_k(v);
-                const int B0 = sx * (g.wx * sx + cx) + sy * (g.wy * sy + cy) + sk * (g.wz * sk + cz);
+                const int B0 = sx * (wx * sx + cx) + sy * (wy * sy + cy) + sk * (wz * sk + cz);
                 // EMPTY (-1) decodes to (4095, 1023, 1023): its increments stay bounded
                 // (|Gx|, |Gy| < 2^23), so an EMPTY base of 2^30 can never beat a real
                 // key (|key| < 2^29) -- no per-increment selects
@@ -222,7 +229,7 @@ __global__ void __launch_bounds__(128) jfa_pass2_kernel(PlaneSrc src, int32_t* _
                         if (EXACT)
                             jfa2_eval_exact(K, v, Km[s][b], W[s][b]);
                         else
-                            jfa2_eval(K, v, Km[s][b], W[s][b]);
+                            jfa2_eval(K, v, Km[s][b], W[s][b], one, zero);
                     }
                 }
             }
@@ -237,8 +244,8 @@ __global__ void __launch_bounds__(128) jfa_pass2_kernel(PlaneSrc src, int32_t* _
                 const bool live = zok && oj < g.ny;
                 const int64_t cell = (int64_t)(oi - g.x0) * plane + (int64_t)oj * g.nz + z;
                 const int32_t wt = W[0][b];
-                const bool tie = !EXACT && wt != RTSDF_EMPTY && (wt & JFA2_TIEBIT);
-                const int32_t w = EXACT || wt == RTSDF_EMPTY ? wt : (wt & ~JFA2_TIEBIT);
+                const bool tie = !EXACT && wt != RTSDF_EMPTY && (Km[0][b] & 1);
+                const int32_t w = wt;
                 if (live) {
                     if (FINAL) {
                         empties += w == RTSDF_EMPTY;

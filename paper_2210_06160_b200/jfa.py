@@ -100,7 +100,7 @@ def integer_weights(hx: float, hy: float, hz: float, dims: tuple) -> tuple:
     if max(w) > 16:  # csrc/jfa.cu weights_ok (EMPTY-key bound of the v2 pass)
         return (0, 0, 0)
     qmax = sum(wi * (n - 1) ** 2 for wi, n in zip(w, dims))
-    if qmax >= 2**29:  # csrc/jfa.cu weights_ok: relative keys need 2 spare bits
+    if qmax >= 2**28:  # csrc/jfa.cu weights_ok: doubled relative keys need 3 spare bits
         return (0, 0, 0)
     return tuple(w)
 
