@@ -296,8 +296,11 @@ __global__ void __launch_bounds__(128) jfa_pass2_kernel(PlaneSrc src, int32_t* _
 // pre-filters them: a strictly larger integer key is a strictly larger exact
 // d2, which fp64 rounding cannot invert (relative gap >= 2^-29), so the fp64
 // argmin lies among the taps at the minimum integer key -- only those pay fp64.
+#ifndef JFA_FIX_MINB
+#define JFA_FIX_MINB 8  // latency bound: occupancy over registers (64 regs, measured best)
+#endif
 template <bool FINAL, bool SLAB>
-__global__ void __launch_bounds__(128) jfa_fixup_kernel(PlaneSrc src, int32_t* __restrict__ dst,
+__global__ void __launch_bounds__(128, JFA_FIX_MINB) jfa_fixup_kernel(PlaneSrc src, int32_t* __restrict__ dst,
                                                         float* __restrict__ dst_sdf, JfaGeom g,
                                                         double beta, JfaFixList fix, FastDiv dnz,
                                                         FastDiv dny) {
@@ -335,19 +338,20 @@ __global__ void __launch_bounds__(128) jfa_fixup_kernel(PlaneSrc src, int32_t* _
                     const int off = (j + (dj - 1) * k) * g.nz + z + (dk - 1) * k;
                     c[(di * 3 + dj) * 3 + dk] = ok ? __ldg(pl[di] + off) : RTSDF_EMPTY;
                 }
-        int key[27];
+        // integer keys recomputed in the second loop (no key[27] array:
+        // registers, not ALU, limit this latency-bound kernel)
+        auto ikey = [&](int32_t v) {
+            const int dx = i - unpack_i(v), dy = j - unpack_j(v), dz = z - unpack_k(v);
+            return v == RTSDF_EMPTY ? 0x7fffffff : g.wx * dx * dx + g.wy * dy * dy + g.wz * dz * dz;
+        };
         int km = 0x7fffffff;
 #pragma unroll
-        for (int t = 0; t < 27; ++t) {
-            const int dx = i - unpack_i(c[t]), dy = j - unpack_j(c[t]), dz = z - unpack_k(c[t]);
-            key[t] = c[t] == RTSDF_EMPTY ? 0x7fffffff : g.wx * dx * dx + g.wy * dy * dy + g.wz * dz * dz;
-            km = min(km, key[t]);
-        }
+        for (int t = 0; t < 27; ++t) km = min(km, ikey(c[t]));
         int32_t best = RTSDF_EMPTY;
         double bd = 1e300;
 #pragma unroll
         for (int t = 0; t < 27; ++t) {
-            if (key[t] != km || c[t] == RTSDF_EMPTY || c[t] == best) continue;
+            if (c[t] == RTSDF_EMPTY || c[t] == best || ikey(c[t]) != km) continue;
             const double d2 = center_d2(i - unpack_i(c[t]), j - unpack_j(c[t]), z - unpack_k(c[t]),
                                         g.hx, g.hy, g.hz);
             if (d2 < bd || (d2 == bd && best != RTSDF_EMPTY && c[t] < best)) {

@@ -20,7 +20,9 @@
 
 #include "common.cuh"
 
+#ifndef RTSDF_FAST_STACK
 #define RTSDF_FAST_STACK 40  // the host rejects search trees deeper than this
+#endif
 
 namespace rtsdf {
 
