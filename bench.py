@@ -113,14 +113,18 @@ def peaks():
 
 def jfa_traffic():
     """DRAM bytes (read + write) per dense JFA pass launch from the committed
-    ncu --set full capture (profiles/r1h_frame_kernels_summary.csv), or None."""
-    p = ROOT / "profiles" / "r1h_frame_kernels_summary.csv"
+    ncu --set full capture (profiles/r1k_frame_kernels_summary.csv), or None."""
+    p = ROOT / "profiles" / "r1k_frame_kernels_summary.csv"
     if not p.exists():
         return None, None
-    rows = [ln.split(",") for ln in p.read_text().splitlines()[1:] if ln.startswith("jfa_pass2_kernel<4")]
+    import csv
+
+    rows = list(csv.reader(p.read_text().splitlines()))
+    head, rows = rows[0], [r for r in rows[1:] if r[0].startswith("jfa_pass2_kernel<4")]
     if not rows:
         return None, None
-    mb = [float(r[-5]) + float(r[-4]) for r in rows]  # dram_rd, dram_wr [MB] (name has commas)
+    rd, wr = head.index("dram_rd[MB]"), head.index("dram_wr[MB]")
+    mb = [float(r[rd]) + float(r[wr]) for r in rows]
     return round(sum(mb) / len(mb) * 1e6), f"profiles/{p.name} (mean of {len(mb)} RY=4 pass launches, k = 64..1)"
 
 

@@ -182,8 +182,10 @@ __global__ void __launch_bounds__(RS_THREADS) compact_kernel(const uint8_t* __re
                                                             const int64_t* __restrict__ offsets,
                                                             int64_t* __restrict__ idx) {
     __shared__ int warp_tot[RS_THREADS / 32];
+    __shared__ uint16_t pos[RS_CELLS_PER_BLOCK];  // block-local offsets of the masked cells
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    const int64_t base = (int64_t)blockIdx.x * RS_CELLS_PER_BLOCK + (int64_t)threadIdx.x * RS_PER_THREAD;
+    const int64_t bbase = (int64_t)blockIdx.x * RS_CELLS_PER_BLOCK;
+    const int64_t base = bbase + (int64_t)threadIdx.x * RS_PER_THREAD;
     const uint8_t* m = mask + c0 + base;
     uint32_t bits = 0;
     if (base + RS_PER_THREAD <= n && ((uintptr_t)m & 15) == 0) {
@@ -204,15 +206,25 @@ __global__ void __launch_bounds__(RS_THREADS) compact_kernel(const uint8_t* __re
     }
     if (lane == 31) warp_tot[wid] = incl;
     __syncthreads();
-    int before = 0;
+    int before = 0, total = 0;
 #pragma unroll
-    for (int w = 0; w < RS_THREADS / 32; ++w) before += w < wid ? warp_tot[w] : 0;
-    int64_t out = offsets[blockIdx.x] + before + incl - cnt;
+    for (int w = 0; w < RS_THREADS / 32; ++w) {
+        before += w < wid ? warp_tot[w] : 0;
+        total += warp_tot[w];
+    }
+    // stage the ascending block-local offsets, then write the int64 indices
+    // coalesced (one thread's run of up to 16 indices would otherwise be a
+    // strided store per lane)
+    int out = before + incl - cnt;
     while (bits) {
         const int r = __ffs(bits) - 1;
-        idx[out++] = c0 + base + r;
+        pos[out++] = (uint16_t)(threadIdx.x * RS_PER_THREAD + r);
         bits &= bits - 1;
     }
+    __syncthreads();
+    int64_t* dst = idx + offsets[blockIdx.x];
+    const int64_t first = c0 + bbase;
+    for (int p = threadIdx.x; p < total; p += RS_THREADS) dst[p] = first + pos[p];
 }
 
 }  // namespace rtsdf
