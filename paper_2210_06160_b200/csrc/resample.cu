@@ -126,6 +126,106 @@ __global__ void __launch_bounds__(RS_THREADS) resample_mask_kernel(
     }
 }
 
+// Same partition and arithmetic as resample_mask_kernel, for grids whose z
+// extent is a multiple of 4: a thread owns 4 groups of 4 consecutive cells of
+// one row, so the cell decode, the x / y weights and the four corner-row
+// offsets are computed once per group, and c_fine / mask_new / mask_old move
+// as 16 / 4-byte vectors.
+__global__ void __launch_bounds__(RS_THREADS) resample_mask4_kernel(
+    RsParams P, float* __restrict__ c_fine, float* __restrict__ out_unmasked,
+    uint8_t* __restrict__ mask_new, int32_t* __restrict__ block_counts,
+    const uint8_t* __restrict__ mask_old, float* __restrict__ run_min,
+    int32_t* __restrict__ front, int32_t* __restrict__ back) {
+    __shared__ int warp_sum[RS_THREADS / 32];
+    __shared__ double tf[3][RS_TAB];
+    __shared__ int ti[3][RS_TAB];
+    const int64_t base = P.c0 + (int64_t)blockIdx.x * RS_CELLS_PER_BLOCK;
+    const int64_t last = min(base + RS_CELLS_PER_BLOCK, P.c0 + P.n_cells) - 1;
+    int i0, j0, k0, i1, j1, k1;
+    cell_ijk(P, (uint32_t)base, i0, j0, k0);
+    cell_ijk(P, (uint32_t)last, i1, j1, k1);
+    const int xs = i0, xn = i1 - i0 + 1;
+    const int ys = i0 == i1 ? j0 : 0, yn = i0 == i1 ? j1 - j0 + 1 : P.fny;
+    const int zs = (i0 == i1 && j0 == j1) ? k0 : 0, zn = (i0 == i1 && j0 == j1) ? k1 - k0 + 1 : P.fnz;
+    const FieldView& f = P.coarse;
+    for (int t = threadIdx.x; t < xn + yn + zn; t += RS_THREADS) {  // host: xn <= RS_TAB
+        AxisW w;
+        int ax, e;
+        if (t < xn) {
+            ax = 0, e = t;
+            w = fine_axis(f.lox, P.fhx, f.hx, f.nx, xs + e);
+        } else if (t < xn + yn) {
+            ax = 1, e = t - xn;
+            w = fine_axis(f.loy, P.fhy, f.hy, f.ny, ys + e);
+        } else {
+            ax = 2, e = t - xn - yn;
+            w = fine_axis(f.loz, P.fhz, f.hz, f.nz, zs + e);
+        }
+        tf[ax][e] = w.f;
+        ti[ax][e] = w.i;
+    }
+    __syncthreads();
+    const int64_t sx = (int64_t)f.ny * f.nz, sy = f.nz;
+    const int dj = f.nx > 1 ? 1 : 0, djy = f.ny > 1 ? 1 : 0, djz = f.nz > 1 ? 1 : 0;
+    int cnt = 0;
+#pragma unroll 1
+    for (int g = 0; g < RS_PER_THREAD / 4; ++g) {
+        const int64_t c = base + ((int64_t)g * RS_THREADS + threadIdx.x) * 4;
+        if (c > last) break;
+        int i, j, k;
+        cell_ijk(P, (uint32_t)c, i, j, k);
+        const int xi = ti[0][i - xs], yi = ti[1][j - ys];
+        const double fx = tf[0][i - xs], fy = tf[1][j - ys];
+        const double ofx = __dsub_rn(1.0, fx), ofy = __dsub_rn(1.0, fy);
+        const float* r00 = f.data + xi * sx + yi * sy;           // (x.i, y.i)
+        const float* r10 = f.data + (xi + dj) * sx + yi * sy;    // (x.j, y.i)
+        const float* r01 = f.data + xi * sx + (yi + djy) * sy;   // (x.i, y.j)
+        const float* r11 = f.data + (xi + dj) * sx + (yi + djy) * sy;
+        float4 vo;
+        uint32_t mpack = 0;
+        const uint32_t mold = mask_old ? *(const uint32_t*)(mask_old + c) : 0u;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            const int zi = ti[2][k + e - zs], zj = zi + djz;
+            const double fz = tf[2][k + e - zs], ofz = __dsub_rn(1.0, fz);
+            // trilinear_w's arithmetic, term for term (field.py:95-128)
+            const double c000 = __ldg(r00 + zi), c100 = __ldg(r10 + zi), c010 = __ldg(r01 + zi),
+                         c110 = __ldg(r11 + zi), c001 = __ldg(r00 + zj), c101 = __ldg(r10 + zj),
+                         c011 = __ldg(r01 + zj), c111 = __ldg(r11 + zj);
+            const double c00 = __dadd_rn(__dmul_rn(c000, ofx), __dmul_rn(c100, fx));
+            const double c10 = __dadd_rn(__dmul_rn(c010, ofx), __dmul_rn(c110, fx));
+            const double c01 = __dadd_rn(__dmul_rn(c001, ofx), __dmul_rn(c101, fx));
+            const double c11 = __dadd_rn(__dmul_rn(c011, ofx), __dmul_rn(c111, fx));
+            const double c0 = __dadd_rn(__dmul_rn(c00, ofy), __dmul_rn(c10, fy));
+            const double c1 = __dadd_rn(__dmul_rn(c01, ofy), __dmul_rn(c11, fy));
+            const double v = __dadd_rn(__dmul_rn(c0, ofz), __dmul_rn(c1, fz));
+            const bool m = v <= P.d;  // compared in fp64 (raysample.py:105)
+            const float vf = (float)v;
+            (&vo.x)[e] = vf;
+            mpack |= (m ? 1u : 0u) << (8 * e);
+            if (out_unmasked && !m) out_unmasked[c + e] = vf;
+            if (!m && ((mold >> (8 * e)) & 0xffu)) {  // left the band: stale state resets
+                run_min[c + e] = __int_as_float(0x7f800000);
+                front[c + e] = 0;
+                back[c + e] = 0;
+            }
+            cnt += m;
+        }
+        if (c_fine) *(float4*)(c_fine + c) = vo;
+        if (mask_new) *(uint32_t*)(mask_new + c) = mpack;
+    }
+    if (block_counts) {
+        for (int o = 16; o; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+        if ((threadIdx.x & 31) == 0) warp_sum[threadIdx.x >> 5] = cnt;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            int s = 0;
+            for (int w = 0; w < RS_THREADS / 32; ++w) s += warp_sum[w];
+            block_counts[blockIdx.x] = s;
+        }
+    }
+}
+
 __global__ void __launch_bounds__(RS_THREADS) count_mask_kernel(const uint8_t* __restrict__ mask,
                                                                int64_t c0, int64_t n,
                                                                int32_t* __restrict__ block_counts) {
@@ -271,8 +371,18 @@ extern "C" int rtsdf_resample_mask_range(const float* coarse, int cnx, int cny, 
     P.div_ny = make_fastdiv((uint32_t)fny);
     P.div_nz = make_fastdiv((uint32_t)fnz);
     int64_t nb = rtsdf_mask_blocks(n_range);
-    resample_mask_kernel<<<(unsigned)nb, RS_THREADS, 0, (cudaStream_t)stream>>>(
-        P, c_fine, out_unmasked, mask_new, block_counts, mask_old, run_min, front, back);
+    // vector form: rows split into whole 4-cell groups, 16 / 4-byte aligned
+    // buffers, weight tables for every block (fine planes per block <= RS_TAB)
+    auto al = [](const void* q, uintptr_t a) { return ((uintptr_t)q & (a - 1)) == 0; };
+    const bool vec = fnz % 4 == 0 && c0 % 4 == 0 && n_range % 4 == 0 &&
+                     (int64_t)fny * fnz >= RS_CELLS_PER_BLOCK / RS_TAB + 1 && al(c_fine, 16) &&
+                     al(mask_new, 4) && al(mask_old, 4) && getenv("RTSDF_RS_SCALAR") == nullptr;
+    if (vec)
+        resample_mask4_kernel<<<(unsigned)nb, RS_THREADS, 0, (cudaStream_t)stream>>>(
+            P, c_fine, out_unmasked, mask_new, block_counts, mask_old, run_min, front, back);
+    else
+        resample_mask_kernel<<<(unsigned)nb, RS_THREADS, 0, (cudaStream_t)stream>>>(
+            P, c_fine, out_unmasked, mask_new, block_counts, mask_old, run_min, front, back);
     count_launch();
     return check_launch("resample_mask");
 }
