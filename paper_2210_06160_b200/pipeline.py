@@ -162,6 +162,12 @@ class FramePipeline:
         return apply_bias(self.coarse, self.cfg.bias)
 
     # --------------------------------------------------------------- frame
+    def _side_stream(self):
+        st = getattr(self, "_side", None)
+        if st is None or st.device != torch.cuda.current_stream().device:
+            st = self._side = torch.cuda.Stream()
+        return st
+
     def advance(self, render=False, camera=None, timing=True) -> FrameRecord:
         """Run one frame of V -> JF -> RT (-> DL when render=True)."""
         cfg = self.cfg
@@ -173,6 +179,20 @@ class FramePipeline:
         if timing:
             events = [torch.cuda.Event(enable_timing=True) for _ in range(len(PASSES) + 1)]
             events[0].record()
+
+        # DL's G-buffer depends only on mesh + camera: it runs on a side stream
+        # while V / JF / RT occupy the main one (joined before the march)
+        gb_done = None
+        if render:
+            cam = camera or self.scene.camera
+            dl = self._dl_buffers(cam)
+            main = torch.cuda.current_stream()
+            side = self._side_stream()
+            side.wait_stream(main)  # the previous frame's march has read dl["gb"]
+            with torch.cuda.stream(side):
+                _render.launch_gbuffer(view, cam, dl["gb"], dl["cam"])
+                gb_done = torch.cuda.Event()
+                gb_done.record(side)
 
         # V: packed self-seeds straight from the triangles (K1)
         first = self._checked_view is not view
@@ -226,9 +246,7 @@ class FramePipeline:
         if render:
             # DL: G-buffer (K6 traversal) -> soft-shadow march (K8, fine_for_shading's
             # bias fused into the samples) -> compose; buffers persist per camera
-            cam = camera or self.scene.camera
-            dl = self._dl_buffers(cam)
-            _render.launch_gbuffer(view, cam, dl["gb"], dl["cam"])
+            torch.cuda.current_stream().wait_event(gb_done)
             light = self.scene.light.unit()
             _render.launch_occlusion(dl["gb"], self.fine, light, self.march_params(),
                                      cfg.shade_draws, cfg.sampling.seed, dl["occ"],
