@@ -283,6 +283,131 @@ __global__ void __launch_bounds__(256) jfa_sparse_kernel(const int32_t* __restri
     if (n_on && blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(n_on, 1ull);  // "measured" (+1)
 }
 
+// Two-phase sparse pass.  Phase 1, one THREAD per output segment: the 27 tap
+// segment bits (k a multiple of 32: whole segments) are OR-ed; a segment no
+// seed can reach is filled with EMPTY right away (vector stores, no tap loads)
+// and its output bit cleared, the others are appended to an active list.
+// Phase 2, one warp per active segment: jfa_sparse_kernel's per-cell rule.
+// The thread-per-segment test costs ~100 thread instructions per segment
+// where the warp-per-segment form spent ~90 warp instructions.
+__global__ void __launch_bounds__(256) jfa_sparse_fill_kernel(int32_t* __restrict__ dst, JfaGeom g,
+                                                              const uint8_t* __restrict__ bm_in,
+                                                              uint8_t* __restrict__ bm_out,
+                                                              FastDiv dzb, FastDiv dny,
+                                                              int32_t* __restrict__ active,
+                                                              unsigned long long* __restrict__ n_active,
+                                                              unsigned long long* __restrict__ n_on) {
+    const int nzb = (int)dzb.d;
+    const uint32_t n_seg = (uint32_t)g.nx * g.ny * nzb;
+    const int off = g.offset, kz = off >> 5;
+    const int lane = threadIdx.x & 31;
+    const uint32_t stride = gridDim.x * blockDim.x;
+    for (uint32_t seg0 = blockIdx.x * blockDim.x + (threadIdx.x & ~31u); seg0 < n_seg; seg0 += stride) {
+        const uint32_t seg = seg0 + lane;
+        bool any = false;
+        if (seg < n_seg) {
+            const uint32_t row = fdiv(seg, dzb);
+            const int zb = (int)(seg - row * dzb.d);
+            const int i = (int)fdiv(row, dny), j = (int)(row - (uint32_t)i * dny.d);
+#pragma unroll
+            for (int di = -1; di <= 1; ++di) {
+                const int qi = i + di * off;
+#pragma unroll
+                for (int dj = -1; dj <= 1; ++dj) {
+                    const int qj = j + dj * off;
+                    if (qi < 0 || qi >= g.nx || qj < 0 || qj >= g.ny) continue;
+                    const uint8_t* r = bm_in + ((int64_t)qi * g.ny + qj) * nzb;
+#pragma unroll
+                    for (int dk = -1; dk <= 1; ++dk) {
+                        const int qz = zb + dk * kz;
+                        if (qz >= 0 && qz < nzb) any |= __ldg(r + qz) != 0;
+                    }
+                }
+            }
+            if (!any) {
+                const int z0 = zb * 32, len = min(32, g.nz - z0);
+                int32_t* d = dst + (int64_t)row * g.nz + z0;
+                if ((((uintptr_t)d) & 15) == 0 && (len & 3) == 0) {
+                    const int4 e = make_int4(RTSDF_EMPTY, RTSDF_EMPTY, RTSDF_EMPTY, RTSDF_EMPTY);
+                    for (int q = 0; q < len; q += 4) *(int4*)(d + q) = e;
+                } else {
+                    for (int q = 0; q < len; ++q) d[q] = RTSDF_EMPTY;
+                }
+                if (bm_out) bm_out[seg] = 0;
+            }
+        }
+        const unsigned m = __ballot_sync(0xffffffffu, any);
+        if (m) {
+            unsigned long long base = 0;
+            if (lane == __ffs(m) - 1) base = atomicAdd(n_active, (unsigned long long)__popc(m));
+            base = __shfl_sync(0xffffffffu, base, __ffs(m) - 1);
+            if (any) active[base + __popc(m & ((1u << lane) - 1))] = (int32_t)seg;
+        }
+    }
+    if (n_on && blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(n_on, 1ull);  // "measured" (+1)
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(256) jfa_sparse_active_kernel(const int32_t* __restrict__ src,
+                                                                int32_t* __restrict__ dst, JfaGeom g,
+                                                                uint8_t* __restrict__ bm_out,
+                                                                FastDiv dzb, FastDiv dny,
+                                                                const int32_t* __restrict__ active,
+                                                                const unsigned long long* __restrict__ n_active,
+                                                                unsigned long long* __restrict__ n_on) {
+    unsigned on_count = 0;
+    const int lane = threadIdx.x & 31;
+    const int off = g.offset;
+    const int64_t plane = (int64_t)g.ny * g.nz;
+    const unsigned long long na = *n_active;
+    const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+    for (uint32_t a = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; a < na; a += nwarps) {
+        const uint32_t seg = (uint32_t)active[a];
+        const uint32_t row = fdiv(seg, dzb);
+        const int zb = (int)(seg - row * dzb.d);
+        const int i = (int)fdiv(row, dny), j = (int)(row - (uint32_t)i * dny.d);
+        const int k = zb * 32 + lane;
+        const int64_t cell = (int64_t)i * plane + (int64_t)j * g.nz + k;
+        int32_t out = RTSDF_EMPTY;
+        if (k < g.nz) {
+            Best<MODE> b;
+            b.p = __ldg(src + cell);
+            if (b.p != RTSDF_EMPTY) {
+                int dx = i - unpack_i(b.p), dy = j - unpack_j(b.p), dz = k - unpack_k(b.p);
+                if (MODE == JFA_INT) b.q = g.wx * dx * dx + g.wy * dy * dy + g.wz * dz * dz;
+                else b.d2 = center_d2(dx, dy, dz, g.hx, g.hy, g.hz);
+            } else {
+                b.q = 0x7fffffff;
+                b.d2 = 1e300;
+            }
+#pragma unroll
+            for (int di = -1; di <= 1; ++di) {
+                const int qi = i + di * off;
+                if (qi < 0 || qi >= g.nx) continue;
+#pragma unroll
+                for (int dj = -1; dj <= 1; ++dj) {
+                    const int qj = j + dj * off;
+                    if (qj < 0 || qj >= g.ny) continue;
+                    const int32_t* rw = src + (int64_t)qi * plane + (int64_t)qj * g.nz;
+#pragma unroll
+                    for (int dk = -1; dk <= 1; ++dk) {
+                        if (di == 0 && dj == 0 && dk == 0) continue;
+                        const int qk = k + dk * off;
+                        if (qk < 0 || qk >= g.nz) continue;
+                        consider<MODE>(b, __ldg(rw + qk), i, j, k, g);
+                    }
+                }
+            }
+            out = b.p;
+            dst[cell] = out;
+        }
+        const unsigned m = __ballot_sync(0xffffffffu, out != RTSDF_EMPTY);
+        if (bm_out && lane == 0) bm_out[seg] = m != 0;
+        on_count += m != 0;
+    }
+    if (n_on && lane == 0 && on_count) atomicAdd(n_on, (unsigned long long)on_count);
+}
+
 __global__ void jfa_init_kernel(const uint8_t* __restrict__ occ, int ny, int nz, int64_t n,
                                 int32_t* __restrict__ seed, int64_t* __restrict__ count) {
     int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -684,13 +809,31 @@ static int run_schedule(int32_t* a, int32_t* b, float* sdf_out, int nx, int ny, 
             // this pass's output bitmap (+ count) feeds the next pass's decision
             const bool next_sparse = off / 2 >= sparse_min_k && (off / 2) % 32 == 0 && pass + 1 < 32;
             unsigned long long* next_slot = next_sparse ? slots + pass + 1 : nullptr;
-            if (int_mode)
-                jfa_sparse_kernel<JFA_INT><<<seg_blocks, 256, 0, st>>>(
-                    src, dst, g, bm[0], next_sparse ? bm[1] : nullptr, dzb, dny, next_slot);
-            else
-                jfa_sparse_kernel<JFA_FP64><<<seg_blocks, 256, 0, st>>>(
-                    src, dst, g, bm[0], next_sparse ? bm[1] : nullptr, dzb, dny, next_slot);
-            count_launch();
+            static const bool one_phase = getenv("RTSDF_JFA_SPARSE1") != nullptr;
+            if (one_phase) {
+                if (int_mode)
+                    jfa_sparse_kernel<JFA_INT><<<seg_blocks, 256, 0, st>>>(
+                        src, dst, g, bm[0], next_sparse ? bm[1] : nullptr, dzb, dny, next_slot);
+                else
+                    jfa_sparse_kernel<JFA_FP64><<<seg_blocks, 256, 0, st>>>(
+                        src, dst, g, bm[0], next_sparse ? bm[1] : nullptr, dzb, dny, next_slot);
+                count_launch();
+            } else {
+                // active list in the (not yet used) fix-up list area, its count in slot 0
+                unsigned long long* n_active = (unsigned long long*)ws;
+                int32_t* active = (int32_t*)((char*)ws + 256);
+                cudaMemsetAsync(n_active, 0, sizeof(unsigned long long), st);
+                const unsigned fill_blocks = (unsigned)((n_seg + 255) / 256);
+                jfa_sparse_fill_kernel<<<fill_blocks, 256, 0, st>>>(
+                    dst, g, bm[0], next_sparse ? bm[1] : nullptr, dzb, dny, active, n_active, next_slot);
+                if (int_mode)
+                    jfa_sparse_active_kernel<JFA_INT><<<seg_blocks, 256, 0, st>>>(
+                        src, dst, g, next_sparse ? bm[1] : nullptr, dzb, dny, active, n_active, next_slot);
+                else
+                    jfa_sparse_active_kernel<JFA_FP64><<<seg_blocks, 256, 0, st>>>(
+                        src, dst, g, next_sparse ? bm[1] : nullptr, dzb, dny, active, n_active, next_slot);
+                count_launch(2);
+            }
             uint8_t* t = bm[0];
             bm[0] = bm[1];
             bm[1] = t;
