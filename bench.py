@@ -128,6 +128,27 @@ def jfa_traffic():
     return round(sum(mb) / len(mb) * 1e6), f"profiles/{p.name} (mean of {len(mb)} RY=4 pass launches, k = 64..1)"
 
 
+def issue_roofline(n_cells, pass_ms, ck):
+    """The JFA pass's binding roofline: instruction issue.  Thread-instructions
+    per cell of the dense pass from the committed ncu capture
+    (profiles/r1k_jfa_pass_k4_opmix.txt); peak = 148 SMs x 4 schedulers x 1
+    warp-instruction / clock x 32 lanes at the measured SM clock."""
+    p = ROOT / "profiles" / "r1k_jfa_pass_k4_opmix.txt"
+    ipc = None
+    if p.exists():
+        for ln in p.read_text().splitlines():
+            if "thread-instructions per cell" in ln:
+                ipc = float(ln.split("=")[1].split()[0])
+    if not ipc:
+        return None
+    mhz = (ck or {}).get("sm_mhz") or 1965.0
+    peak = 148 * 4 * mhz * 1e6 * 32 / ipc / 1e9  # Gvox-pass/s at 100 % issue
+    got = n_cells / (pass_ms * 1e-3) / 1e9
+    return {"instr_per_cell": ipc, "peak_gvox_pass_per_s": round(peak, 1),
+            "achieved_gvox_pass_per_s": round(got, 1), "frac": round(got / peak, 4),
+            "source": f"profiles/{p.name}"}
+
+
 # ------------------------------------------------------------------ our arm
 def run_ours(args, rank, world, local_rank):
     import torch
@@ -329,8 +350,10 @@ def run_ours(args, rank, world, local_rank):
                      "traffic_source": traffic_src,
                      "algorithmic_bytes_per_launch": n_cells * 8, "peak_source": hbm_src,
                      "dominant_kernel": dominant,
-                     "note": "sample_update (ray traversal) is issue/latency bound, not HBM or tensor "
-                             "bound; see rays_per_s"},
+                     "issue_roofline": issue_roofline(n_cells, pass_ms, ck),
+                     "note": "the JFA pass is instruction-issue bound (27 exact candidates per cell, "
+                             "see issue_roofline and DESIGN.md section 7); sample_update (ray "
+                             "traversal) is issue/latency bound; see rays_per_s"},
         "kernels_ms": {k: round(v, 4) for k, v in kernels_ms.items()},
         "e2e": e2e, "gpu_launches": int(launches), "clocks": ck,
     }
