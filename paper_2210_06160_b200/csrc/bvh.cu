@@ -289,7 +289,9 @@ __global__ void bvh_pack_fast_kernel(const double* __restrict__ node_lo,
             s += fabs(tri_e1[3 * q + a]) + fabs(tri_e2[3 * q + a]);
         }
         t.scale = __double2float_ru(s * 1.0000001);
-        t.pad_[0] = t.pad_[1] = 0.0f;
+        const double am = fabs(tri_a[3 * q]) + fabs(tri_a[3 * q + 1]) + fabs(tri_a[3 * q + 2]);
+        t.amag = __double2float_ru(am * 1.0000001);
+        t.pad_ = 0.0f;
         ftris[q] = t;
     }
 }

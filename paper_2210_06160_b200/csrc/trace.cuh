@@ -50,7 +50,8 @@ struct __align__(16) FastTri {
     float e1[3];
     float e2[3];
     float scale;  // |e1|_1 + |e2|_1 rounded up (rounding bound)
-    float pad_[2];
+    float amag;   // |a|_1 rounded up (tri_maybe's fp32-vertex error term)
+    float pad_;
 };
 static_assert(sizeof(FastTri) == 48, "fast tri layout");
 
@@ -123,8 +124,14 @@ __device__ __forceinline__ float box_entry(float lx, float ly, float lz, float h
 // fp32 Moller-Trumbore on un-normalised values with an a-priori error bound
 // eb >= |fp32 - exact| of det, U, V, W (inputs rounded to fp32, ~10 roundings,
 // padded ~4x).  Returns false only when the exact test must reject.
+// cm > 0: T was formed in fp32 from fp32-rounded origin and vertex (o_f - a_f)
+// instead of rounding the fp64 difference; each component then carries an
+// extra absolute error <= 2^-24 (|o_c| + |a_c|), i.e. |dT|_1 <= 2^-24 cm with
+// cm = |o|_1 + |a|_1, which moves U and V by <= |dT|_1 scale and W by
+// <= |dT|_1 scale^2 -- added to eb with a 4x margin.
 __device__ __forceinline__ bool tri_maybe(const FastTri& tr, float tx, float ty, float tz,
-                                          float dx, float dy, float dz, float t_best) {
+                                          float dx, float dy, float dz, float t_best,
+                                          float cm = 0.0f) {
     float px = __fsub_rn(__fmul_rn(dy, tr.e2[2]), __fmul_rn(dz, tr.e2[1]));
     float py = __fsub_rn(__fmul_rn(dz, tr.e2[0]), __fmul_rn(dx, tr.e2[2]));
     float pz = __fsub_rn(__fmul_rn(dx, tr.e2[1]), __fmul_rn(dy, tr.e2[0]));
@@ -136,7 +143,8 @@ __device__ __forceinline__ bool tri_maybe(const FastTri& tr, float tx, float ty,
     float V = fmaf(dx, qx, fmaf(dy, qy, __fmul_rn(dz, qz)));
     float W = fmaf(tr.e2[0], qx, fmaf(tr.e2[1], qy, __fmul_rn(tr.e2[2], qz)));
     float tn = fabsf(tx) + fabsf(ty) + fabsf(tz);
-    float eb = 4e-6f * (tn + 1.0f) * tr.scale * (tr.scale + 1.0f);
+    float eb = 4e-6f * (tn + 1.0f) * tr.scale * (tr.scale + 1.0f) +
+               2.4e-7f * cm * tr.scale * fmaxf(1.0f, tr.scale);
     float ad = fabsf(det);
     if (!(ad > 4.0f * eb)) return true;  // ill-conditioned, tiny or NaN: exact test decides
     float s = det > 0.0f ? 1.0f : -1.0f;
@@ -284,10 +292,14 @@ __device__ __forceinline__ bool leaf_tris(const FastTri* __restrict__ tris, cons
         tr.e2[0] = f1.z; tr.e2[1] = f1.w; tr.e2[2] = f2.x;
         tr.scale = f2.y;
         const BvhTri* ex = exact + k;
-        float tx = (float)(ox - __ldg(ex->a)), ty = (float)(oy - __ldg(ex->a + 1)),
-              tz = (float)(oz - __ldg(ex->a + 2));
+        // T from the fp32 origin and vertex: the fp64 triangle record is only
+        // touched by the exact confirmation (the pre-test's error bound covers
+        // the two extra roundings, see tri_maybe)
+        const float fox = (float)ox, foy = (float)oy, foz = (float)oz;
+        const float tx = __fsub_rn(fox, f0.x), ty = __fsub_rn(foy, f0.y), tz = __fsub_rn(foz, f0.z);
+        const float cm = fabsf(fox) + fabsf(foy) + fabsf(foz) + f2.z;
         RTSDF_TSTAT(2, 1);
-        if (!tri_maybe(tr, tx, ty, tz, fdx, fdy, fdz, tb)) continue;
+        if (!tri_maybe(tr, tx, ty, tz, fdx, fdy, fdz, tb, cm)) continue;
         RTSDF_TSTAT(3, 1);
         double t = ray_tri(ox, oy, oz, dx, dy, dz, ex);
         if (t >= 0.0 && t <= best_t) {
