@@ -79,6 +79,7 @@ class ShardedFramePipeline:
         self.started = False
         self.last_image = None
         self._dl = None
+        self._gather_buf = None  # rank 0: persistent gather target of the fine slabs
         L = _lib.lib()
         self._clo = (_lib.D * 3)(*scene.lo)
         self._ch = (_lib.D * 3)(*self.h)
@@ -187,10 +188,15 @@ class ShardedFramePipeline:
         count = self.stage_rt()
         img = None
         if render:
-            full = gather_slabs(self.fine, self.bounds, self.rank, group)
+            if self._gather_buf is None and self.rank == 0:
+                nmax = max(n for _, n in self.bounds)
+                self._gather_buf = torch.empty((nmax * self.world,) + self.dims[1:],
+                                               dtype=self.fine.dtype, device=self.fine.device)
+            full = gather_slabs(self.fine, self.bounds, self.rank, group, out=self._gather_buf)
             if self.rank == 0:
                 img = self.stage_dl(full)
-            dist.barrier(group)
+            # no per-frame barrier: the next frame's collectives order the
+            # ranks on the device, and the host may run ahead
         self.frame += 1
         return count, img
 
@@ -212,9 +218,11 @@ def exchange_coarse_halo(coarse_h: torch.Tensor, rank: int, world: int, group=No
             req.wait()
 
 
-def gather_slabs(local: torch.Tensor, bounds, rank: int, group=None):
+def gather_slabs(local: torch.Tensor, bounds, rank: int, group=None, out=None):
     """Concatenated slabs on rank 0 (None elsewhere).  Slabs may differ by a
-    plane; gather needs equal sizes, so each is padded to the largest."""
+    plane; gather needs equal sizes, so each is padded to the largest.  `out`
+    (rank 0, optional): a persistent (world * nmax, ...) buffer received into
+    directly -- with equal slabs the result is a view of it, no copy."""
     import torch.distributed as dist
 
     nmax = max(n for _, n in bounds)
@@ -224,8 +232,12 @@ def gather_slabs(local: torch.Tensor, bounds, rank: int, group=None):
         send = torch.zeros((nmax,) + rest, dtype=local.dtype, device=local.device)
         send[: local.shape[0]] = local
     if rank == 0:
-        parts = [torch.empty((nmax,) + rest, dtype=local.dtype, device=local.device) for _ in bounds]
+        if out is None:
+            out = torch.empty((nmax * len(bounds),) + rest, dtype=local.dtype, device=local.device)
+        parts = [out[r * nmax: (r + 1) * nmax] for r in range(len(bounds))]
         dist.gather(send, parts, dst=0, group=group)
+        if all(n == nmax for _, n in bounds):
+            return out
         return torch.cat([p[:n] for p, (_, n) in zip(parts, bounds)])
     dist.gather(send, None, dst=0, group=group)
     return None

@@ -106,6 +106,9 @@ def launch_step_slab(local, halo_lo, halo_hi, dst, nx, x0, k, h, w, lo, hi):
         _lib.ptr(ws), ws.numel(), _lib.stream()), "jfa_step_slab")
 
 
+_PLANS: dict = {}
+
+
 def flood_slab(local: torch.Tensor, nx: int, rank: int, world: int, h, group=None) -> torch.Tensor:
     """Full JFA schedule on this rank's slab (init seeds in `local`, global
     packed coordinates); returns the flooded slab.  Collective: every rank of
@@ -120,7 +123,10 @@ def flood_slab(local: torch.Tensor, nx: int, rank: int, world: int, h, group=Non
     halo_hi = torch.empty_like(halo_lo)
     src, dst = local, torch.empty_like(local)
     for k in _jfa.jfa_offsets(dims):
-        plan = plan_pass(nx, bounds, k)
+        key = (nx, world, k)
+        plan = _PLANS.get(key)
+        if plan is None:  # pure host logic: once per (grid, world, offset)
+            plan = _PLANS[key] = plan_pass(nx, bounds, k)
         exchange(src, halo_lo, halo_hi, plan, rank, bounds, group)
         lo, hi = halo_ranges(nx, x0, nxl, k)
         launch_step_slab(src, halo_lo, halo_hi, dst, nx, x0, k, h, w, lo, hi)
