@@ -34,22 +34,25 @@ struct Jfa2Task {
 
 // One candidate against one output's running (Km, W).  Keys are even (the
 // non-EXACT pass doubles the weights); an integer tie between a DIFFERENT seed
-// and the running minimum marks Km odd by subtracting 1.  An odd Km = 2m - 1
-// orders exactly like 2m against every (even) key, so later equal keys are
-// neither smaller nor equal (already tied) and a strictly smaller key clears
-// the mark: at the end Km is odd iff >= 2 distinct seeds share the minimum.
-// 4 ALU ops (3 predicate compares, a min) + 2 predicated IMADs on the FMA pipe
-// (`one`/`zero` are opaque to ptxas, which would otherwise fold the moves
-// into ALU selects; the ALU pipe is the pass's bottleneck).
+// and the running minimum marks Km odd.  An odd Km = 2m - 1 orders exactly
+// like 2m against every (even) key, so later equal keys are neither smaller
+// nor equal (already tied) and a strictly smaller key clears the mark: at the
+// end Km is odd iff >= 2 distinct seeds share the minimum (and W, which a tie
+// also overwrites, is then re-decided by the fix-up).  With
+//     p = K <= Km  and  v != W
+// both cases are one update: Km = min(Km - 1, K) (K < Km: K; K == Km: Km - 1)
+// and W = v.  A repeat of the winner (v == W, hence K == Km) changes nothing.
+// 6 instructions: the key, 2 predicate compares and IMNMX (ALU), Km - 1 and
+// the predicated winner move as IMADs (FMA pipe; `one` / `zero` are opaque to
+// ptxas, which would otherwise turn the moves into ALU selects).
 __device__ __forceinline__ void jfa2_eval(int K, int32_t v, int& Km, int32_t& W, int one, int zero) {
     asm volatile(
-        "{\n\t.reg .pred plt, peq, pt;\n\t"
-        "setp.lt.s32 plt, %2, %0;\n\t"
-        "setp.eq.s32 peq, %2, %0;\n\t"
-        "setp.ne.and.s32 pt, %3, %1, peq;\n\t"
-        "min.s32 %0, %0, %2;\n\t"
-        "@plt mad.lo.s32 %1, %1, %5, %3;\n\t"
-        "@pt mad.lo.s32 %0, %0, %4, -1;\n\t}"
+        "{\n\t.reg .pred p;\n\t.reg .s32 km1;\n\t"
+        "setp.le.s32 p, %2, %0;\n\t"
+        "setp.ne.and.s32 p, %3, %1, p;\n\t"
+        "mad.lo.s32 km1, %0, %4, -1;\n\t"
+        "@p min.s32 %0, km1, %2;\n\t"
+        "@p mad.lo.s32 %1, %1, %5, %3;\n\t}"
         : "+r"(Km), "+r"(W)
         : "r"(K), "r"(v), "r"(one), "r"(zero));
 }
