@@ -62,18 +62,20 @@ __device__ __forceinline__ void jfa2_eval(int K, int32_t v, int& Km, int32_t& W,
 // then exactly proportional to the integer key, so the reference's rule
 // (fp64 d2, then lexicographic) IS the lexicographic order of (key, packed
 // seed) -- ties resolve in the hot loop, no flags, no fix-up.  (K, v) < (Km, W)
-// with the seed compared unsigned (EMPTY = 0xffffffff is the largest):
-// 3 predicate compares, a min and a select.
-__device__ __forceinline__ void jfa2_eval_exact(int K, int32_t v, int& Km, int32_t& W) {
+// with the seed compared unsigned (EMPTY = 0xffffffff is the largest): one
+// 64-bit signed compare of {K : v} (key high, seed low -- the low word counts
+// unsigned), i.e. ISETP.U32 + ISETP.EX, and the two moves as predicated IMADs
+// on the FMA pipe: 5 instructions per candidate with its key.
+__device__ __forceinline__ void jfa2_eval_exact(int K, int32_t v, int& Km, int32_t& W, int zero) {
     asm volatile(
-        "{\n\t.reg .pred peq, pe, p;\n\t"
-        "setp.eq.s32 peq, %2, %0;\n\t"
-        "setp.lt.and.u32 pe, %3, %1, peq;\n\t"
-        "setp.lt.or.s32 p, %2, %0, pe;\n\t"
-        "min.s32 %0, %0, %2;\n\t"
-        "selp.b32 %1, %3, %1, p;\n\t}"
+        "{\n\t.reg .pred p;\n\t.reg .b64 a, b;\n\t"
+        "mov.b64 a, {%3, %2};\n\t"
+        "mov.b64 b, {%1, %0};\n\t"
+        "setp.lt.s64 p, a, b;\n\t"
+        "@p mad.lo.s32 %0, %0, %4, %2;\n\t"
+        "@p mad.lo.s32 %1, %1, %4, %3;\n\t}"
         : "+r"(Km), "+r"(W)
-        : "r"(K), "r"(v));
+        : "r"(K), "r"(v), "r"(zero));
 }
 
 struct JfaFixList {
@@ -199,7 +201,7 @@ __global__ void __launch_bounds__(128) jfa_pass2_kernel(PlaneSrc src, int32_t* _
                     for (int b = 0; b < RY; ++b) {
                         K -= Gy;  // output row b = tap row -1 + (b + 1)
                         if (EXACT)
-                            jfa2_eval_exact(K, v, Km[s][b], W[s][b]);
+                            jfa2_eval_exact(K, v, Km[s][b], W[s][b], zero);
                         else
                             jfa2_eval(K, v, Km[s][b], W[s][b], one, zero);
                     }
@@ -230,7 +232,7 @@ __global__ void __launch_bounds__(128) jfa_pass2_kernel(PlaneSrc src, int32_t* _
                         if (b < 0 || b >= RY) continue;  // compile-time
                         const int K = db == 0 ? Bs[s] : (db < 0 ? Bs[s] + Gy : Bs[s] - Gy);
                         if (EXACT)
-                            jfa2_eval_exact(K, v, Km[s][b], W[s][b]);
+                            jfa2_eval_exact(K, v, Km[s][b], W[s][b], zero);
                         else
                             jfa2_eval(K, v, Km[s][b], W[s][b], one, zero);
                     }
