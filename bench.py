@@ -131,9 +131,9 @@ def jfa_traffic():
 def issue_roofline(n_cells, pass_ms, ck):
     """The JFA pass's binding roofline: instruction issue.  Thread-instructions
     per cell of the dense pass from the committed ncu capture
-    (profiles/r1k_jfa_pass_k4_opmix.txt); peak = 148 SMs x 4 schedulers x 1
+    (profiles/r1l_jfa_pass_k4_opmix.txt); peak = 148 SMs x 4 schedulers x 1
     warp-instruction / clock x 32 lanes at the measured SM clock."""
-    p = ROOT / "profiles" / "r1k_jfa_pass_k4_opmix.txt"
+    p = ROOT / "profiles" / "r1l_jfa_pass_k4_opmix.txt"
     ipc = None
     if p.exists():
         for ln in p.read_text().splitlines():
