@@ -514,6 +514,10 @@ static void launch_pass2(PlaneSrc s, int32_t* dst, float* dst_sdf, const JfaGeom
     Jfa2Task T;
     T.one = 1;
     T.zero = 0;
+#ifndef JFA2_SKIP_K
+#define JFA2_SKIP_K 16
+#endif
+    T.skip = k >= JFA2_SKIP_K;
     T.nzb = (g.nz + 31) / 32;
     T.jres = k < g.ny ? k : g.ny;
     T.jgroups = (chain_y + ry - 1) / ry;

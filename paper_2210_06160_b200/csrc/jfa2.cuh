@@ -23,6 +23,12 @@
 #pragma once
 #include "common.cuh"
 
+#ifndef JFA2_FULL_LOADS
+#define JFA2_FULL_LOADS 0
+#endif
+#ifndef JFA2_SKIP_MODE
+#define JFA2_SKIP_MODE 1
+#endif
 #define JFA2_EMPTY_KEY (1 << 30)  // larger than any real (doubled) key: |key| < 2^29
 
 namespace rtsdf {
@@ -30,6 +36,7 @@ namespace rtsdf {
 struct Jfa2Task {
     int nzb, jres, jgroups, ires, isegs, L;
     int one, zero;  // = 1, 0 (opaque to ptxas, see jfa2_eval)
+    int skip;       // pass input may hold all-EMPTY tap segments (k >= 16)
 };
 
 // One candidate against one output's running (Km, W).  Keys are even (the
@@ -155,6 +162,15 @@ __global__ void __launch_bounds__(128) jfa_pass2_kernel(PlaneSrc src, int32_t* _
                 m = okmask;
             }
         }
+#if JFA2_FULL_LOADS
+        if (m == (1u << (3 * (RY + 2))) - 1u) {  // interior plane (warp-uniform): plain loads
+#pragma unroll
+            for (int bt = 0; bt < RY + 2; ++bt)
+#pragma unroll
+                for (int c = 0; c < 3; ++c) vals[bt][c] = __ldg(pl + offs[bt][c]);
+            return;
+        }
+#endif
 #pragma unroll
         for (int bt = 0; bt < RY + 2; ++bt)
 #pragma unroll
@@ -214,7 +230,14 @@ __global__ void __launch_bounds__(128) jfa_pass2_kernel(PlaneSrc src, int32_t* _
 #pragma unroll
             for (int c = -1; c <= 1; ++c) {
                 const int32_t v = cur[bt + 1][c + 1];
+#if JFA2_SKIP_MODE == 1
+                // the all-EMPTY vote only in passes that can have EMPTY tap
+                // segments (uniform branch on the task; dense passes keep the
+                // per-tap region boundary, which ptxas schedules better)
+                if (T.skip && __all_sync(0xffffffffu, v == RTSDF_EMPTY)) continue;
+#else
                 if (__all_sync(0xffffffffu, v == RTSDF_EMPTY)) continue;  // warp-uniform skip
+#endif
                 const int sx = unpack_i(v), sy = unpack_j(v), sk = unpack_k(v);
                 const int B0 = sx * (wx * sx + cx) + sy * (wy * sy + cy) + sk * (wz * sk + cz);
                 // EMPTY (-1) decodes to (4095, 1023, 1023): its increments stay bounded
