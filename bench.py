@@ -113,8 +113,8 @@ def peaks():
 
 def jfa_traffic():
     """DRAM bytes (read + write) per dense JFA pass launch from the committed
-    ncu --set full capture (profiles/r1l_frame_kernels_summary.csv), or None."""
-    p = ROOT / "profiles" / "r1l_frame_kernels_summary.csv"
+    ncu --set full capture (profiles/r1m_frame_kernels_summary.csv), or None."""
+    p = ROOT / "profiles" / "r1m_frame_kernels_summary.csv"
     if not p.exists():
         return None, None
     import csv
