@@ -150,6 +150,9 @@ __global__ void __launch_bounds__(SAMPLE_THREADS) sample_update_kernel(SamplePar
 #endif
 #define WF_BUDGET 4   // binary search tree: internal-node visits in pass 1
 #define WF_BUDGET4 2  // BVH4: root only (ground-plane leaves finish in pass 1)
+#ifndef WF_B2_PER_SM
+#define WF_B2_PER_SM 12  // pass-2 blocks per SM (grid-stride over the long-ray queue)
+#endif
 
 // Per-texel accumulators instead of per-ray results: the closest hit t as its
 // fp64 bit pattern (t >= 0, so unsigned integer order is fp64 order; ~0 = no
@@ -833,7 +836,7 @@ extern "C" int rtsdf_sample_update(const void* bvh_packed, int64_t n_nodes, int6
             return e ? atoi(e) : 0;
         }();
         const int budget = budget_env > 0 ? budget_env : (wide ? WF_BUDGET4 : WF_BUDGET);
-        const unsigned b1 = (unsigned)(blocks < cap ? blocks : cap), b2 = (unsigned)(num_sms() * 12);
+        const unsigned b1 = (unsigned)(blocks < cap ? blocks : cap), b2 = (unsigned)(num_sms() * WF_B2_PER_SM);
         // persistent per-lane-refill tracer: exact, but measured slower than the
         // two-pass wavefront on B200 (6.67 vs 6.32 ms at C3), so opt-in only
         static const bool persist = getenv("RTSDF_WF_PERSIST") != nullptr;
