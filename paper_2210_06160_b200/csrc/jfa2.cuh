@@ -13,13 +13,14 @@
 // For a loaded seed s at tap plane a / tap row bt, the key of output (a', b')
 //     Key = |s|^2_w - 2 w . (x * s) = q(s, x) - |x|^2_w
 // is B - (a' - a) Gx - (b' - bt) Gy with B, Gx = 2 wx k si, Gy = 2 wy k sj
-// computed once per value: every candidate costs one IADD plus a compare and
-// two selects.  The minimum integer key is the reference's fp64 minimum.  An
-// integer tie between two DIFFERENT seeds (a few % of cells in the late
-// passes) only marks the output (odd running key, jfa2_eval); flagged cells are appended to a list
-// and re-decided by jfa_fixup_kernel with the reference's own rule
-// (fp64 d2, then lexicographic; jfa.py:108-124), so the hot loop has no fp64
-// and no divergent branch.
+// computed once per value: every candidate costs its key (one IMAD) plus the
+// 5-instruction update of jfa2_eval (4 with jfa2_eval_exact).  The minimum
+// integer key is the reference's fp64 minimum.  An integer tie between two
+// DIFFERENT seeds (a few % of cells in the late passes) only marks the output
+// (odd running key, jfa2_eval); marked cells are appended to a list and
+// re-decided by jfa_fixup_kernel with the reference's own rule (fp64 d2, then
+// lexicographic; jfa.py:108-124), so the hot loop has no fp64 and no
+// divergent branch.
 #pragma once
 #include "common.cuh"
 
@@ -190,7 +191,7 @@ __global__ void __launch_bounds__(128) jfa_pass2_kernel(PlaneSrc src, int32_t* _
         // depends only on (seed, output), so the RY + 2 copies of a tap column
         // are one candidate per output: 3 columns x 3 slots x RY rows instead
         // of the 3 x 3 x 3 x RY tap/row pairs (repeats of a (key, seed) pair
-        // cannot change the running minimum, the winner or the tie flag).
+        // cannot change the running minimum, the winner or the tie mark).
         // Only tried in the sparse early passes (k >= 64): after them, rows of
         // different residue classes hold different provisional seeds and the
         // test (15 compares + a vote per plane) almost never succeeds.
