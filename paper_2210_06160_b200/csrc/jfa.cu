@@ -483,6 +483,17 @@ static bool dims_ok(int nx, int ny, int nz) {
     return true;
 }
 
+// jfa2.cuh NAT: min over the grid of the virtual EMPTY seed's weighted d2
+// (taken at the far corner) > the largest real weighted d2 in the grid.
+static bool natural_empty_ok(const JfaGeom& g) {
+    static const bool off = getenv("RTSDF_JFA_NO_NAT") != nullptr;
+    if (off) return false;
+    auto sq = [](double v) { return v * v; };
+    const double e = g.wx * sq(4096.0 - g.nx) + g.wy * sq(1024.0 - g.ny) + g.wz * sq(1024.0 - g.nz);
+    const double r = g.wx * sq(g.nx - 1.0) + g.wy * sq(g.ny - 1.0) + g.wz * sq(g.nz - 1.0);
+    return e > r;
+}
+
 // K2 v2 launch (INT mode): task decomposition of jfa2.cuh, then the exact
 // re-decision of the (rare) integer-tie cells the pass flagged.
 static JfaFixList fix_list(void* ws, int64_t n_cells) {
@@ -511,6 +522,7 @@ static void launch_pass2(PlaneSrc s, int32_t* dst, float* dst_sdf, const JfaGeom
     // Segment length L: each unit re-loads 2 halo planes per L outputs, so
     // longer is cheaper (measured at C3: L = 24 is ~8 % faster than 8) as long
     // as the grid still fills the GPU for two waves (~16 resident warps / SM).
+    const bool nat = natural_empty_ok(g);
     Jfa2Task T;
     T.one = 1;
     T.zero = 0;
@@ -538,7 +550,8 @@ static void launch_pass2(PlaneSrc s, int32_t* dst, float* dst_sdf, const JfaGeom
     static const bool v3_on = getenv("RTSDF_JFA_V3") != nullptr;
     if (g.exact) {  // ties resolve inside the pass: no flags, no fix-up
         if (ry == 4)
-            jfa_pass2_kernel<4, FINAL, SLAB, true><<<blocks, 128, 0, st>>>(s, dst, dst_sdf, g, T, beta, empty_count, fix);
+            nat ? jfa_pass2_kernel<4, FINAL, SLAB, true, true><<<blocks, 128, 0, st>>>(s, dst, dst_sdf, g, T, beta, empty_count, fix)
+                : jfa_pass2_kernel<4, FINAL, SLAB, true><<<blocks, 128, 0, st>>>(s, dst, dst_sdf, g, T, beta, empty_count, fix);
         else if (ry == 2)
             jfa_pass2_kernel<2, FINAL, SLAB, true><<<blocks, 128, 0, st>>>(s, dst, dst_sdf, g, T, beta, empty_count, fix);
         else
@@ -554,7 +567,8 @@ static void launch_pass2(PlaneSrc s, int32_t* dst, float* dst_sdf, const JfaGeom
         else
             jfa_pass3_kernel<1, FINAL, SLAB><<<blocks, 128, 0, st>>>(s, dst, dst_sdf, g, T, beta, empty_count, fix);
     } else if (ry == 4)
-        jfa_pass2_kernel<4, FINAL, SLAB, false><<<blocks, 128, 0, st>>>(s, dst, dst_sdf, g, T, beta, empty_count, fix);
+        nat ? jfa_pass2_kernel<4, FINAL, SLAB, false, true><<<blocks, 128, 0, st>>>(s, dst, dst_sdf, g, T, beta, empty_count, fix)
+            : jfa_pass2_kernel<4, FINAL, SLAB, false><<<blocks, 128, 0, st>>>(s, dst, dst_sdf, g, T, beta, empty_count, fix);
     else if (ry == 2)
         jfa_pass2_kernel<2, FINAL, SLAB, false><<<blocks, 128, 0, st>>>(s, dst, dst_sdf, g, T, beta, empty_count, fix);
     else

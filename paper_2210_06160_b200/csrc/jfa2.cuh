@@ -92,7 +92,11 @@ struct JfaFixList {
     int64_t cap;
 };
 
-template <int RY, bool FINAL, bool SLAB, bool EXACT>
+// NAT: the host proved that the packed EMPTY (-1) decodes to a virtual seed
+// (4095, 1023, 1023) whose key exceeds every real seed's key at every cell of
+// the grid (jfa.cu natural_empty_ok), so an EMPTY tap needs no select: it can
+// neither win nor tie, and a run of EMPTY taps leaves (Km, W) = (init, EMPTY).
+template <int RY, bool FINAL, bool SLAB, bool EXACT, bool NAT = false>
 __global__ void __launch_bounds__(128) jfa_pass2_kernel(PlaneSrc src, int32_t* __restrict__ dst,
                                                         float* __restrict__ dst_sdf, JfaGeom g,
                                                         Jfa2Task T, double beta,
@@ -208,7 +212,7 @@ __global__ void __launch_bounds__(128) jfa_pass2_kernel(PlaneSrc src, int32_t* _
                 if (__all_sync(0xffffffffu, v == RTSDF_EMPTY)) continue;
                 const int sx = unpack_i(v), sy = unpack_j(v), sk = unpack_k(v);
                 const int B0 = sx * (wx * sx + cx) + sy * (wy * sy + cy) + sk * (wz * sk + cz);
-                const int B = v != RTSDF_EMPTY ? B0 : JFA2_EMPTY_KEY;
+                const int B = NAT || v != RTSDF_EMPTY ? B0 : JFA2_EMPTY_KEY;
                 const int Gx = gxk * sx, Gy = gyk * sy;
                 const int Bs[3] = {B + Gx, B, B - Gx};
 #pragma unroll
@@ -244,7 +248,7 @@ __global__ void __launch_bounds__(128) jfa_pass2_kernel(PlaneSrc src, int32_t* _
                 // EMPTY (-1) decodes to (4095, 1023, 1023): its increments stay bounded
                 // (|Gx|, |Gy| < 2^23), so an EMPTY base of 2^30 can never beat a real
                 // key (|key| < 2^29) -- no per-increment selects
-                const int B = v != RTSDF_EMPTY ? B0 : JFA2_EMPTY_KEY;
+                const int B = NAT || v != RTSDF_EMPTY ? B0 : JFA2_EMPTY_KEY;
                 const int Gx = gxk * sx, Gy = gyk * sy;
                 // K(a', b') = B - (a' - a) Gx - (b' - bt) Gy; slot s <-> a' = a - 1 + s
                 const int Bs[3] = {B + Gx, B, B - Gx};
