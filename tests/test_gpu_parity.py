@@ -126,6 +126,34 @@ def test_jfa_every_pass_matches_oracle(rt, name, dims):
     np.testing.assert_array_equal(_np(rt.seeds_to_sdf(cur).data), O.seeds_to_sdf(ref, h))
 
 
+@pytest.mark.parametrize("dims,hi,frac,weights", [
+    # weights 1:9:16 over 1000-cell axes: the packed EMPTY's virtual seed is
+    # NOT provably the farthest (jfa.cu natural_empty_ok false -> select path)
+    ((8, 1000, 1000), (0.064, 24.0, 32.0), 2e-4, (1, 9, 16)),
+    # C3's 1:4:1 weights on a random dense-ish soup: many integer ties
+    ((64, 48, 80), (0.512, 0.768, 0.64), 0.01, (1, 4, 1)),
+    # dyadic spacing 1/128: fp64 d2 exact -> EXACT mode (64-bit lexicographic test)
+    ((64, 48, 80), (0.5, 0.375, 0.625), 0.01, (1, 1, 1)),
+])
+def test_jfa_random_occupancy_every_pass_and_schedule(rt, dims, hi, frac, weights):
+    """Random seeds, non-dyadic spacings (INT mode with tie marks + fix-ups):
+    every pass and the whole schedule (sparse early passes) == the oracle."""
+    rng = np.random.default_rng(7)
+    occ = (rng.random(dims) < frac).astype(np.uint8)
+    lo, hi = np.zeros(3), np.array(hi, dtype=np.float64)
+    h = (hi - lo) / np.array(dims, dtype=np.float64)
+    assert rt.jfa.integer_weights(*map(float, h), dims) == weights
+    vg = rt.VoxelGrid(rt._device.to_device(occ), lo, hi)
+    ref = O.jfa_init(occ)
+    cur = rt.jfa_init(vg)
+    for off in rt.jfa_offsets(dims):
+        ref = O.jfa_step(ref, off, h)
+        cur = rt.jfa_step(cur, off)
+        np.testing.assert_array_equal(_np(cur.seed), ref, err_msg=f"offset {off}")
+    np.testing.assert_array_equal(_np(rt.jfa_run(vg).seed), ref)
+    np.testing.assert_array_equal(_np(rt.jump_flood(vg).data), O.seeds_to_sdf(ref, h))
+
+
 def test_jfa_golden_c3_and_sp128(rt):
     G = golden()
     scene, mesh = scene_mesh("sphere_plane")
