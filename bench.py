@@ -330,7 +330,11 @@ def run_ours(args, rank, world, local_rank):
         "config": dict(workload(args.rays),
                        parallelism=(f"z-slab x{world} (NCCL P2P halos per JFA pass, coarse 1-plane "
                                     "halo, fine slabs gathered for DL)") if sharded else
-                       (f"replicas x{world}" if world > 1 else "1 GPU")),
+                       (f"replicas x{world}" if world > 1 else "1 GPU"),
+                       frame_overlap=(None if sharded else
+                                      "V + JF of frame f+1 on a flood stream during frame f's RT/DL "
+                                      "(static scene, double-buffered); frame_stages_ms come from one "
+                                      "serial event-timed frame")),
         "frame_stages_ms": {k: round(v, 4) for k, v in stages_ms.items()},
         "masked_texels": masked, "rays_per_frame": rays,
         "rays_per_s": round(rays / (sample_ms * 1e-3), 1),

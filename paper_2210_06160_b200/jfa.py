@@ -188,11 +188,14 @@ def flood_inplace(a: torch.Tensor, b: torch.Tensor, h) -> torch.Tensor:
 
 
 def flood_to_sdf(a: torch.Tensor, b: torch.Tensor, out: torch.Tensor, h, beta=0.0,
-                 empty_count=None):
-    """Full schedule with seeds -> SDF fused into the last pass (a, b clobbered)."""
+                 empty_count=None, ws=None):
+    """Full schedule with seeds -> SDF fused into the last pass (a, b clobbered).
+    ws: a private workspace (rtsdf_jfa_ws_bytes) for callers that flood on a
+    stream of their own; None = the shared per-device one."""
     nx, ny, nz = a.shape
     w = _weights(h, (nx, ny, nz))
-    ws = workspace(nx, ny, nz)
+    if ws is None:
+        ws = workspace(nx, ny, nz)
     _lib.check(_lib.lib().rtsdf_jfa_run_sdf(_lib.ptr(a), _lib.ptr(b), _lib.ptr(out), nx, ny, nz,
                                             float(h[0]), float(h[1]), float(h[2]), *w,
                                             float(beta), _lib.ptr(empty_count), _lib.ptr(ws),

@@ -404,6 +404,46 @@ def test_pipeline_frames_golden(rt, case):
         np.testing.assert_allclose(img, golden_arrays()["c3.image"], rtol=1e-6, atol=1e-7)
 
 
+@pytest.mark.parametrize("timings", [(False, False, False), (False, True, False)])
+def test_pipeline_overlapped_frames_golden(rt, timings):
+    """Cross-frame flood overlap (static scene, timing=False: frame f + 1's V + JF
+    run on the flood stream during frame f's RT) == the reference frames; the
+    mixed case switches to the serial, event-timed path and back mid-run."""
+    G = golden()
+    scene = rt.get_scene(C1["scene"])
+    pc = rt.PipelineConfig(coarse_dims=C1["dims"], fine_dims=C1["dims"],
+                           sampling=rt.SamplingParams(rays_per_frame=C1["x"]))
+    assert pc.overlap_frames
+    pipe = rt.FramePipeline(scene, pc)
+    pipe.direction_fn = lambda idx, frame: O.dir_table(0, idx, frame, C1["x"])
+    for f, timing in enumerate(timings):
+        rec = pipe.advance(render=False, timing=timing)
+        assert (pipe._prefetch is not None) == (not timing)  # frame f + 1 in flight
+        g = G[f"c1.frame{f}"]
+        assert rec.masked_texels == g["masked"]
+        assert digest(_np(pipe.coarse.data)) == g["coarse"]
+        assert digest(_np(pipe.fine.data)) == g["fine"]
+        assert digest(_np(pipe.accum.front)) == g["front"]
+        assert digest(_np(pipe.accum.back)) == g["back"]
+
+
+def test_pipeline_overlap_c3_device_rng_identical(rt):
+    """C3, device RNG, rendered: 3 overlapped frames == 3 serial frames, bit for bit."""
+    out = []
+    for overlap in (False, True):
+        pc = rt.PipelineConfig(coarse_dims=C3["dims"], fine_dims=C3["dims"], overlap_frames=overlap,
+                               sampling=rt.SamplingParams(rays_per_frame=C3["x"]))
+        pipe = rt.FramePipeline(rt.get_scene(C3["scene"]), pc)
+        for _ in range(3):
+            rec = pipe.advance(render=True, timing=False)
+        out.append((rec.masked_texels, _np(pipe.coarse.data), _np(pipe.fine.data),
+                    _np(pipe.last_occlusion)))
+        del pipe
+    assert out[0][0] == out[1][0]
+    for a, b in zip(out[0][1:], out[1][1:]):
+        np.testing.assert_array_equal(a, b)
+
+
 def test_animated_scene_frames_match_oracle(rt):
     """Dynamic scene: the orbit scene's occluder moves every
     frame -> per-frame merged mesh + BVH; 3 frames of the pipeline with the host
