@@ -112,6 +112,10 @@ class FramePipeline:
         self._checked_view = None
         self._prefetch = None  # (frame, JF buffer set, event) flooded ahead
         self._jf_ws = None
+        # cfg.overlap_frames, switchable between frames: off when the caller
+        # rewrites the mesh buffers every frame (frame f + 1's V is launched
+        # during frame f and would read them one upload early)
+        self.overlap_frames = config.overlap_frames
         # parity mode: callable(masked_idx ndarray, frame) -> (M, x, 3) host direction
         # table (the north star's host-supplied table); None = device SplitMix64
         self.direction_fn = None
@@ -256,7 +260,7 @@ class FramePipeline:
         # V + JF: packed self-seeds straight from the triangles (K1), full
         # schedule (K2) + seeds -> SDF (K3).  Static scenes with overlap_frames
         # run them on the flood stream one frame ahead (see _flood_ahead).
-        overlap = cfg.overlap_frames and not timing and not self.scene.animated
+        overlap = self.overlap_frames and not timing and not self.scene.animated
         pre = self._prefetch
         self._prefetch = None
         main = torch.cuda.current_stream()
