@@ -338,7 +338,7 @@ def run_ours(args, rank, world, local_rank):
                        (f"replicas x{world}" if world > 1 else "1 GPU"),
                        frame_overlap=(None if sharded else
                                       "V + JF of frame f+1 on a flood stream during frame f's RT/DL "
-                                      "(static scene, double-buffered); frame_stages_ms come from one "
+                                      "(static scene, BVH <= 16 MB, double-buffered); frame_stages_ms come from one "
                                       "serial event-timed frame; off for e2e, whose every frame uploads its mesh")),
         "frame_stages_ms": {k: round(v, 4) for k, v in stages_ms.items()},
         "masked_texels": masked, "rays_per_frame": rays,

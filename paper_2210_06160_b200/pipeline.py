@@ -7,8 +7,9 @@ HBM; a frame is a fixed sequence of ~35 kernel launches, with the JFA seeds
 emitted directly by the voxelizer and the fine field updated in place.  V + JF
 depend on the geometry only, so for a static scene frame f + 1's are launched
 on a flood stream while frame f's RT / DL run on the caller's stream
-(`PipelineConfig.overlap_frames`; double-buffered seeds + coarse field).  Pass durations come from CUDA
-events, not the host clock.
+(`PipelineConfig.overlap_frames`, auto = while the BVH is far below L2;
+double-buffered seeds + coarse field).  Pass durations come from CUDA events,
+not the host clock.
 
 `hybrid_sdf(scene, config, frames)` is the north-star entry point.
 """
@@ -48,8 +49,11 @@ class PipelineConfig:
     repeats: int = 1
     # static scenes: flood frame f+1 (V + JF, which depend on the geometry only)
     # on a second stream while frame f's RT / DL run (B200 form; no effect on
-    # any result -- every frame still voxelizes and floods its own seeds)
-    overlap_frames: bool = True
+    # any result -- every frame still voxelizes and floods its own seeds).
+    # None = auto: on while the tracer's BVH + triangles stay far below L2
+    # (the flood's streaming grids would evict them: C4's 180 MB tree ran
+    # 112-117 ms/frame overlapped vs 110 serial; C3's 0.2 MB tree 8.62 vs 9.00)
+    overlap_frames: bool | None = None
 
     def __post_init__(self):
         for f, c in zip(self.fine_dims, self.coarse_dims):
@@ -112,7 +116,7 @@ class FramePipeline:
         self._checked_view = None
         self._prefetch = None  # (frame, JF buffer set, event) flooded ahead
         self._jf_ws = None
-        # cfg.overlap_frames, switchable between frames: off when the caller
+        # cfg.overlap_frames (None = auto), switchable between frames: off when the caller
         # rewrites the mesh buffers every frame (frame f + 1's V is launched
         # during frame f and would read them one upload early)
         self.overlap_frames = config.overlap_frames
@@ -205,6 +209,14 @@ class FramePipeline:
                           ws=self._jf_ws)
         return js["coarse"]
 
+    OVERLAP_MAX_BVH_BYTES = 16 << 20  # << the 126 MB L2
+
+    def _overlap_for(self, view) -> bool:
+        if self.overlap_frames is not None:
+            return bool(self.overlap_frames)
+        bvh = view.bvh
+        return bvh.search.numel() * bvh.search.element_size() <= self.OVERLAP_MAX_BVH_BYTES
+
     def _flood_ahead(self, frame):
         """Launch V + JF of `frame` on the flood stream.  It waits for
         everything already queued on the main stream -- frame - 2's RT read the
@@ -260,7 +272,7 @@ class FramePipeline:
         # V + JF: packed self-seeds straight from the triangles (K1), full
         # schedule (K2) + seeds -> SDF (K3).  Static scenes with overlap_frames
         # run them on the flood stream one frame ahead (see _flood_ahead).
-        overlap = self.overlap_frames and not timing and not self.scene.animated
+        overlap = not timing and not self.scene.animated and self._overlap_for(view)
         pre = self._prefetch
         self._prefetch = None
         main = torch.cuda.current_stream()

@@ -413,8 +413,9 @@ def test_pipeline_overlapped_frames_golden(rt, timings):
     scene = rt.get_scene(C1["scene"])
     pc = rt.PipelineConfig(coarse_dims=C1["dims"], fine_dims=C1["dims"],
                            sampling=rt.SamplingParams(rays_per_frame=C1["x"]))
-    assert pc.overlap_frames
+    assert pc.overlap_frames is None  # auto
     pipe = rt.FramePipeline(scene, pc)
+    assert pipe._overlap_for(scene.view(0))  # a 5,120-triangle tree: far below L2
     pipe.direction_fn = lambda idx, frame: O.dir_table(0, idx, frame, C1["x"])
     for f, timing in enumerate(timings):
         rec = pipe.advance(render=False, timing=timing)
