@@ -116,6 +116,7 @@ class FramePipeline:
         self._checked_view = None
         self._prefetch = None  # (frame, JF buffer set, event) flooded ahead
         self._jf_ws = None
+        self._flood_marked = {}  # id -> tensor already recorded on the flood stream
         # cfg.overlap_frames (None = auto), switchable between frames: off when the caller
         # rewrites the mesh buffers every frame (frame f + 1's V is launched
         # during frame f and would read them one upload early)
@@ -207,6 +208,15 @@ class FramePipeline:
             self._jf_ws = torch.empty(n, dtype=torch.uint8, device=js["coarse"].device)
         _jfa.flood_to_sdf(js["seed_a"], js["seed_b"], js["coarse"], vox.cell_size, cfg.beta,
                           ws=self._jf_ws)
+        cur = torch.cuda.current_stream()
+        if cur == getattr(self, "_flood", None):
+            # buffers allocated on the caller's stream and written here: the
+            # allocator must not hand them out again before this work is done
+            mb = view.mesh_buffers()
+            for t in (*js.values(), self._jf_ws, *vars(mb).values()):
+                if isinstance(t, torch.Tensor) and id(t) not in self._flood_marked:
+                    t.record_stream(cur)
+                    self._flood_marked[id(t)] = t
         return js["coarse"]
 
     OVERLAP_MAX_BVH_BYTES = 16 << 20  # << the 126 MB L2
