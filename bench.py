@@ -188,6 +188,10 @@ def run_ours(args, rank, world, local_rank):
         def step():
             pipe.advance(render=True, timing=False)
 
+    def join():  # the frame flooded ahead (V + JF of step K + 1) is inside the timed region
+        if not sharded:
+            pipe.join()
+
     for _ in range(max(3, args.warmup)):
         step()
     barrier()
@@ -199,6 +203,7 @@ def run_ours(args, rank, world, local_rank):
     e0.record()
     for _ in range(args.steps):
         step()
+    join()
     e1.record()
     barrier()
     launches = _lib.launch_count() - l0

@@ -52,7 +52,7 @@ class PipelineConfig:
     # any result -- every frame still voxelizes and floods its own seeds).
     # None = auto: on while the tracer's BVH + triangles stay far below L2
     # (the flood's streaming grids would evict them: C4's 180 MB tree ran
-    # 112-117 ms/frame overlapped vs 110 serial; C3's 0.2 MB tree 8.62 vs 9.00)
+    # 112-117 ms/frame overlapped vs 110 serial; C3's 0.2 MB tree 8.70 vs 9.00)
     overlap_frames: bool | None = None
 
     def __post_init__(self):
@@ -219,6 +219,14 @@ class FramePipeline:
                     self._flood_marked[id(t)] = t
         return js["coarse"]
 
+    def join(self):
+        """Make the caller's stream wait for the frame flooded ahead (if any):
+        after it, every kernel this pipeline launched precedes what the caller
+        queues next -- timing loops end with it so the timed region holds
+        exactly one V + JF per frame."""
+        if self._prefetch is not None:
+            torch.cuda.current_stream().wait_event(self._prefetch[2])
+
     OVERLAP_MAX_BVH_BYTES = 16 << 20  # << the 126 MB L2
 
     def _overlap_for(self, view) -> bool:
@@ -244,7 +252,7 @@ class FramePipeline:
         st = getattr(self, "_flood", None)
         if st is None or st.device != torch.cuda.current_stream().device:
             st = self._flood = torch.cuda.Stream()  # default priority (measured: a high-priority
-            # flood stream 8.81 vs 8.62 ms/frame, a high-priority RT stream 8.63)
+            # flood stream 8.81 vs 8.62 ms/frame, a high-priority RT stream 8.63; unjoined timing)
         return st
 
     def _side_stream(self):

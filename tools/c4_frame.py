@@ -41,6 +41,7 @@ for _ in range(2):
 e0.record()
 for _ in range(frames):
     pipe.advance(render=True, timing=False)
+pipe.join()
 e1.record()
 torch.cuda.synchronize()
 print(f"C4 ms/frame with the flood overlap forced on {e0.elapsed_time(e1) / frames:.2f}")

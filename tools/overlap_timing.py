@@ -19,6 +19,7 @@ for overlap in (True, True):
     e0.record()
     for _ in range(20):
         pipe.advance(render=True, timing=False)
+    pipe.join()
     e1.record()
     torch.cuda.synchronize()
     print("overlap", overlap, "ms/frame", round(e0.elapsed_time(e1) / 20, 4), flush=True)
