@@ -144,6 +144,9 @@ class FramePipeline:
             )
             self._bufs["jf"] = [dict(seed_a=self._bufs["seed_a"], seed_b=self._bufs["seed_b"],
                                      coarse=self._bufs["coarse"]), None]
+            # private JFA workspace: the flood stream must not share _jfa's
+            n = int(_lib.lib().rtsdf_jfa_ws_bytes(*cd))
+            self._jf_ws = torch.empty(n, dtype=torch.uint8, device=dev)
         return self._bufs
 
     def _jf_set(self, s):
@@ -203,9 +206,6 @@ class FramePipeline:
             self._checked_view = view
         if events is not None:
             events[1].record()
-        if self._jf_ws is None:  # private: the flood stream must not share _jfa's
-            n = int(_lib.lib().rtsdf_jfa_ws_bytes(*map(int, cfg.coarse_dims)))
-            self._jf_ws = torch.empty(n, dtype=torch.uint8, device=js["coarse"].device)
         _jfa.flood_to_sdf(js["seed_a"], js["seed_b"], js["coarse"], vox.cell_size, cfg.beta,
                           ws=self._jf_ws)
         cur = torch.cuda.current_stream()
@@ -242,6 +242,7 @@ class FramePipeline:
         queued after it and overlaps it."""
         flood = self._flood_stream()
         flood.wait_stream(torch.cuda.current_stream())
+        self._jf_set(frame % 2)  # allocated on the caller's stream (see _coarse_pass)
         with torch.cuda.stream(flood):
             self._coarse_pass(self.scene.view(frame), frame % 2)
             ev = torch.cuda.Event()
@@ -301,6 +302,7 @@ class FramePipeline:
         elif overlap:
             flood = self._flood_stream()
             flood.wait_stream(main)
+            self._jf_set(frame % 2)
             with torch.cuda.stream(flood):
                 self._coarse_pass(view, frame % 2)
                 ev = torch.cuda.Event()
