@@ -162,3 +162,20 @@ def test_product_does_not_import_oracle():
     pat = re.compile(r"(import\s+oracle|from\s+oracle|rtsdf_oracle|oracle\.py|sys\.path.*oracle)")
     for f in list(pkg.glob("*.py")) + list((pkg / "csrc").glob("*.c*")):
         assert not pat.search(f.read_text()), f
+
+
+def test_pipeline_overlap_config_host_side():
+    """Flood-ahead overlap knobs (no GPU): auto by default, switchable per
+    pipeline, join() a no-op with nothing flooded ahead, animated scenes never
+    overlap (their next frame needs a new mesh + BVH)."""
+    import paper_2210_06160_b200 as rt
+
+    pc = rt.PipelineConfig(coarse_dims=(8, 8, 8), fine_dims=(8, 8, 8))
+    assert pc.overlap_frames is None
+    pipe = rt.FramePipeline(rt.get_scene("sphere"), pc)
+    assert pipe.overlap_frames is None and pipe._prefetch is None
+    pipe.join()
+    pipe.overlap_frames = False
+    assert pipe._overlap_for(None) is False  # explicit setting wins before any BVH lookup
+    assert rt.get_scene("orbit").animated and not rt.get_scene("sphere").animated
+    assert rt.FramePipeline.OVERLAP_MAX_BVH_BYTES < 126 << 20
