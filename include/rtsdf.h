@@ -259,12 +259,22 @@ int rtsdf_exact_distance(const void* bvh_packed, int64_t n_nodes, const double* 
  * of spp cone-sampled shadow rays (origin pos + 1e-4 nrm, stream
  * (seed, pixel, 1)) with no hit; 1.0 where uncovered.  light / t1 / t2 are
  * the unit light direction and the cone basis (host[3] each, render.py:237-
- * 241); tan_r = tan(angular radius).  CUDA sincos stands in for glibc.     */
+ * 241); tan_r = tan(angular radius).  cos / sin are the bit-exact
+ * restatement of the host glibc's (glibc_sincos.cuh), as below.            */
 int rtsdf_reference_visibility(const void* bvh_packed, int64_t n_nodes, const double* g_pos,
                                const double* g_nrm, const uint8_t* g_cov, int height, int width,
                                const double* light /*host[3]*/, const double* t1 /*host[3]*/,
                                const double* t2 /*host[3]*/, double tan_r, int spp,
                                uint64_t seed, double* out_vis, void* stream);
+
+/* Replaces rng.py:46-53 (unit_sphere_dir) for n stream keys x x counters:
+ * dirs[(t * x + r) * 3 + c], the reference's uniform sphere directions with
+ * the host libm's cos / sin restated bit for bit (glibc 2.39 FMA build,
+ * glibc_sincos.cuh) -- the same device code the sampler uses.              */
+int rtsdf_unit_sphere_dirs(const uint64_t* keys, int64_t n, int x, double* dirs, void* stream);
+/* glibc sin / cos (|x| < 105414350, NaN beyond) of n device doubles: the
+ * restatement's own check against the host libm (tests).                   */
+int rtsdf_glibc_sincos(const double* x, int64_t n, double* s, double* c, void* stream);
 
 /* ------------------------------------------------------------- soft shadow */
 /* Replaces render.py:167 (_occlusion_kernel): per covered pixel fp64 sphere

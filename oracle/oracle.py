@@ -35,6 +35,7 @@ _SIGS = {
     "oracle_uniform": (D, [U64, U64]),
     "oracle_unit_sphere_dir": (None, [U64, U64, P]),
     "oracle_dir_table": (None, [U64, P, I64, I64, I, P]),
+    "oracle_libm_sincos": (None, [P, I64, P, P]),
     "oracle_bvh_build": (I64, [P, P, I64, P, P, P, P, P]),
     "oracle_ray_query": (None, [P, P, P, P, P, P, P, P, P, P, P, I64, D, P, P, P]),
     "oracle_ray_brute": (None, [P, P, P, P, P, P, P, P, P, I64, P, P, I64, D, P, P, P]),
@@ -190,6 +191,14 @@ def dir_table(seed, idx, frame, x):
     out = np.empty((len(idx), int(x), 3), np.float64)
     lib().oracle_dir_table(int(seed) & (2**64 - 1), _p(idx), len(idx), int(frame), int(x), _p(out))
     return out
+
+
+def libm_sincos(x):
+    """The host libm's (sin, cos) of every element (the reference's rng.py:53 calls)."""
+    x = _c(x, np.float64)
+    s, c = np.empty_like(x), np.empty_like(x)
+    lib().oracle_libm_sincos(_p(x), x.size, _p(s), _p(c))
+    return s, c
 
 
 # ----------------------------------------------------------------- geometry

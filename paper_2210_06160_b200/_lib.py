@@ -63,6 +63,8 @@ SIGNATURES = {
     "rtsdf_compact_mask_range": (I, [P, I64, I64, P, P, P, P, SZ, P]),
     "rtsdf_exact_distance": (I, [P, I64, P, I64, P, P]),
     "rtsdf_reference_visibility": (I, [P, I64, P, P, P, I, I, DP, DP, DP, D, I, U64, P, P]),
+    "rtsdf_unit_sphere_dirs": (I, [P, I64, I, P, P]),
+    "rtsdf_glibc_sincos": (I, [P, I64, P, P, P]),
     "rtsdf_bvh_build_host": (I64, [P, P, I64, P, P, P, P, P]),
     "rtsdf_bvh_build_sah_host": (I64, [P, P, I64, I, P, P, P, P, P]),
     "rtsdf_bvh_packed_bytes": (SZ, [I64, I64]),

@@ -8,6 +8,7 @@
 #include <stdint.h>
 
 #include "../../include/rtsdf.h"
+#include "glibc_sincos.cuh"
 
 #define RTSDF_EMPTY (-1)
 #define RTSDF_MAX_DIM 1024
@@ -151,10 +152,10 @@ __device__ __forceinline__ void unit_sphere_dir(uint64_t key, uint64_t counter, 
     double z = __dsub_rn(1.0, __dmul_rn(2.0, u));
     double r = __dsqrt_rn(dmax_(0.0, __dsub_rn(1.0, __dmul_rn(z, z))));
     double phi = __dmul_rn(6.283185307179586, v);
-    double s, c;
-    sincos(phi, &s, &c);  // CUDA libdevice; may differ from glibc in the last ulp
-    dx = __dmul_rn(r, c);
-    dy = __dmul_rn(r, s);
+    // rng.py:53 calls the host libm's cos / sin: its glibc FMA build, restated
+    // bit for bit in glibc_sincos.cuh (CUDA's sincos differs in the last ulp)
+    dx = __dmul_rn(r, gs::glibc_cos(phi));
+    dy = __dmul_rn(r, gs::glibc_sin(phi));
     dz = z;
 }
 

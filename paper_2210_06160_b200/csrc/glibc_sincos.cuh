@@ -1,0 +1,208 @@
+// glibc_sincos.cuh -- bit-exact restatement of the host libm sin/cos that the
+// reference's ray directions go through (rng.py:53: r * np.cos(phi),
+// r * np.sin(phi); numba lowers them to libm calls).
+//
+// On this image that is glibc 2.39's sysdeps/ieee754/dbl-64/s_sin.c, which
+// x86-64 dispatches by ifunc to its FMA build (__sin_fma / __cos_fma) on every
+// host with FMA + AVX2.  That build lets gcc contract a*b + c into FMA, so the
+// rounding of every step depends on where the compiler fused: the functions
+// below follow the machine code of __sin_fma / __cos_fma instruction by
+// instruction (each GS_FMA is one vfmadd/vfnmadd of the binary, each GS_MUL /
+// GS_ADD / GS_SUB one unfused vmulsd / vaddsd / vsubsd), restated in glibc's
+// own structure (do_sin, do_cos, reduce_sincos, TAYLOR_SIN).  The range
+// covered is |x| < 105414350 (glibc's reduce_sincos range; the ray
+// directions only need [0, 2 pi)); larger arguments (glibc's branred) are not
+// restated and return NaN.
+//
+// Compiled for the device (DFMA / DMUL / DADD with explicit rounding, so nvcc
+// neither fuses nor splits anything) and for the host (gcc -ffp-contract=off,
+// fma() from libm): tests/test_glibc_sincos.py checks the host build against
+// math.sin / math.cos over 2^24 arguments of the form 2 pi v and every branch
+// boundary, and the GPU tests check the device against the reference's golden
+// direction tables.
+#pragma once
+#include <math.h>
+#include <stdint.h>
+#include <string.h>
+
+#ifdef __CUDACC__
+#define GS_HD __host__ __device__ __forceinline__
+#else
+#define GS_HD static inline
+#endif
+
+#if defined(__CUDA_ARCH__)
+#define GS_MUL(a, b) __dmul_rn((a), (b))
+#define GS_ADD(a, b) __dadd_rn((a), (b))
+#define GS_SUB(a, b) __dsub_rn((a), (b))
+#define GS_FMA(a, b, c) __fma_rn((a), (b), (c))
+#else
+#define GS_MUL(a, b) ((a) * (b))
+#define GS_ADD(a, b) ((a) + (b))
+#define GS_SUB(a, b) ((a) - (b))
+#define GS_FMA(a, b, c) fma((a), (b), (c))
+#endif
+
+namespace rtsdf {
+namespace gs {
+
+#ifdef __CUDACC__
+#define RTSDF_GS_TABLE_DECL __device__ const double gs_table_dev[RTSDF_GS_TABLE_N]
+#include "glibc_sincostab.inc"
+#undef RTSDF_GS_TABLE_DECL
+#endif
+#define RTSDF_GS_TABLE_DECL static const double gs_table_host[RTSDF_GS_TABLE_N]
+#include "glibc_sincostab.inc"
+#undef RTSDF_GS_TABLE_DECL
+
+GS_HD double tab(int i) {
+#if defined(__CUDA_ARCH__)
+    return __ldg(gs_table_dev + i);  // per-lane indices: L1, not the constant cache
+#else
+    return gs_table_host[i];
+#endif
+}
+
+GS_HD uint64_t bits(double x) {
+#if defined(__CUDA_ARCH__)
+    return (uint64_t)__double_as_longlong(x);
+#else
+    uint64_t u;
+    memcpy(&u, &x, 8);
+    return u;
+#endif
+}
+GS_HD double from_bits(uint64_t u) {
+#if defined(__CUDA_ARCH__)
+    return __longlong_as_double((long long)u);
+#else
+    double x;
+    memcpy(&x, &u, 8);
+    return x;
+#endif
+}
+GS_HD double gabs(double x) { return from_bits(bits(x) & 0x7fffffffffffffffull); }
+GS_HD double gneg(double x) { return from_bits(bits(x) ^ 0x8000000000000000ull); }
+GS_HD double gcopysign(double m, double s) {
+    return from_bits((bits(m) & 0x7fffffffffffffffull) | (bits(s) & 0x8000000000000000ull));
+}
+
+// constants of s_sin.c / usncs.h (values as stored in the binary)
+#define GS_BIG 0x1.8p+45          // 52776558133248
+#define GS_TOINT 0x1.8p+52        // 6755399441055744
+#define GS_HPINV 0x1.45f306dc9c883p-1
+#define GS_HP0 0x1.921fb54442d18p+0
+#define GS_HP1 0x1.1a62633145c07p-54
+#define GS_MP1 0x1.921fb58p+0
+#define GS_MP2 -0x1.dde973cp-27
+#define GS_PP3 -0x1.cb3b398p-55
+#define GS_PP4 -0x1.d747f23e32ed7p-83
+#define GS_SN3 -0x1.5555555555515p-3
+#define GS_SN5 0x1.11110e829872fp-7
+#define GS_CS2 0x1p-1
+#define GS_CS4 -0x1.5555555555535p-5
+#define GS_CS6 0x1.6c16bedd9e239p-10
+#define GS_S1 -0x1.5555555555555p-3
+#define GS_S2 0x1.1111111110ecep-7
+#define GS_S3 -0x1.a01a019db08b8p-13
+#define GS_S4 0x1.71de27b9a7ed9p-19
+#define GS_S5 -0x1.addffc2fcdf59p-26
+
+// TAYLOR_SIN(xx, a, da) = a + ((POLY(xx) * a - 0.5 * da) * xx + da)
+// (__sin_fma: the chain of 5 vfmadd213sd, vfmsub132sd, vfmadd132sd, vaddsd)
+GS_HD double taylor_sin(double a, double da) {
+    const double xx = GS_MUL(a, a);
+    double p = GS_FMA(xx, GS_S5, GS_S4);
+    p = GS_FMA(xx, p, GS_S3);
+    p = GS_FMA(xx, p, GS_S2);
+    p = GS_FMA(xx, p, GS_S1);
+    const double t = GS_FMA(p, a, gneg(GS_MUL(da, 0.5)));
+    return GS_ADD(a, GS_FMA(xx, t, da));
+}
+
+// do_sin(x, dx): table path for 0.126 <= |x| < 0.855469 (plus the reduced
+// argument's tail dx); TAYLOR_SIN below 0.126
+GS_HD double do_sin(double x, double dx) {
+    const double xold = x;
+    if (gabs(x) < 0.126) return taylor_sin(x, dx);
+    if (x <= 0.0) dx = gneg(dx);
+    const double u = GS_ADD(gabs(x), GS_BIG);
+    const int k = (int)((uint32_t)bits(u) << 2);
+    x = GS_SUB(gabs(x), GS_SUB(u, GS_BIG));
+    const double xx = GS_MUL(x, x);
+    const double s = GS_ADD(x, GS_FMA(GS_MUL(x, xx), GS_FMA(xx, GS_SN5, GS_SN3), dx));
+    const double c = GS_FMA(x, dx, GS_MUL(xx, GS_FMA(xx, GS_FMA(xx, GS_CS6, GS_CS4), GS_CS2)));
+    const double sn = tab(k), ssn = tab(k + 1), cs = tab(k + 2), ccs = tab(k + 3);
+    // cor = (ssn + s * ccs - sn * c) + cs * s
+    const double cor = GS_FMA(s, cs, GS_FMA(gneg(c), sn, GS_FMA(s, ccs, ssn)));
+    return gcopysign(GS_ADD(sn, cor), xold);
+}
+
+// do_cos(x, dx)
+GS_HD double do_cos(double x, double dx) {
+    if (x < 0.0) dx = gneg(dx);
+    const double u = GS_ADD(gabs(x), GS_BIG);
+    const int k = (int)((uint32_t)bits(u) << 2);
+    x = GS_ADD(GS_SUB(gabs(x), GS_SUB(u, GS_BIG)), dx);
+    const double xx = GS_MUL(x, x);
+    const double s = GS_FMA(GS_MUL(x, xx), GS_FMA(xx, GS_SN5, GS_SN3), x);
+    const double c = GS_MUL(xx, GS_FMA(xx, GS_FMA(xx, GS_CS6, GS_CS4), GS_CS2));
+    const double sn = tab(k), ssn = tab(k + 1), cs = tab(k + 2), ccs = tab(k + 3);
+    // cor = (ccs - s * ssn - cs * c) - sn * s
+    const double cor = GS_FMA(gneg(s), sn, GS_FMA(gneg(c), cs, GS_FMA(gneg(s), ssn, ccs)));
+    return GS_ADD(cs, cor);
+}
+
+// reduce_sincos: x = n pi/2 + (a + da)
+GS_HD int reduce_sincos(double x, double& a, double& da) {
+    const double t = GS_FMA(x, GS_HPINV, GS_TOINT);
+    const double xn = GS_SUB(t, GS_TOINT);
+    const int n = (int)(bits(t) & 3);
+    const double y = GS_FMA(gneg(xn), GS_MP2, GS_FMA(gneg(xn), GS_MP1, x));
+    const double t2 = GS_FMA(gneg(xn), GS_PP3, y);
+    double db = GS_FMA(gneg(xn), GS_PP3, GS_SUB(y, t2));
+    const double b = GS_FMA(gneg(xn), GS_PP4, t2);
+    db = GS_ADD(db, GS_FMA(gneg(xn), GS_PP4, GS_SUB(t2, b)));
+    a = b;
+    da = db;
+    return n;
+}
+
+GS_HD double do_sincos(double a, double da, int n) {
+    const double r = (n & 1) ? do_cos(a, da) : do_sin(a, da);
+    return (n & 2) ? gneg(r) : r;
+}
+
+GS_HD double glibc_sin(double x) {
+    const uint32_t k = (uint32_t)(bits(x) >> 32) & 0x7fffffffu;
+    if (k < 0x3e500000u) return x;
+    if (k < 0x3feb6000u) return do_sin(x, 0.0);
+    if (k < 0x400368fdu) return gcopysign(do_cos(GS_SUB(GS_HP0, gabs(x)), GS_HP1), x);
+    if (k < 0x419921fbu) {
+        double a, da;
+        const int n = reduce_sincos(x, a, da);
+        return do_sincos(a, da, n);
+    }
+    return from_bits(0x7ff8000000000000ull);  // not restated (branred / non-finite)
+}
+
+GS_HD double glibc_cos(double x) {
+    const uint32_t k = (uint32_t)(bits(x) >> 32) & 0x7fffffffu;
+    if (k < 0x3e400000u) return 1.0;
+    if (k < 0x3feb6000u) return do_cos(x, 0.0);
+    if (k < 0x400368fdu) {
+        const double y = GS_SUB(GS_HP0, gabs(x));
+        const double a = GS_ADD(y, GS_HP1);
+        const double da = GS_ADD(GS_SUB(y, a), GS_HP1);
+        return do_sin(a, da);
+    }
+    if (k < 0x419921fbu) {
+        double a, da;
+        const int n = reduce_sincos(x, a, da);
+        return do_sincos(a, da, n + 1);
+    }
+    return from_bits(0x7ff8000000000000ull);
+}
+
+}  // namespace gs
+}  // namespace rtsdf

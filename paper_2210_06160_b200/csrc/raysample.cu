@@ -23,6 +23,7 @@ struct SampleParams {
     const int64_t* idx;
     const int64_t* count;
     int64_t m_cap;
+    int64_t n_begin;  // sample_update_kernel: first texel (the tail beyond the wavefront capacity)
     FieldView coarse;
     int fnx, fny, fnz;
     double fhx, fhy, fhz;
@@ -59,9 +60,9 @@ __global__ void __launch_bounds__(SAMPLE_THREADS) sample_update_kernel(SamplePar
     const int my_t = lane / seg, pos = lane - my_t * seg;
     const int64_t nyz = (int64_t)P.fny * P.fnz;
     const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
-    for (int64_t wbase = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; wbase * tpw < M;
-         wbase += warps) {
-        const int64_t n = wbase * tpw + my_t;
+    for (int64_t wbase = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+         P.n_begin + wbase * tpw < M; wbase += warps) {
+        const int64_t n = P.n_begin + wbase * tpw + my_t;
         const bool active = my_t < tpw && n < M;
         int64_t lin = active ? __ldg(P.idx + n) : 0;
         int i = (int)(lin / nyz), j = (int)((lin / P.fnz) % P.fny), k = (int)(lin % P.fnz);
@@ -478,51 +479,6 @@ __global__ void __launch_bounds__(WF_THREADS, WF_MINB) wf_pass2_kernel(SamplePar
     }
 }
 
-// Persistent tracer (opt-in, RTSDF_WF_PERSIST): every lane owns one ray at a time
-// and advances it one node visit / leaf per iteration; as soon as a lane's ray
-// completes it writes the per-ray result and the idle lanes of the warp fetch
-// the next rays from a global counter (one warp-aggregated atomic).  Short and
-// long rays no longer share a warp's lifetime, so lanes stay busy until the
-// whole ray set drains (the budgeted two-pass wavefront still left pass 2 at
-// 26 % SIMD efficiency).  Ray ids are fetched in order, so a warp keeps working
-// on neighbouring texels.
-__global__ void __launch_bounds__(WF_THREADS, WF_MINB) wf_persist4_kernel(SampleParams P, WfBuffers B) {
-    __shared__ int32_t stack_mem[RTSDF_FAST_STACK * WF_THREADS];
-    __shared__ __half tstack_mem[RTSDF_FAST_STACK * WF_THREADS];
-    int32_t* stack = stack_mem + threadIdx.x;
-    __half* tstack = tstack_mem + threadIdx.x;
-    const int lane = threadIdx.x & 31;
-    const int64_t R = min(*P.count, P.m_cap) * P.x;
-    int64_t r = -1;  // current ray; -1 idle, -2 drained
-    Trace4State s;
-    while (true) {
-        const bool idle = r == -1;
-        const unsigned m = __ballot_sync(0xffffffffu, idle);
-        if (m) {
-            int64_t base = 0;
-            if (lane == (__ffs(m) - 1))
-                base = (int64_t)atomicAdd((unsigned long long*)B.qcount, (unsigned long long)__popc(m));
-            base = __shfl_sync(0xffffffffu, base, __ffs(m) - 1);
-            if (idle) {
-                const int64_t rr = base + __popc(m & ((1u << lane) - 1));
-                if (rr < R) {
-                    double ox, oy, oz, dx, dy, dz;
-                    wf_ray(P, B, rr, ox, oy, oz, dx, dy, dz);
-                    trace4_init(s, ox, oy, oz, dx, dy, dz, P.t_max);
-                    r = rr;
-                } else {
-                    r = -2;
-                }
-            }
-        }
-        if (__all_sync(0xffffffffu, r == -2)) break;
-        if (r >= 0 && trace4_step(P.bvh4, s, stack, tstack, WF_THREADS)) {
-            if (s.best_id >= 0) wf_commit(B, fdiv((unsigned)r, P.div_x), s.best_t, s.best_facing);
-            r = -1;
-        }
-    }
-}
-
 // raysample.py:140-152 (per-texel min / votes, in ray order) + :229-244 (Eq. 1)
 __global__ void __launch_bounds__(WF_THREADS) wf_reduce_update_kernel(SampleParams P, WfBuffers B) {
     const int64_t M = min(*P.count, P.m_cap);
@@ -577,149 +533,6 @@ static size_t wf_ws_bytes(int64_t m_cap, int x) {
            oct_scan_temp_bytes(wf_oct_blocks(R)) + 256;
 }
 
-// ----------------------------------------------------------------------------
-// Direction-binned sampler.  A block takes a group of G masked texels (G * x <=
-// BIN_RAYS rays), generates every ray's direction, counting-sorts the rays by
-// cube-map direction bin in shared memory and traces them in sorted order, so
-// a warp holds ~32 rays of similar direction from neighbouring texels instead
-// of 32 random directions from one texel (the traversal's SIMD efficiency was
-// 36 %).  Per-ray results land in shared memory and each texel is reduced and
-// updated by one thread in ray order -- deterministic, no global atomics.
-#define BIN_THREADS 128
-#define BIN_RAYS 512
-#define BIN_COUNT 24
-#define BIN_STACK RTSDF_FAST_STACK
-
-__device__ __forceinline__ int dir_bin(double dx, double dy, double dz) {
-    double ax = fabs(dx), ay = fabs(dy), az = fabs(dz);
-    int face, u, v;
-    if (ax >= ay && ax >= az) { face = dx >= 0 ? 0 : 1; u = dy >= 0; v = dz >= 0; }
-    else if (ay >= az) { face = dy >= 0 ? 2 : 3; u = dx >= 0; v = dz >= 0; }
-    else { face = dz >= 0 ? 4 : 5; u = dx >= 0; v = dy >= 0; }
-    return face * 4 + u * 2 + v;
-}
-
-__global__ void __launch_bounds__(BIN_THREADS) sample_update_binned_kernel(SampleParams P) {
-    extern __shared__ __align__(16) unsigned char smem[];
-    const int x = P.x;
-    const int G = BIN_RAYS / x;                            // texels per group (x <= BIN_RAYS)
-    double* sdir = (double*)smem;                          // [BIN_RAYS][3]
-    double* st = sdir + 3 * BIN_RAYS;                      // [BIN_RAYS] hit t (or -1)
-    int32_t* stack_mem = (int32_t*)(st + BIN_RAYS);        // [BIN_STACK][BIN_THREADS]
-    int16_t* sorder = (int16_t*)(stack_mem + BIN_STACK * BIN_THREADS);  // [BIN_RAYS]
-    uint8_t* sbin = (uint8_t*)(sorder + BIN_RAYS);         // [BIN_RAYS]
-    uint8_t* sfac = sbin + BIN_RAYS;                       // [BIN_RAYS]
-    double* scen = (double*)(sfac + BIN_RAYS);             // [G][3] texel centres
-    __shared__ int hist[BIN_COUNT], cursor[BIN_COUNT];
-
-    const int tid = threadIdx.x;
-    const int64_t M = min(*P.count, P.m_cap);
-    const int64_t nyz = (int64_t)P.fny * P.fnz;
-    const int64_t groups = (M + G - 1) / G;
-    for (int64_t grp = blockIdx.x; grp < groups; grp += gridDim.x) {
-        const int64_t n0 = grp * G;
-        const int g = (int)min((int64_t)G, M - n0);
-        const int R = g * x;
-        if (tid < BIN_COUNT) hist[tid] = 0;
-        // texel centres (raysample.py:167-169)
-        for (int q = tid; q < g; q += BIN_THREADS) {
-            int64_t lin = __ldg(P.idx + n0 + q);
-            int i = (int)(lin / nyz), j = (int)((lin / P.fnz) % P.fny), k = (int)(lin % P.fnz);
-            scen[3 * q] = P.coarse.lox + ((double)i + 0.5) * P.fhx;
-            scen[3 * q + 1] = P.coarse.loy + ((double)j + 0.5) * P.fhy;
-            scen[3 * q + 2] = P.coarse.loz + ((double)k + 0.5) * P.fhz;
-        }
-        __syncthreads();
-        // directions + bins
-        for (int r = tid; r < R; r += BIN_THREADS) {
-            const int q = r / x, ray = r - q * x;
-            const int64_t n = n0 + q;
-            double dx, dy, dz;
-            if (P.dirs) {
-                const double* d = P.dirs + 3 * (n * x + ray);
-                dx = d[0];
-                dy = d[1];
-                dz = d[2];
-            } else {
-                int64_t lin = __ldg(P.idx + n);
-                uint64_t key = stream_key(P.seed, (uint64_t)lin, (uint64_t)P.frame);
-                unit_sphere_dir(key, (uint64_t)ray, dx, dy, dz);
-            }
-            sdir[3 * r] = dx;
-            sdir[3 * r + 1] = dy;
-            sdir[3 * r + 2] = dz;
-            int b = dir_bin(dx, dy, dz);
-            sbin[r] = (uint8_t)b;
-            atomicAdd(&hist[b], 1);
-        }
-        __syncthreads();
-        if (tid == 0) {
-            int s = 0;
-            for (int b = 0; b < BIN_COUNT; ++b) {
-                cursor[b] = s;
-                s += hist[b];
-            }
-        }
-        __syncthreads();
-        for (int r = tid; r < R; r += BIN_THREADS) sorder[atomicAdd(&cursor[sbin[r]], 1)] = (int16_t)r;
-        __syncthreads();
-        // trace in bin order: consecutive lanes hold rays of one direction bin
-        for (int p = tid; p < R; p += BIN_THREADS) {
-            const int r = sorder[p];
-            const int q = r / x;
-            int32_t id;
-            int facing;
-            double t = trace_fast(P.bvh, scen[3 * q], scen[3 * q + 1], scen[3 * q + 2],
-                                  sdir[3 * r], sdir[3 * r + 1], sdir[3 * r + 2], P.t_max,
-                                  stack_mem + tid, BIN_THREADS, id, facing);
-            st[r] = id >= 0 ? t : -1.0;
-            sfac[r] = (uint8_t)(id >= 0 ? facing : 0);
-        }
-        __syncthreads();
-        // per texel, in ray order (raysample.py:140-152) + Eq. 1 (raysample.py:229-244)
-        for (int q = tid; q < g; q += BIN_THREADS) {
-            const int64_t n = n0 + q;
-            double best = __longlong_as_double(0x7ff0000000000000ll);
-            int fr = 0, bk = 0;
-            for (int ray = 0; ray < x; ++ray) {
-                const int r = q * x + ray;
-                const int f = sfac[r];
-                if (f) {
-                    const double t = st[r];
-                    if (t < best) best = t;
-                    fr += f == 1;
-                    bk += f == 2;
-                }
-            }
-            if (P.samp_min) P.samp_min[n] = best;
-            if (P.samp_front) P.samp_front[n] = fr;
-            if (P.samp_back) P.samp_back[n] = bk;
-            if (!P.prev) continue;
-            const int64_t lin = __ldg(P.idx + n);
-            float rm = P.run_min[lin];
-            int32_t f = P.front[lin], b = P.back[lin];
-            if (!P.mask_old[lin]) {
-                rm = __int_as_float(0x7f800000);
-                f = 0;
-                b = 0;
-            }
-            double m = best;
-            if (m < (double)rm) rm = (float)m;
-            f += fr;
-            b += bk;
-            P.run_min[lin] = rm;
-            P.front[lin] = f;
-            P.back[lin] = b;
-            double c = (double)(float)trilinear(P.coarse, scen[3 * q], scen[3 * q + 1],
-                                                scen[3 * q + 2]);
-            double blend = P.alpha * fabs((double)P.prev[lin]) + (1.0 - P.alpha) * c;
-            double mag = blend < m ? blend : m;
-            P.out[lin] = b > f ? (float)(-mag) : (float)mag;
-        }
-        __syncthreads();
-    }
-}
-
 static void launch_oct_queue(const WfBuffers& B, int64_t R, cudaStream_t st) {
     const int64_t nc = wf_chunks(R), nb = wf_oct_blocks(R);
     wf_oct_count_kernel<<<(unsigned)nb, WF_OCT_THREADS, 0, st>>>(nc, B);
@@ -727,12 +540,6 @@ static void launch_oct_queue(const WfBuffers& B, int64_t R, cudaStream_t st) {
     cub::DeviceScan::ExclusiveScan(B.scan_tmp, tb, (const Oct8*)B.oct_blk, (Oct8*)B.oct_pos,
                                    Oct8Sum(), Oct8{}, (int)nb, st);
     wf_oct_scatter_kernel<<<(unsigned)nb, WF_OCT_THREADS, 0, st>>>(nc, B);
-}
-
-static size_t binned_smem_bytes(int x) {
-    return (size_t)BIN_RAYS * (3 + 1) * sizeof(double) +
-           (size_t)BIN_STACK * BIN_THREADS * sizeof(int32_t) + BIN_RAYS * (2 + 1 + 1) +
-           (size_t)(BIN_RAYS / x) * 3 * sizeof(double);
 }
 
 }  // namespace rtsdf
@@ -765,6 +572,7 @@ extern "C" int rtsdf_sample_update(const void* bvh_packed, int64_t n_nodes, int6
     P.idx = idx;
     P.count = count;
     P.m_cap = m_cap;
+    P.n_begin = 0;
     P.coarse = FieldView{rs->coarse, rs->cnx, rs->cny, rs->cnz, rs->clo[0], rs->clo[1],
                          rs->clo[2], rs->ch[0], rs->ch[1], rs->ch[2], 0.0f};
     P.fnx = rs->fnx;
@@ -792,17 +600,12 @@ extern "C" int rtsdf_sample_update(const void* bvh_packed, int64_t n_nodes, int6
     P.back = back;
     P.alpha = alpha;
     P.out = out;
-    // sampler selection: wavefront (default, needs the workspace), warp-per-texel
-    // (RTSDF_SAMPLER=warp or no workspace) or direction-binned (experimental)
-    static const int mode = [] {
-        const char* e = getenv("RTSDF_SAMPLER");
-        if (!e) return 0;
-        return e[0] == 'b' ? 2 : (e[0] == 'w' && e[1] == 'a' ? 1 : 0);
-    }();
+    // wavefront sampler (needs the workspace); the warp-per-texel kernel when
+    // there is none or x is beyond the packed-vote range
     const bool wf_ok = x >= 1 && x <= 65535 && ws && ws_bytes >= wf_ws_bytes(m_cap, x) &&
                        m_cap * (int64_t)x < ((int64_t)1 << 31);
     cudaStream_t st = (cudaStream_t)stream;
-    if (mode == 0 && wf_ok) {
+    if (wf_ok) {
         WfBuffers B;
         char* p = (char*)ws;
         B.qcount = (int64_t*)p;
@@ -831,69 +634,51 @@ extern "C" int rtsdf_sample_update(const void* bvh_packed, int64_t n_nodes, int6
         int64_t blocks = (R + WF_THREADS - 1) / WF_THREADS;
         int64_t cap = (int64_t)num_sms() * 24;
         const bool wide = n_nodes4 > 0;
-        static const int budget_env = [] {
-            const char* e = getenv("RTSDF_WF_BUDGET");
-            return e ? atoi(e) : 0;
-        }();
         // large BVH4s (C4: ~10^5 nodes): almost no ray finishes at the root, so pass 1
         // only generates, classifies and queues (budget 1: measured 110.5 -> 109.5
         // ms/frame at C4); small ones finish their ground-plane leaves in pass 1
-        const int budget = budget_env > 0 ? budget_env
-                                          : (wide ? (n_nodes4 > 4096 ? 1 : WF_BUDGET4) : WF_BUDGET);
+        const int budget = wide ? (n_nodes4 > 4096 ? 1 : WF_BUDGET4) : WF_BUDGET;
         const unsigned b1 = (unsigned)(blocks < cap ? blocks : cap), b2 = (unsigned)(num_sms() * WF_B2_PER_SM);
-        // persistent per-lane-refill tracer: exact, but measured slower than the
-        // two-pass wavefront on B200 (6.67 vs 6.32 ms at C3), so opt-in only
-        static const bool persist = getenv("RTSDF_WF_PERSIST") != nullptr;
-        int launches = 4;
+        int launches = 4;  // setup, pass 1, pass 2, reduce + update
         wf_setup_kernel<<<(unsigned)cap, WF_THREADS, 0, st>>>(P, B);
-        if (!B.aligned || (wide && persist)) {  // accumulators not initialised by pass 1
+        if (!B.aligned) {  // accumulators not initialised by pass 1
             wf_init_kernel<<<(unsigned)cap, WF_THREADS, 0, st>>>(P, B);
             ++launches;
         }
-        if (wide && persist) {
-            P.bvh4 = fast_bvh4_view(bvh_packed, n_nodes, n_tris);
-            wf_persist4_kernel<<<(unsigned)(num_sms() * 8), WF_THREADS, 0, st>>>(P, B);
-        } else if (wide) {
+        if (wide) {
             P.bvh4 = fast_bvh4_view(bvh_packed, n_nodes, n_tris);
             wf_pass1_kernel<true><<<b1, WF_THREADS, 0, st>>>(P, B, budget);
             launch_oct_queue(B, R, st);
-            launches += 2;  // + cub's scan
+            launches += 2;  // count + scatter (+ cub's scan)
             wf_pass2_kernel<true><<<b2, WF_THREADS, 0, st>>>(P, B);
         } else {
             wf_pass1_kernel<false><<<b1, WF_THREADS, 0, st>>>(P, B, budget);
             launch_oct_queue(B, R, st);
-            launches += 2;  // + cub's scan
+            launches += 2;
             wf_pass2_kernel<false><<<b2, WF_THREADS, 0, st>>>(P, B);
         }
         int64_t ublocks = (m_cap + WF_THREADS - 1) / WF_THREADS;
         wf_reduce_update_kernel<<<(unsigned)(ublocks < cap ? ublocks : cap), WF_THREADS, 0, st>>>(P, B);
+        // texels beyond the workspace capacity (the host sized it from an earlier
+        // frame's count without a sync): traced and updated by the workspace-free
+        // warp-per-texel kernel -- same per-ray results, same order-free
+        // reduction, so the frame is exact whatever the capacity; a no-op when
+        // *count <= m_cap
+        SampleParams T = P;
+        T.n_begin = m_cap;
+        T.m_cap = INT64_MAX;
+        sample_update_kernel<<<(unsigned)(num_sms() * 4), SAMPLE_THREADS, 0, st>>>(T);
+        ++launches;
         count_launch(launches);
         return check_launch("sample_update");
     }
-    if (mode == 2 && x >= 1 && x <= BIN_RAYS) {  // direction-binned path (experimental)
-        static bool attr = false;
-        const size_t smem = binned_smem_bytes(x);
-        if (!attr) {
-            cudaFuncSetAttribute(sample_update_binned_kernel,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)binned_smem_bytes(1));
-            attr = true;
-        }
-        const int G = BIN_RAYS / x;
-        int64_t blocks = (m_cap + G - 1) / G;
-        int64_t cap = (int64_t)num_sms() * 8;
-        if (blocks > cap) blocks = cap;
-        if (blocks < 1) blocks = 1;
-        sample_update_binned_kernel<<<(unsigned)blocks, BIN_THREADS, smem, (cudaStream_t)stream>>>(P);
-    } else {
-        int tpw = x >= 32 || x == 0 ? 1 : 32 / x;
-        int64_t warps_needed = (m_cap + tpw - 1) / tpw;
-        int64_t blocks = (warps_needed + SAMPLE_THREADS / 32 - 1) / (SAMPLE_THREADS / 32);
-        int64_t cap = (int64_t)num_sms() * 16;
-        if (blocks > cap) blocks = cap;
-        if (blocks < 1) blocks = 1;
-        sample_update_kernel<<<(unsigned)blocks, SAMPLE_THREADS, 0, (cudaStream_t)stream>>>(P);
-    }
+    int tpw = x >= 32 || x == 0 ? 1 : 32 / x;
+    int64_t warps_needed = (m_cap + tpw - 1) / tpw;
+    int64_t blocks = (warps_needed + SAMPLE_THREADS / 32 - 1) / (SAMPLE_THREADS / 32);
+    int64_t cap = (int64_t)num_sms() * 16;
+    if (blocks > cap) blocks = cap;
+    if (blocks < 1) blocks = 1;
+    sample_update_kernel<<<(unsigned)blocks, SAMPLE_THREADS, 0, st>>>(P);
     count_launch();
     return check_launch("sample_update");
 }

@@ -10,8 +10,7 @@
 //   * reference_visibility (render.py:195-254): per covered pixel, the
 //     fraction of spp cone-sampled shadow rays with no hit (closest-hit
 //     traversal of the reference-order BVH, t_max = inf).  Directions use
-//     CUDA's sincos where the reference calls glibc cos/sin (last-ulp
-//     differences; the tests bound the effect).
+//     the bit-exact restatement of the host libm's cos/sin (glibc_sincos.cuh).
 //
 // One thread per point / pixel, fp64 without contraction (--fmad=false).
 #include "common.cuh"
@@ -160,8 +159,7 @@ __global__ void __launch_bounds__(128) reference_visibility_kernel(
         const double v = uniform01(key, 2 * (uint64_t)s + 1);
         const double r = V.tan_r * sqrt(u);
         const double phi = 6.283185307179586 * v;  // 2.0 * math.pi folded exactly
-        double sn, c;
-        sincos(phi, &sn, &c);
+        const double sn = gs::glibc_sin(phi), c = gs::glibc_cos(phi);  // render.py's math.cos/sin
         const double dx = V.lx + r * (c * V.t1x + sn * V.t2x);
         const double dy = V.ly + r * (c * V.t1y + sn * V.t2y);
         const double dz = V.lz + r * (c * V.t1z + sn * V.t2z);
@@ -175,9 +173,50 @@ __global__ void __launch_bounds__(128) reference_visibility_kernel(
     out[p] = (double)open / V.spp;
 }
 
+__global__ void unit_sphere_dirs_kernel(const uint64_t* __restrict__ keys, int64_t n, int x,
+                                        double* __restrict__ dirs) {
+    const int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (q >= n * x) return;
+    const int64_t t = q / x;
+    unit_sphere_dir(keys[t], (uint64_t)(q - t * x), dirs[3 * q], dirs[3 * q + 1], dirs[3 * q + 2]);
+}
+
+__global__ void glibc_sincos_kernel(const double* __restrict__ xs, int64_t n, double* __restrict__ s,
+                                    double* __restrict__ c) {
+    const int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (q >= n) return;
+    const double x = xs[q];
+    s[q] = gs::glibc_sin(x);
+    c[q] = gs::glibc_cos(x);
+}
+
 }  // namespace rtsdf
 
 using namespace rtsdf;
+
+extern "C" int rtsdf_unit_sphere_dirs(const uint64_t* keys, int64_t n, int x, double* dirs,
+                                      void* stream) {
+    if (n < 0 || x < 0 || (n * x > 0 && (!keys || !dirs))) {
+        set_error("unit_sphere_dirs: bad arguments");
+        return RTSDF_ERR_INVALID;
+    }
+    if (n * x == 0) return RTSDF_OK;
+    unit_sphere_dirs_kernel<<<(unsigned)((n * x + 127) / 128), 128, 0, (cudaStream_t)stream>>>(keys, n,
+                                                                                              x, dirs);
+    count_launch();
+    return check_launch("unit_sphere_dirs");
+}
+
+extern "C" int rtsdf_glibc_sincos(const double* x, int64_t n, double* s, double* c, void* stream) {
+    if (n < 0 || (n > 0 && (!x || !s || !c))) {
+        set_error("glibc_sincos: bad arguments");
+        return RTSDF_ERR_INVALID;
+    }
+    if (n == 0) return RTSDF_OK;
+    glibc_sincos_kernel<<<(unsigned)((n + 127) / 128), 128, 0, (cudaStream_t)stream>>>(x, n, s, c);
+    count_launch();
+    return check_launch("glibc_sincos");
+}
 
 extern "C" int rtsdf_exact_distance(const void* bvh_packed, int64_t n_nodes, const double* points,
                                     int64_t n, double* out, void* stream) {

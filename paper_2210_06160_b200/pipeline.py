@@ -66,23 +66,25 @@ class FrameRecord:
     """frame, durations_ns (pass -> int), masked_texels, rays_traced (pipeline.py:49-58).
 
     Device-side values are resolved lazily so advance() never has to sync.
+    Durations come from CUDA event pairs, `repeats` pairs per pass; like the
+    reference's _timed (pipeline.py:61-70) the reported value is
+    sorted(times)[len // 2].
     """
 
     def __init__(self, frame, durations, masked_dev, rays_per_texel, events=None):
         self.frame = frame
         self._durations = durations
-        self._events = events
+        self._events = events  # pass -> [(start, end), ...]
         self._masked_dev = masked_dev
         self._rays = rays_per_texel
 
     @property
     def durations_ns(self) -> dict:
         if self._events is not None:
-            ev = self._events
-            ev[-1].synchronize()
-            for i, name in enumerate(PASSES):
-                a, b = ev[i], ev[i + 1]
-                self._durations[name] = int(round(a.elapsed_time(b) * 1e6))
+            for name, pairs in self._events.items():
+                pairs[-1][1].synchronize()
+                times = sorted(int(round(a.elapsed_time(b) * 1e6)) for a, b in pairs)
+                self._durations[name] = times[len(times) // 2]
             self._events = None
         return self._durations
 
@@ -101,6 +103,28 @@ class FrameRecord:
         return sum(self.durations_ns.values())
 
 
+class _Timer:
+    """Per-pass CUDA event pairs on the current stream (no host sync)."""
+
+    def __init__(self, on: bool, repeats: int):
+        self.on = on
+        self.repeats = max(1, int(repeats)) if on else 1
+        self.events = {p: [] for p in PASSES} if on else None
+
+    def run(self, name, fn):
+        """fn(rep) for rep in range(repeats), each between its own event pair."""
+        out = None
+        for rep in range(self.repeats):
+            if self.on:
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record()
+            out = fn(rep)
+            if self.on:
+                b.record()
+                self.events[name].append((a, b))
+        return out
+
+
 class FramePipeline:
     def __init__(self, scene: Scene, config: PipelineConfig):
         self.scene = scene
@@ -117,6 +141,9 @@ class FramePipeline:
         self._prefetch = None  # (frame, JF buffer set, event) flooded ahead
         self._jf_ws = None
         self._flood_marked = {}  # id -> tensor already recorded on the flood stream
+        self._m_cap = None  # sampler workspace texel capacity (grow-only, _sample_capacity)
+        self._count_host = None
+        self._count_pending = None
         # cfg.overlap_frames (None = auto), switchable between frames: off when the caller
         # rewrites the mesh buffers every frame (frame f + 1's V is launched
         # during frame f and would read them one upload early)
@@ -192,22 +219,43 @@ class FramePipeline:
         return apply_bias(self.coarse, self.cfg.bias)
 
     # --------------------------------------------------------------- frame
-    def _coarse_pass(self, view, s, events=None):
+    def _coarse_pass(self, view, s, timer=None):
         """V (K1) + JF (K2, K3 fused) of `view` into JF buffer set s, on the
         current stream; returns the coarse SDF buffer."""
         cfg = self.cfg
+        timer = timer or _Timer(False, 1)
         js = self._jf_set(s)
         first = self._checked_view is not view
-        vox = _voxel.voxelize_seeds(view.mesh, cfg.coarse_dims, (self.scene.lo, self.scene.hi),
-                                    check=first, buffers=view.mesh_buffers(), out=js["seed_a"])
+
+        def vox(rep):
+            return _voxel.voxelize_seeds(view.mesh, cfg.coarse_dims, (self.scene.lo, self.scene.hi),
+                                         check=first and rep == 0, buffers=view.mesh_buffers(),
+                                         out=js["seed_a"])
+
+        vox_res = timer.run("V", vox)
         if first:
-            if not vox.any_occupied():
+            if not vox_res.any_occupied():
                 raise _jfa.NoSeedsError("voxel grid has no occupied cells")
             self._checked_view = view
-        if events is not None:
-            events[1].record()
-        _jfa.flood_to_sdf(js["seed_a"], js["seed_b"], js["coarse"], vox.cell_size, cfg.beta,
-                          ws=self._jf_ws)
+
+        def flood(rep):
+            if rep:  # the flood consumed seed_a: re-voxelize outside the JF timing
+                _voxel.voxelize_seeds(view.mesh, cfg.coarse_dims, (self.scene.lo, self.scene.hi),
+                                      check=False, buffers=view.mesh_buffers(), out=js["seed_a"])
+            return None
+
+        def jf(rep):
+            _jfa.flood_to_sdf(js["seed_a"], js["seed_b"], js["coarse"], vox_res.cell_size, cfg.beta,
+                              ws=self._jf_ws)
+
+        if timer.repeats > 1:
+            for rep in range(timer.repeats):
+                flood(rep)
+                sub = _Timer(True, 1)
+                sub.run("JF", jf)
+                timer.events["JF"] += sub.events["JF"]
+        else:
+            timer.run("JF", jf)
         cur = torch.cuda.current_stream()
         if cur == getattr(self, "_flood", None):
             # buffers allocated on the caller's stream and written here: the
@@ -242,9 +290,11 @@ class FramePipeline:
         queued after it and overlaps it."""
         flood = self._flood_stream()
         flood.wait_stream(torch.cuda.current_stream())
-        self._jf_set(frame % 2)  # allocated on the caller's stream (see _coarse_pass)
+        view = self.scene.view(frame)
+        view.mesh_buffers()  # allocated on the caller's stream (see _coarse_pass)
+        self._jf_set(frame % 2)
         with torch.cuda.stream(flood):
-            self._coarse_pass(self.scene.view(frame), frame % 2)
+            self._coarse_pass(view, frame % 2)
             ev = torch.cuda.Event()
             ev.record(flood)
         self._prefetch = (frame, frame % 2, ev)
@@ -262,17 +312,75 @@ class FramePipeline:
             st = self._side = torch.cuda.Stream()
         return st
 
+    def _sample_capacity(self, cb) -> int:
+        """Texel capacity of the sampler workspace, grow-only and sync-free after
+        the first frame: the masked count of earlier frames is copied to pinned
+        host memory asynchronously and read only once its event has completed
+        (never waited on).  Texels beyond the capacity are still sampled, by the
+        workspace-free tail kernel (rtsdf_sample_update), so the capacity only
+        steers speed, never the result."""
+        if self._m_cap is None:
+            self._m_cap = max(int(cb.count.item()), 1)  # frame 0: one sync
+            return self._m_cap
+        pend = self._count_pending
+        if pend is not None and pend[1].query():
+            seen = int(pend[0][0])
+            if seen > 0.9 * self._m_cap:
+                self._m_cap = int(seen * 1.25) + 1
+            self._count_pending = None
+        return self._m_cap
+
+    def _note_count(self, cb):
+        if self._count_pending is None:
+            if self._count_host is None:
+                self._count_host = torch.empty(1, dtype=torch.int64).pin_memory()
+            self._count_host.copy_(cb.count, non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record()
+            self._count_pending = (self._count_host, ev)
+
+    def _rt_pass(self, view, frame, b):
+        """RT: resample + mask + band reset (K4), compaction, fused sample + Eq. 1
+        (K6/K7); returns the new mask buffer."""
+        cfg = self.cfg
+        g = _rs._RsGeom(self.coarse, tuple(cfg.fine_dims))
+        mask_new = b["mask_b"] if self.accum.mask is b["mask_a"] else b["mask_a"]
+        cb = b["compact"]
+        _rs.launch_resample(g, cfg.sampling.mask_distance, out_unmasked=self.fine.data,
+                            mask_new=mask_new, block_counts=cb.block_counts, accum=self.accum)
+        _rs.launch_compact(mask_new, cb)
+        t_max = cfg.sampling.t_max
+        if t_max is None:
+            t_max = float(np.linalg.norm(self.coarse.hi - self.coarse.lo))
+        dirs = None
+        m_cap = None
+        if self.direction_fn is not None and cfg.sampling.rays_per_frame > 0:
+            m = int(cb.count.item())  # parity mode: the host table needs the texel list
+            idx = cb.idx[:m].cpu().numpy()
+            dirs = to_device(np.ascontiguousarray(self.direction_fn(idx, frame), dtype=np.float64))
+            m_cap = max(m, 1)
+        elif cfg.sampling.rays_per_frame > 0:
+            m_cap = self._sample_capacity(cb)
+        _rs.launch_sample_update(view.bvh, g, cb, cfg.sampling, frame, t_max, dirs=dirs,
+                                 prev=self.fine.data, accum=self.accum, out=self.fine.data,
+                                 m_cap=m_cap if m_cap is not None else 1)
+        self._note_count(cb)
+        return mask_new
+
     def advance(self, render=False, camera=None, timing=True) -> FrameRecord:
-        """Run one frame of V -> JF -> RT (-> DL when render=True)."""
+        """Run one frame of V -> JF -> RT (-> DL when render=True).
+
+        No host synchronisation after the first frame (parity mode's host
+        direction table aside).  timing=True records per-pass CUDA events,
+        `cfg.repeats` times per pass (median, as pipeline.py:61-70); RT repeats
+        run on a restored copy of the temporal state, so the result is that of
+        one frame."""
         cfg = self.cfg
         frame = self.frame
         view = self.scene.view(frame)
         b = self._buffers()
         lo, hi = self.scene.lo, self.scene.hi
-        events = None
-        if timing:
-            events = [torch.cuda.Event(enable_timing=True) for _ in range(len(PASSES) + 1)]
-            events[0].record()
+        timer = _Timer(timing, cfg.repeats)
 
         # DL's G-buffer depends only on mesh + camera: it runs on a side stream
         # while V / JF / RT occupy the main one (joined before the march)
@@ -300,6 +408,9 @@ class FramePipeline:
         if overlap and pre is not None and pre[0] == frame:
             coarse_buf = self._jf_set(pre[1])["coarse"]
         elif overlap:
+            # buffers of the first overlapped frame are allocated on the caller's
+            # stream before the flood stream touches them (see _coarse_pass)
+            view.mesh_buffers()
             flood = self._flood_stream()
             flood.wait_stream(main)
             self._jf_set(frame % 2)
@@ -310,7 +421,7 @@ class FramePipeline:
             main.wait_event(ev)
             coarse_buf = self._jf_set(frame % 2)["coarse"]
         else:
-            coarse_buf = self._coarse_pass(view, 0, events)
+            coarse_buf = self._coarse_pass(view, 0, timer)
         self.coarse = DistanceField(coarse_buf, np.asarray(lo, np.float64), np.asarray(hi, np.float64),
                                     beta=cfg.beta)
         if overlap:
@@ -319,33 +430,25 @@ class FramePipeline:
             self.fine = _rs.fine_from_coarse(self.coarse, cfg.fine_dims)
             self.accum = AccumulatorField.empty(cfg.fine_dims)
             self.accum.mask = b["mask_a"]
-        if timing:
-            events[2].record()
 
-        # RT: resample + mask + band reset (K4), compaction, fused sample + Eq. 1 (K6/K7)
-        g = _rs._RsGeom(self.coarse, tuple(cfg.fine_dims))
-        mask_new = b["mask_b"] if self.accum.mask is b["mask_a"] else b["mask_a"]
-        cb = b["compact"]
-        _rs.launch_resample(g, cfg.sampling.mask_distance, out_unmasked=self.fine.data,
-                            mask_new=mask_new, block_counts=cb.block_counts, accum=self.accum)
-        _rs.launch_compact(mask_new, cb)
-        t_max = cfg.sampling.t_max
-        if t_max is None:
-            t_max = float(np.linalg.norm(self.coarse.hi - self.coarse.lo))
-        dirs = None
-        if self.direction_fn is not None and cfg.sampling.rays_per_frame > 0:
-            m = int(cb.count.item())
-            idx = cb.idx[:m].cpu().numpy()
-            dirs = to_device(np.ascontiguousarray(self.direction_fn(idx, frame), dtype=np.float64))
-        _rs.launch_sample_update(view.bvh, g, cb, cfg.sampling, frame, t_max, dirs=dirs,
-                                 prev=self.fine.data, accum=self.accum, out=self.fine.data)
+        state = None
+        if timer.repeats > 1:  # pipeline.py:131: every repeat starts from the same state
+            acc = self.accum
+            state = [t.clone() for t in (self.fine.data, acc.min_dist, acc.front, acc.back)]
+
+        def rt(rep):
+            if rep:
+                for dst, src in zip((self.fine.data, self.accum.min_dist, self.accum.front,
+                                     self.accum.back), state):
+                    dst.copy_(src)
+            return self._rt_pass(view, frame, b)
+
+        mask_new = timer.run("RT", rt)
         self.accum.mask = mask_new
         self.accum.frames_seen += 1
         self.fine = DistanceField(self.fine.data, self.coarse.lo, self.coarse.hi,
                                   beta=self.coarse.beta, bias=self.fine.bias, frame=frame)
-        masked = cb.count.clone()
-        if timing:
-            events[3].record()
+        masked = b["compact"].count.clone()
 
         self.last_image = None
         if render:
@@ -353,17 +456,19 @@ class FramePipeline:
             # bias fused into the samples) -> compose; buffers persist per camera
             torch.cuda.current_stream().wait_event(gb_done)
             light = self.scene.light.unit()
-            _render.launch_occlusion(dl["gb"], self.fine, light, self.march_params(),
-                                     cfg.shade_draws, cfg.sampling.seed, dl["occ"],
-                                     sample_bias=cfg.bias)
-            _render.launch_compose(dl["gb"], dl["occ"], light, (0.05, 0.07, 0.10), dl["img"])
+
+            def dlp(rep):
+                _render.launch_occlusion(dl["gb"], self.fine, light, self.march_params(),
+                                         cfg.shade_draws, cfg.sampling.seed, dl["occ"],
+                                         sample_bias=cfg.bias)
+                _render.launch_compose(dl["gb"], dl["occ"], light, (0.05, 0.07, 0.10), dl["img"])
+
+            timer.run("DL", dlp)
             self.last_occlusion = dl["occ"]
             self.last_image = dl["img"]
-        if timing:
-            events[4].record()
 
         rec = FrameRecord(frame, {p: 0 for p in PASSES}, masked, cfg.sampling.rays_per_frame,
-                          events)
+                          {k: v for k, v in timer.events.items() if v} if timing else None)
         self.records.append(rec)
         self.frame += 1
         return rec

@@ -1,11 +1,12 @@
-"""Counter-based random streams (rng.py:1-53) -- host numpy form.
+"""Counter-based random streams (rng.py:1-53) -- host numpy form + device tables.
 
-The device kernels carry their own SplitMix64 (csrc/common.cuh).  This module
-is the HOST side of the north star's "host-supplied ray-direction table":
-parity runs feed the sampler directions generated here with glibc cos/sin
-(numpy == numba bit for bit), because CUDA's fp64
-sin/cos are not guaranteed to round identically to glibc.  It is also used by
-the scalar API helpers (sample_texel, soft_shadow jitter).
+The sampler generates its directions on the device: SplitMix64 plus a bit-exact
+restatement of the host glibc's cos / sin (csrc/glibc_sincos.cuh), so the
+default, benchmarked path draws exactly the reference's directions.  This
+module is the host side: the north star's "host-supplied ray-direction table"
+(numpy == numba bit for bit), the scalar API helpers
+(sample_texel, soft_shadow jitter) and `device_direction_table`, which runs the
+sampler's own direction code for a list of texels.
 """
 
 from __future__ import annotations
@@ -59,4 +60,20 @@ def direction_table(seed: int, texel_index, frame: int, x: int) -> np.ndarray:
     return np.ascontiguousarray(np.stack([dx, dy, dz], axis=-1))
 
 
-__all__ = ["mix64", "stream_key", "uniform", "unit_sphere_dir", "direction_table"]
+def device_direction_table(seed: int, texel_index, frame: int, x: int) -> np.ndarray:
+    """direction_table computed by the device kernels' code path (rtsdf_unit_sphere_dirs)."""
+    import torch
+
+    from . import _lib
+    from ._device import to_device
+
+    idx = np.asarray(texel_index, dtype=np.int64).reshape(-1)
+    keys = to_device(stream_key(seed, idx, frame).astype(np.uint64).view(np.int64))
+    out = torch.empty((len(idx), int(x), 3), dtype=torch.float64, device=keys.device)
+    _lib.check(_lib.lib().rtsdf_unit_sphere_dirs(_lib.ptr(keys), len(idx), int(x), _lib.ptr(out),
+                                                 _lib.stream()), "unit_sphere_dirs")
+    return out.cpu().numpy()
+
+
+__all__ = ["mix64", "stream_key", "uniform", "unit_sphere_dir", "direction_table",
+           "device_direction_table"]

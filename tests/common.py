@@ -30,7 +30,18 @@ def golden_arrays():
         return {k: z[k] for k in z.files}
 
 
-def scene_mesh(name):
+@lru_cache(maxsize=1)
+def golden_large() -> dict:
+    return json.loads((GOLDEN / "golden_large.json").read_text())
+
+
+@lru_cache(maxsize=1)
+def golden_large_arrays():
+    with np.load(GOLDEN / "golden_large.npz") as z:
+        return {k: z[k] for k in z.files}
+
+
+def scene_mesh(name, frame=0):
     """(scene, merged world mesh) built by the product's host-side scene code."""
     from paper_2210_06160_b200 import scenes
     from paper_2210_06160_b200.geometry import make_mesh
@@ -38,7 +49,7 @@ def scene_mesh(name):
     scene = scenes.get_scene(name)
     verts, tris, base = [], [], 0
     for inst in scene.instances:
-        m = inst.transform_at(0)
+        m = inst.transform_at(frame)
         v = inst.mesh.vertices @ m[:, :3].T + m[:, 3]
         verts.append(v)
         tris.append(inst.mesh.triangles + base)

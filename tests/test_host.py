@@ -9,7 +9,7 @@ from pathlib import Path
 import numpy as np
 import pytest
 
-from common import digest, golden, golden_arrays, scene_mesh
+from common import digest, golden, golden_arrays, golden_large, golden_large_arrays, scene_mesh
 
 ROOT = Path(__file__).resolve().parent.parent
 
@@ -78,6 +78,45 @@ def test_scene_meshes_match_reference(name, key):
     assert mesh.num_triangles == g["n_tris"]
     for k in ("vertices", "triangles", "normals"):
         assert digest(getattr(mesh, k)) == g[k], k
+
+
+def test_orbit_scene_is_the_references_blob_orbit():
+    """the orbit scene's occluder is the vendored blob.obj and its
+    per-frame merged meshes equal the reference's (tests/golden/make_golden_large.py)."""
+    from paper_2210_06160_b200 import scenes
+
+    G = golden_large()
+    blob = scenes.load_blob_mesh()
+    assert blob.num_triangles == G["orbit.blob"]["n_tris"] == 1024
+    assert digest(blob.vertices) == G["orbit.blob"]["vertices"]
+    assert digest(blob.triangles) == G["orbit.blob"]["triangles"]
+    for f in range(3):
+        _, mesh = scene_mesh("orbit", f)
+        for k in ("vertices", "triangles", "normals"):
+            assert digest(getattr(mesh, k)) == G[f"orbit.mesh{f}"][k], (f, k)
+
+
+def test_rsdf_writer_bytes_match_reference(tmp_path):
+    """field.save_field writes the reference's RSDF v1 bytes exactly (header
+    <4sI3I6fffQ + x-fastest f32 payload, field.py:190-201); the reader side of
+    the reference-written file is a GPU test (load_field returns a device field)."""
+    import torch
+
+    from paper_2210_06160_b200 import field as F
+
+    G, A = golden_large(), golden_large_arrays()
+    data = A["rsdf.data"]
+    fld = F.DistanceField(torch.from_numpy(data.copy()), np.array([-1.0, -0.5, -2.0]),
+                          np.array([1.0, 0.75, 0.5]), beta=0.125, bias=0.01, frame=5)
+    p = tmp_path / "ours.rsdf"
+    F.save_field(fld, p)
+    raw = p.read_bytes()
+    assert len(raw) == G["rsdf"]["size"]
+    assert raw == A["rsdf.bytes"].tobytes()
+    # x-fastest payload: the first nx floats are data[:, 0, 0]
+    hdr = len(raw) - data.size * 4
+    np.testing.assert_array_equal(np.frombuffer(raw[hdr:hdr + 4 * data.shape[0]], np.float32),
+                                  data[:, 0, 0])
 
 
 def test_integer_weights_exact():
