@@ -13,8 +13,11 @@ frame split over the N GPUs, NCCL P2P halo planes per JFA pass, fine slabs
 gathered on rank 0 for the shading; "scaling": "strong"), value = max-over-
 ranks time / frames; --replicas runs N independent frames instead ("weak").
 --impl reference times the reference algorithm's CPU implementation (the
-oracle port in oracle/, OpenMP over all host cores) on a bounded sample of
-the same frame per step.
+oracle port in oracle/, OpenMP over all host cores): every step is one whole
+C3 frame with the temporal state carried over, nothing sampled or
+extrapolated.  With WORLD_SIZE unset, --gpus N > 1 re-launches itself under
+torch.distributed.run with N ranks (127.0.0.1); under torchrun WORLD_SIZE
+must equal --gpus.
 """
 
 from __future__ import annotations
@@ -47,7 +50,9 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--rays", type=int, default=32)
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
-    ap.add_argument("--parts", type=int, default=8, help="reference arm: sample = 1/parts")
+    ap.add_argument("--cpu-frames", type=int, default=3,
+                    help="cpu_baseline: full C3 frames timed (after one warm-up frame)")
+    ap.add_argument("--cpu-baseline-only", action="store_true", help=argparse.SUPPRESS)
     ap.add_argument("--replicas", action="store_true",
                     help="N > 1: N independent frames instead of the z-slab sharded frame")
     ap.add_argument("--sharded", action="store_true",
@@ -330,21 +335,22 @@ def run_ours(args, rank, world, local_rank):
 
     kernels_ms = {"jfa_pass_total": jfa_ms, "sample_update": sample_ms}
     traffic_b, traffic_src = jfa_traffic()
-    dominant = "sample_update" if sample_ms > jfa_ms / len(offs) else "jfa_step"
+    dominant = "sample_update" if sample_ms > jfa_ms else "jfa_pass (schedule)"
     out = {
         "metric": METRIC, "value": round(value, 4), "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": round(ms_per_step, 4),
         "higher_is_better": False, "scaling": "strong" if sharded else "weak", "vs_baseline": None,
         "dtype": "f64+i32",
         "data": "synthetic: reference-identical procedural sphere_plane scene (1,282 triangles)",
-        "config": dict(workload(args.rays),
-                       parallelism=(f"z-slab x{world} (NCCL P2P halos per JFA pass, coarse 1-plane "
-                                    "halo, fine slabs gathered for DL)") if sharded else
-                       (f"replicas x{world}" if world > 1 else "1 GPU"),
-                       frame_overlap=(None if sharded else
-                                      "V + JF of frame f+1 on a flood stream during frame f's RT/DL "
-                                      "(static scene, BVH <= 16 MB, double-buffered); frame_stages_ms come from one "
-                                      "serial event-timed frame; off for e2e, whose every frame uploads its mesh")),
+        "config": workload(args.rays),
+        "layout": {"parallelism": (f"z-slab x{world} (NCCL P2P halos per JFA pass, coarse 1-plane "
+                                   "halo, fine slabs gathered for DL)") if sharded else
+                   (f"replicas x{world}" if world > 1 else "1 GPU"),
+                   "frame_overlap": (None if sharded else
+                                     "V + JF of frame f+1 on a flood stream during frame f's RT/DL "
+                                     "(static scene, BVH <= 16 MB, double-buffered); frame_stages_ms "
+                                     "come from one serial event-timed frame; off for e2e, whose every "
+                                     "frame uploads its mesh")},
         "frame_stages_ms": {k: round(v, 4) for k, v in stages_ms.items()},
         "masked_texels": masked, "rays_per_frame": rays,
         "rays_per_s": round(rays / (sample_ms * 1e-3), 1),
@@ -374,8 +380,8 @@ def run_ours(args, rank, world, local_rank):
     return out
 
 
-def cpu_full_frame():
-    """One full C3 frame on the CPU oracle (OpenMP, all host cores): V+JF+RT+DL."""
+def cpu_runner(x):
+    """The CPU oracle (OpenMP over every host core) set up for full C3 frames."""
     sys.path.insert(0, str(ROOT / "oracle"))
     import oracle as O
 
@@ -390,60 +396,87 @@ def cpu_full_frame():
         alb.append(np.tile(np.asarray(inst.albedo, np.float32), (inst.mesh.num_triangles, 1)))
         base += len(inst.mesh.vertices)
     mesh = make_mesh(np.vstack(verts), np.vstack(tris))
-    return O, scene, mesh, np.vstack(alb)
+    return O.CpuFrameRunner(mesh, np.vstack(alb), scene.bounds, DIMS, scene.camera,
+                            scene.light.unit(), scene.light.angular_radius, x=x)
 
 
-def run_cpu_baseline():
-    O, scene, mesh, alb = cpu_full_frame()
-    t0 = time.perf_counter()
-    H = O.HybridOracle(mesh.vertices, mesh.triangles, mesh.normals, scene.bounds, DIMS, DIMS, x=32)
-    t_bvh = time.perf_counter()
-    H.advance()
-    cam = scene.camera
-    pos, fwd, right, up = cam.basis()
-    half_h = math.tan(math.radians(cam.vfov_deg) * 0.5)
-    gp, gn, _, gc = O.gbuffer(H.bvh, mesh.normals, alb, pos, fwd, right, up,
-                              half_h * cam.width / cam.height, half_h, cam.width, cam.height)
-    hf = (scene.hi - scene.lo) / np.array(DIMS, dtype=np.float64)
-    eps = float(max(hf))
-    O.occlusion(H.fine - np.float32(0.01), scene.lo, hf, gp, gn, gc, scene.light.unit(), eps, 256,
-                0.05, float(np.linalg.norm(scene.hi - scene.lo)),
-                1 / math.tan(scene.light.angular_radius), 1.0, 2 * eps + 0.01, 1, 0)
-    t1 = time.perf_counter()
-    return {"value": round((t1 - t_bvh) * 1e3, 1), "unit": UNIT, "cores": O.num_threads(),
+def run_cpu_baseline(args):
+    """cpu_baseline: one warm-up + --cpu-frames whole C3 frames on the oracle
+    (~3 s each on 16 host threads), median ms/frame."""
+    R = cpu_runner(args.rays)
+    R.step()
+    ts = [R.step() * 1e3 for _ in range(max(1, args.cpu_frames))]
+    return {"value": round(float(np.median(ts)), 1), "unit": UNIT, "cores": R.threads,
             "kind": "port",
-            "sample": "1 full C3 frame (V + 9-pass JFA + s2sdf + resample/mask + 76.7 M rays + "
-                      "Eq.1 + G-buffer + 240x180 march) on the C oracle, OpenMP; BVH build excluded"}
+            "sample": f"{len(ts)} whole C3 frames after 1 warm-up frame (V + 9-pass JFA + s2sdf + "
+                      "resample/mask + 76.7 M rays + Eq.1 + G-buffer + 240x180 march, temporal "
+                      "state carried), median; C oracle, OpenMP; BVH built once (static scene)"}
+
+
+def cpu_baseline_subprocess(args):
+    """The cpu_baseline leg in its own process (no GPU state, no allocator
+    pressure on the timed GPU process)."""
+    cmd = [sys.executable, str(Path(__file__).resolve()), "--cpu-baseline-only",
+           "--rays", str(args.rays), "--cpu-frames", str(args.cpu_frames)]
+    env = {k: v for k, v in os.environ.items()
+           if k not in ("RANK", "LOCAL_RANK", "WORLD_SIZE", "MASTER_ADDR", "MASTER_PORT")}
+    r = subprocess.run(cmd, capture_output=True, text=True, env=env)
+    for ln in reversed(r.stdout.splitlines()):
+        if ln.startswith("{"):
+            return json.loads(ln)
+    return {"value": None, "unit": UNIT, "kind": "port", "error": (r.stderr or "")[-400:]}
 
 
 # ------------------------------------------------------------ reference arm
 def run_reference(args):
-    O, scene, mesh, alb = cpu_full_frame()
-    sampler = O.CpuFrameSampler(mesh, alb, scene.bounds, DIMS, scene.camera, scene.light.unit(),
-                                scene.light.angular_radius, x=args.rays, parts=args.parts)
-    for s in range(args.warmup):
-        sampler.step(s)
-    est = [sampler.step(args.warmup + s) for s in range(args.steps)]
-    value = float(np.mean(est)) * 1e3
-    cpu = {"value": round(value, 1), "unit": UNIT, "cores": sampler.threads, "kind": "port",
-           "sample": f"per step: full voxelize/s2sdf/resample/Eq.1/G-buffer + 1/{args.parts} of every "
-                     "JFA pass's planes, of the masked texels' rays and of the shadow rows "
-                     f"(rotating), extrapolated x{args.parts}"}
+    """The reference's CPU implementation of the path on this box's host cores:
+    every step is one whole C3 frame (nothing sampled, nothing extrapolated)."""
+    R = cpu_runner(args.rays)
+    for _ in range(args.warmup):
+        R.step()
+    t0 = time.perf_counter()
+    ts = [R.step() for _ in range(args.steps)]
+    wall = time.perf_counter() - t0
+    value = float(np.mean(ts)) * 1e3
+    cpu = {"value": round(value, 1), "unit": UNIT, "cores": R.threads, "kind": "port",
+           "sample": f"{args.steps} whole C3 frames after {args.warmup} warm-up frames (V + 9-pass "
+                     "JFA + s2sdf + resample/mask + 76.7 M rays + Eq.1 + G-buffer + 240x180 march, "
+                     "temporal state carried); C oracle, OpenMP; BVH built once (static scene)"}
     return {"impl": "reference", "metric": METRIC, "value": round(value, 1), "unit": UNIT,
             "n_gpus": 0, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": round(value, 1), "higher_is_better": False, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f64+i32", "data": "synthetic",
-            "config": dict(workload(args.rays), parallelism=f"{sampler.threads} host threads"),
-            "cpu_baseline": cpu,
+            "vs_baseline": None, "dtype": "f64+i32",
+            "data": "synthetic: reference-identical procedural sphere_plane scene (1,282 triangles)",
+            "config": workload(args.rays), "layout": f"{R.threads} host threads",
+            "timed_wall_s": round(wall, 2), "cpu_baseline": cpu,
             "e2e": {"value": round(value, 1), "unit": UNIT, "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
 
 
+def _free_port():
+    import socket
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
 def main():
     args = parse()
+    if args.cpu_baseline_only:
+        print(json.dumps(run_cpu_baseline(args)), flush=True)
+        return
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        # one process per GPU: re-launch under torchrun ourselves
+        os.execv(sys.executable, [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+                                  f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+                                  f"--master-port={_free_port()}", str(Path(__file__).resolve()),
+                                  *sys.argv[1:]])
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
     if args.impl == "reference":
         if rank == 0:
             print(json.dumps(run_reference(args)), flush=True)
@@ -458,7 +491,7 @@ def main():
     out = run_ours(args, rank, world, local_rank)
     if rank == 0:
         if world == 1 and not args.no_cpu:
-            out["cpu_baseline"] = run_cpu_baseline()
+            out["cpu_baseline"] = cpu_baseline_subprocess(args)
         print(json.dumps(out), flush=True)
     if group:
         import torch.distributed as tdist

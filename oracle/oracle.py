@@ -417,45 +417,28 @@ def jfa_step_range(src, dst, offset, h, i0, i1):
                                 float(h[1]), float(h[2]), int(i0), int(i1))
 
 
-class CpuFrameSampler:
-    """Bounded-sample timing of one hybrid frame (V+JF+RT+DL) on the CPU oracle.
-
-    bench.py's cpu_baseline / --impl reference leg.  Setup (untimed) runs one
-    full frame to capture each JFA pass's true input, the masked texel list,
-    the per-texel ray results and the G-buffer.  step(s) then times the cheap
-    full-grid stages in full (voxelize, seeds->SDF, resample+mask, Eq. 1
-    update, G-buffer) and chunk s of `parts` of the expensive ones (every JFA
-    pass over 1/parts of the planes, ray sampling over 1/parts of the masked
-    texels, the shadow march over 1/parts of the rows), and returns the
-    full-frame estimate  t_full_stages + parts * t_chunk.
-    """
+class CpuFrameRunner:
+    """Whole C3-style frames on the CPU oracle, timed end to end: the
+    reference arm / cpu_baseline of bench.py.  Each step is one complete
+    FramePipeline.advance(render=True) (pipeline.py:109-160): voxelize, the
+    full JFA schedule, seeds -> SDF, resample + mask, every masked texel's x
+    rays, the Eq. 1 update with the temporal state carried frame to frame,
+    the G-buffer and the soft-shadow march -- no sampling, no extrapolation.
+    The BVH of the static scene is built once, as the reference's memoised
+    SceneView does (scenes.py:56-63)."""
 
     def __init__(self, mesh, albedo, bounds, dims, camera, light_unit, light_angle, x=32, d=0.1,
-                 alpha=0.95, bias=0.01, parts=8):
+                 alpha=0.95, bias=0.01):
         import math
-        import time
 
         self.mesh, self.albedo = mesh, np.ascontiguousarray(albedo, np.float32)
         self.lo = np.asarray(bounds[0], np.float64)
         self.hi = np.asarray(bounds[1], np.float64)
         self.dims = tuple(dims)
-        self.x, self.d, self.alpha, self.bias, self.parts = x, d, alpha, bias, parts
+        self.bias = bias
         self.h = (self.hi - self.lo) / np.array(dims, dtype=np.float64)
-        t0 = time.perf_counter()
-        self.bvh = bvh_build(mesh.vertices, mesh.triangles, mesh.normals)
-        occ = voxelize(mesh.vertices, mesh.triangles, dims, (self.lo, self.hi))
-        seed = jfa_init(occ)
-        self.pass_inputs = []
-        for off in jfa_offsets(dims):
-            self.pass_inputs.append((off, seed))
-            seed = jfa_step(seed, off, self.h)
-        self.seeds = seed
-        self.coarse = seeds_to_sdf(seed, self.h)
-        self.fine0 = resample_mask(self.coarse, self.lo, self.hi, dims, np.inf)[0]
-        _, mask = resample_mask(self.coarse, self.lo, self.hi, dims, d)
-        self.idx = np.flatnonzero(mask.ravel()).astype(np.int64)
-        self.t_max = float(np.linalg.norm(self.hi - self.lo))
-        self.samp = sample_masked(self.bvh, self.idx, self.lo, self.h, dims, x, 0, 0, self.t_max)
+        self.H = HybridOracle(mesh.vertices, mesh.triangles, mesh.normals, bounds, dims, dims, x=x,
+                              d=d, alpha=alpha)
         pos, fwd, right, up = camera.basis()
         half_h = math.tan(math.radians(camera.vfov_deg) * 0.5)
         self.cam = (pos, fwd, right, up, half_h * camera.width / camera.height, half_h,
@@ -463,55 +446,17 @@ class CpuFrameSampler:
         self.light = np.asarray(light_unit, np.float64)
         self.k = 1.0 / math.tan(light_angle)
         self.eps = float(max(self.h))
-        self.gb = gbuffer(self.bvh, mesh.normals, self.albedo, *self.cam)
-        self.setup_seconds = time.perf_counter() - t0
+        self.t_max = float(np.linalg.norm(self.hi - self.lo))
         self.threads = num_threads()
 
-    def step(self, s: int) -> float:
+    def step(self) -> float:
+        """One full frame; returns its wall time in seconds."""
         import time
 
-        P = self.parts
-        s %= P
-        nx = self.dims[0]
-        i0, i1 = nx * s // P, nx * (s + 1) // P
-        M = len(self.idx)
-        n0, n1 = M * s // P, M * (s + 1) // P
-        H = self.cam[7]
-        r0, r1 = H * s // P, H * (s + 1) // P
-        mesh = self.mesh
-        t_full = t_chunk = 0.0
         t = time.perf_counter()
-        voxelize(mesh.vertices, mesh.triangles, self.dims, (self.lo, self.hi))       # V
-        t_full += time.perf_counter() - t
-        t = time.perf_counter()
-        for off, src in self.pass_inputs:                                             # JF passes
-            dst = np.empty_like(src)
-            jfa_step_range(src, dst, off, self.h, i0, i1)
-        t_chunk += time.perf_counter() - t
-        t = time.perf_counter()
-        seeds_to_sdf(self.seeds, self.h)                                              # JF s2sdf
-        resample_mask(self.coarse, self.lo, self.hi, self.dims, self.d)               # RT mask
-        t_full += time.perf_counter() - t
-        t = time.perf_counter()
-        sample_masked(self.bvh, self.idx[n0:n1], self.lo, self.h, self.dims, self.x, 0, 0,
-                      self.t_max)                                                     # RT rays
-        t_chunk += time.perf_counter() - t
-        t = time.perf_counter()
-        acc = empty_accum(self.dims)
-        out = self.fine0.copy()
-        mo = np.zeros(self.dims, np.uint8)
-        mn = np.zeros(self.dims, np.uint8)
-        mn.ravel()[self.idx] = 1
-        lib().oracle_update_fine(_p(self.fine0), _p(self.fine0), _p(mo), _p(mn), out.size,
-                                 _p(acc["min_dist"]), _p(acc["front"]), _p(acc["back"]),
-                                 _p(self.idx), M, _p(self.samp[0]), _p(self.samp[1]),
-                                 _p(self.samp[2]), float(self.alpha), _p(out))        # RT Eq. 1
-        gbuffer(self.bvh, mesh.normals, self.albedo, *self.cam)                       # DL G-buffer
-        t_full += time.perf_counter() - t
-        t = time.perf_counter()
-        gp, gn, _, gc = self.gb
-        occlusion(out - np.float32(self.bias), self.lo, self.h, gp[r0:r1], gn[r0:r1], gc[r0:r1],
-                  self.light, self.eps, 256, 0.05, self.t_max, self.k, 1.0,
-                  2 * self.eps + self.bias, 1, 0)                                     # DL march
-        t_chunk += time.perf_counter() - t
-        return t_full + P * t_chunk
+        self.H.advance()
+        gp, gn, _, gc = gbuffer(self.H.bvh, self.mesh.normals, self.albedo, *self.cam)
+        self.occ = occlusion(self.H.fine - np.float32(self.bias), self.lo, self.h, gp, gn, gc,
+                             self.light, self.eps, 256, 0.05, self.t_max, self.k, 1.0,
+                             2 * self.eps + self.bias, 1, 0)
+        return time.perf_counter() - t

@@ -153,9 +153,12 @@ __device__ __forceinline__ void unit_sphere_dir(uint64_t key, uint64_t counter, 
     double r = __dsqrt_rn(dmax_(0.0, __dsub_rn(1.0, __dmul_rn(z, z))));
     double phi = __dmul_rn(6.283185307179586, v);
     // rng.py:53 calls the host libm's cos / sin: its glibc FMA build, restated
-    // bit for bit in glibc_sincos.cuh (CUDA's sincos differs in the last ulp)
-    dx = __dmul_rn(r, gs::glibc_cos(phi));
-    dy = __dmul_rn(r, gs::glibc_sin(phi));
+    // bit for bit in glibc_sincos.cuh (CUDA's sincos differs in the last ulp);
+    // the straight-line pair form keeps a warp's random phis on one path
+    double s, c;
+    gs::glibc_sincos_nb(phi, s, c);
+    dx = __dmul_rn(r, c);
+    dy = __dmul_rn(r, s);
     dz = z;
 }
 

@@ -204,5 +204,71 @@ GS_HD double glibc_cos(double x) {
     return from_bits(0x7ff8000000000000ull);
 }
 
+// ---------------------------------------------------------------------------
+// (sin x, cos x) for 0 <= x < 105414350 as ONE straight-line evaluation with
+// no data-dependent branch -- the form the sampler uses for phi = 2 pi v.
+// glibc picks a different formula per range of x (and per quadrant n after
+// reduction), so 32 random directions in a warp would run up to six paths one
+// after another.  Every pair (sin, cos) is however exactly one do_sin(A, DA)
+// and one do_cos(B, DB) on per-range arguments:
+//   |x| < 0.855469:   sin = do_sin(x, 0)             cos = do_cos(x, 0)
+//   |x| < 2.426265:   sin = |do_cos(hp0 - x, hp1)|    cos = do_sin(a, da)  (a + da = hp0 - x)
+//   otherwise:        x = n pi/2 + (a + da); {do_sin(a, da), do_cos(a, da)}
+//                     placed and negated by n (do_sincos(., n) / (., n + 1))
+// plus glibc's tiny-argument returns (sin = x below 2^-26, cos = 1 below
+// 2^-27).  The arguments are chosen by selects, TAYLOR_SIN and the table path
+// of do_sin are both evaluated and selected, and every operation is the one
+// glibc_sin / glibc_cos perform on that input -- so the results are bit-
+// identical to them (tests/test_glibc_sincos.py checks it on both sides of
+// every range boundary).
+GS_HD double sel(bool p, double a, double b) { return p ? a : b; }
+
+GS_HD double do_sin_nb(double x, double dx) {
+    const double xold = x;
+    const double tay = taylor_sin(x, dx);
+    const double d2 = (x <= 0.0) ? gneg(dx) : dx;
+    const double ax = gabs(x);
+    const double u = GS_ADD(ax, GS_BIG);
+    const int k = (int)((uint32_t)bits(u) << 2) & 511;  // the taylor lanes index anything: keep in range
+    const double xr = GS_SUB(ax, GS_SUB(u, GS_BIG));
+    const double xx = GS_MUL(xr, xr);
+    const double s = GS_ADD(xr, GS_FMA(GS_MUL(xr, xx), GS_FMA(xx, GS_SN5, GS_SN3), d2));
+    const double c = GS_FMA(xr, d2, GS_MUL(xx, GS_FMA(xx, GS_FMA(xx, GS_CS6, GS_CS4), GS_CS2)));
+    const int kk = k < RTSDF_GS_TABLE_N - 3 ? k : 0;
+    const double sn = tab(kk), ssn = tab(kk + 1), cs = tab(kk + 2), ccs = tab(kk + 3);
+    const double cor = GS_FMA(s, cs, GS_FMA(gneg(c), sn, GS_FMA(s, ccs, ssn)));
+    const double tab_r = gcopysign(GS_ADD(sn, cor), xold);
+    return sel(ax < 0.126, tay, tab_r);
+}
+
+GS_HD void glibc_sincos_nb(double x, double& sn_out, double& cs_out) {
+    const uint32_t kx = (uint32_t)(bits(x) >> 32) & 0x7fffffffu;
+    const bool r1 = kx < 0x3feb6000u, r2 = !r1 && kx < 0x400368fdu, r3 = !r1 && !r2;
+    // range 2 arguments
+    const double y = GS_SUB(GS_HP0, gabs(x));
+    const double a2 = GS_ADD(y, GS_HP1);
+    const double da2 = GS_ADD(GS_SUB(y, a2), GS_HP1);
+    // range 3 reduction (harmless on the other lanes)
+    double a3, da3;
+    const int n = reduce_sincos(x, a3, da3);
+    const double sa = sel(r1, x, sel(r2, a2, a3)), sda = sel(r1, 0.0, sel(r2, da2, da3));
+    const double ca = sel(r1, x, sel(r2, y, a3)), cda = sel(r1, 0.0, sel(r2, GS_HP1, da3));
+    const double S = do_sin_nb(sa, sda);
+    const double Cc = do_cos(ca, cda);
+    // range 3 placement: sin = do_sincos(n), cos = do_sincos(n + 1)
+    const int m = n + 1;
+    double s3 = (n & 1) ? Cc : S;
+    s3 = (n & 2) ? gneg(s3) : s3;
+    double c3 = (m & 1) ? Cc : S;
+    c3 = (m & 2) ? gneg(c3) : c3;
+    double so = sel(r1, S, sel(r2, gcopysign(Cc, x), s3));
+    double co = sel(r1, Cc, sel(r2, S, c3));
+    so = sel(kx < 0x3e500000u, x, so);
+    co = sel(kx < 0x3e400000u, 1.0, co);
+    (void)r3;
+    sn_out = so;
+    cs_out = co;
+}
+
 }  // namespace gs
 }  // namespace rtsdf

@@ -107,3 +107,38 @@ def test_thresholds_and_table_knots(host_gs):
 def test_outside_restated_range_is_nan(host_gs):
     s, c = host_gs(np.array([2.0e8, -3.0e9, np.inf]))
     assert np.isnan(s).all() and np.isnan(c).all()
+
+
+SRC_NB = r"""
+#include "glibc_sincos.cuh"
+extern "C" void gs_nb_many(const double* x, long n, double* s, double* c) {
+    for (long i = 0; i < n; ++i) rtsdf::gs::glibc_sincos_nb(x[i], s[i], c[i]);
+}
+"""
+
+
+def test_branch_free_pair_equals_glibc(tmp_path):
+    """glibc_sincos_nb (the sampler's straight-line (sin, cos)) == libm sin, cos
+    for every non-negative argument form it is used on."""
+    (tmp_path / "nb.cpp").write_text(SRC_NB)
+    so = tmp_path / "libnb.so"
+    subprocess.run(["g++", "-O2", "-ffp-contract=off", "-fno-fast-math", "-std=c++17", "-shared",
+                    "-fPIC", "-I", str(ROOT / "paper_2210_06160_b200" / "csrc"), "-o", str(so),
+                    str(tmp_path / "nb.cpp"), "-lm"], check=True)
+    lib = C.CDLL(str(so))
+    lib.gs_nb_many.argtypes = [C.c_void_p, C.c_long, C.c_void_p, C.c_void_p]
+    rng = np.random.default_rng(3)
+    k = rng.integers(0, 2**53, size=1 << 22, dtype=np.uint64)
+    parts = [6.283185307179586 * (k.astype(np.float64) * (1.0 / 9007199254740992.0)),
+             np.ldexp(1.0 + rng.random(1 << 18), rng.integers(-60, 27, size=1 << 18)),
+             np.array([0.0, 5e-324, 2.0**-1074 * 7])]
+    for t in [2.0**-26, 2.0**-27, 0.126, 0.855469, 2.426265, np.pi / 2, np.pi, 2 * np.pi] + \
+            [(q + 0.5) / 128 for q in range(110)]:
+        parts.append((np.float64(t).view(np.int64) + np.arange(-2048, 2048)).view(np.float64))
+    x = np.concatenate(parts)
+    x = x[(x >= 0) & (x < 105414350.0)]
+    s, c = np.empty_like(x), np.empty_like(x)
+    lib.gs_nb_many(x.ctypes.data, x.size, s.ctypes.data, c.ctypes.data)
+    ws, wc = O.libm_sincos(x)
+    np.testing.assert_array_equal(s.view(np.uint64), ws.view(np.uint64))
+    np.testing.assert_array_equal(c.view(np.uint64), wc.view(np.uint64))
