@@ -471,7 +471,7 @@ __global__ void linear_to_packed_kernel(const int32_t* __restrict__ l, int32_t* 
 }  // namespace rtsdf
 
 #include "jfa2.cuh"
-#include "jfa3.cuh"
+#include "jfa4.cuh"
 
 namespace rtsdf {
 
@@ -545,9 +545,6 @@ static void launch_pass2(PlaneSrc s, int32_t* dst, float* dst_sdf, const JfaGeom
     cudaMemsetAsync(fix.count, 0, sizeof(int64_t), st);
     int64_t warps = (int64_t)T.nzb * T.jres * T.jgroups * T.ires * T.isegs;
     unsigned blocks = (unsigned)((warps + 3) / 4);
-    // v3 (select-free 5-key pass, jfa3.cuh) is exact but measured slower than
-    // v2 on B200 (more instructions, 159 registers): opt-in only
-    static const bool v3_on = getenv("RTSDF_JFA_V3") != nullptr;
     if (g.exact) {  // ties resolve inside the pass: no flags, no fix-up
         if (ry == 4)
             nat ? jfa_pass2_kernel<4, FINAL, SLAB, true, true><<<blocks, 128, 0, st>>>(s, dst, dst_sdf, g, T, beta, empty_count, fix)
@@ -559,14 +556,7 @@ static void launch_pass2(PlaneSrc s, int32_t* dst, float* dst_sdf, const JfaGeom
         count_launch(1);
         return;
     }
-    if (v3_on && jfa3_ok(g)) {
-        if (ry == 4)
-            jfa_pass3_kernel<4, FINAL, SLAB><<<blocks, 128, 0, st>>>(s, dst, dst_sdf, g, T, beta, empty_count, fix);
-        else if (ry == 2)
-            jfa_pass3_kernel<2, FINAL, SLAB><<<blocks, 128, 0, st>>>(s, dst, dst_sdf, g, T, beta, empty_count, fix);
-        else
-            jfa_pass3_kernel<1, FINAL, SLAB><<<blocks, 128, 0, st>>>(s, dst, dst_sdf, g, T, beta, empty_count, fix);
-    } else if (ry == 4)
+    if (ry == 4)
         nat ? jfa_pass2_kernel<4, FINAL, SLAB, false, true><<<blocks, 128, 0, st>>>(s, dst, dst_sdf, g, T, beta, empty_count, fix)
             : jfa_pass2_kernel<4, FINAL, SLAB, false><<<blocks, 128, 0, st>>>(s, dst, dst_sdf, g, T, beta, empty_count, fix);
     else if (ry == 2)
@@ -577,6 +567,67 @@ static void launch_pass2(PlaneSrc s, int32_t* dst, float* dst_sdf, const JfaGeom
         s, dst, dst_sdf, g, beta, fix, make_fastdiv((uint32_t)g.nz), make_fastdiv((uint32_t)g.ny));
     count_launch(2);
 }
+
+// K2 v4 launch (INT mode): residue-chain tiles, integer ties resolved in the kernel.
+template <bool FINAL, bool SLAB>
+static void launch_pass4(PlaneSrc s, int32_t* dst, float* dst_sdf, const JfaGeom& g, double beta,
+                         int64_t* empty_count, void* ws, cudaStream_t st) {
+    const int k = g.offset;
+    const int chain_y = (g.ny + k - 1) / k;
+    const int ry = chain_y >= 4 ? 4 : (chain_y >= 2 ? 2 : 1);
+    const bool nat = natural_empty_ok(g);
+    Jfa4Task T;
+    T.one = 1;
+    T.zero = 0;
+    T.skip = k >= 16;
+    T.nz_pos = g.nz;
+    T.single = g.nz <= 32;
+    T.zw = T.single ? 1 : (g.nz + 29) / 30;
+    T.lc = (g.nz + k - 1) / k;
+    T.nlong = g.nz - k * (T.lc - 1);  // residues with lc positions (k >= nz: every z, lc = 1)
+    if (T.nlong > k) T.nlong = k;
+    T.jres = k < g.ny ? k : g.ny;
+    T.jgroups = (chain_y + ry - 1) / ry;
+    T.ires = k < g.nxl ? k : g.nxl;
+    const int chain_x = (g.nxl + k - 1) / k;
+    // segment length L: 2 halo planes per L outputs; halve while the grid
+    // would not fill the GPU for two waves (~16 resident warps / SM)
+    T.L = 24;
+    const int64_t want = (int64_t)num_sms() * 16 * 2;
+    while (T.L > 4 && (int64_t)T.zw * T.jres * T.jgroups * T.ires * ((chain_x + T.L - 1) / T.L) < want)
+        T.L /= 2;
+    T.isegs = (chain_x + T.L - 1) / T.L;
+    const int64_t warps = (int64_t)T.zw * T.jres * T.jgroups * T.ires * T.isegs;
+    const unsigned blocks = (unsigned)((warps + 3) / 4);
+    JfaFixList fix = fix_list(ws, (int64_t)g.nxl * g.ny * g.nz);
+    if (!g.exact) cudaMemsetAsync(fix.count, 0, sizeof(int64_t), st);
+#define RTSDF_P4(RYV, EX, NA) \
+    jfa_pass4_kernel<RYV, FINAL, SLAB, EX, NA><<<blocks, 128, 0, st>>>(s, dst, dst_sdf, g, T, beta, empty_count, fix)
+    if (g.exact) {
+        if (ry == 4) { if (nat) RTSDF_P4(4, true, true); else RTSDF_P4(4, true, false); }
+        else if (ry == 2) { if (nat) RTSDF_P4(2, true, true); else RTSDF_P4(2, true, false); }
+        else { if (nat) RTSDF_P4(1, true, true); else RTSDF_P4(1, true, false); }
+    } else {
+        if (ry == 4) { if (nat) RTSDF_P4(4, false, true); else RTSDF_P4(4, false, false); }
+        else if (ry == 2) { if (nat) RTSDF_P4(2, false, true); else RTSDF_P4(2, false, false); }
+        else { if (nat) RTSDF_P4(1, false, true); else RTSDF_P4(1, false, false); }
+        // the (rare) overflow of the kernel's per-warp tie queues; a no-op when empty
+        jfa_fixup_kernel<FINAL, SLAB><<<(unsigned)num_sms(), 128, 0, st>>>(
+            s, dst, dst_sdf, g, beta, fix, make_fastdiv((uint32_t)g.nz), make_fastdiv((uint32_t)g.ny));
+        count_launch(1);
+    }
+#undef RTSDF_P4
+    count_launch(1);
+}
+
+// v4 (jfa4.cuh) vs v2 (jfa2.cuh), measured on B200 (tools/jfa_time.py):
+// EXACT (dyadic spacings, ties resolved in the pass) C4 512^3 late passes
+// 1.21 vs 1.32 ms -> v4.  Non-EXACT C3 (1:4:1) dense passes 0.69 vs 0.56 ms ->
+// v2: both sit at the ~6-instruction-per-candidate floor (27 per cell), and
+// v4's saving on loads / decode (own column only) is outweighed by its halo
+// lanes, its in-kernel tie fix-ups and instruction-cache misses
+// (profiles/r2_jfa_v4_vs_v2.txt).
+static bool use_v4(const JfaGeom& g) { return g.exact; }
 
 static int launch_step(PlaneSrc s, int32_t* dst, const JfaGeom& g, bool slab, void* ws,
                        cudaStream_t st) {
@@ -591,6 +642,9 @@ static int launch_step(PlaneSrc s, int32_t* dst, const JfaGeom& g, bool slab, vo
         if (slab) jfa_step_kernel<JFA_INT, true><<<grid, block, 0, st>>>(s, dst, g);
         else jfa_step_kernel<JFA_INT, false><<<grid, block, 0, st>>>(s, dst, g);
         count_launch();
+    } else if (int_mode && use_v4(g)) {
+        if (slab) launch_pass4<false, true>(s, dst, nullptr, g, 0.0, nullptr, ws, st);
+        else launch_pass4<false, false>(s, dst, nullptr, g, 0.0, nullptr, ws, st);
     } else if (int_mode) {
         if (slab) launch_pass2<false, true>(s, dst, nullptr, g, 0.0, nullptr, ws, st);
         else launch_pass2<false, false>(s, dst, nullptr, g, 0.0, nullptr, ws, st);
@@ -799,7 +853,8 @@ static int run_schedule(int32_t* a, int32_t* b, float* sdf_out, int nx, int ny, 
         JfaGeom g{nx, ny, nz, 0, nx, 0, 0, 0, 0, off, hx, hy, hz, wx, wy, wz, exact};
         PlaneSrc s{src, nullptr, nullptr};
         if (sdf_out && off == 1 && int_mode) {  // last pass writes the SDF directly
-            launch_pass2<true, false>(s, nullptr, sdf_out, g, beta, empty_count, ws, st);
+            if (use_v4(g)) launch_pass4<true, false>(s, nullptr, sdf_out, g, beta, empty_count, ws, st);
+            else launch_pass2<true, false>(s, nullptr, sdf_out, g, beta, empty_count, ws, st);
             publish_counts(hist, slots, st);
             return check_launch("jfa_run_sdf");
         }
