@@ -47,7 +47,7 @@ int64_t rtsdf_launch_count(void);
 
 /* ---------------------------------------------------------------- voxelize */
 /* Replaces voxel.py:179 (_voxelize_kernel call) + the OOB check voxel.py:168-175
- * + jfa.py:98 (jfa_init's np.where).  Conservative closed-box 13-axis SAT in
+ * + jfa.py:54 (jfa_init's np.where).  Conservative closed-box 13-axis SAT in
  * fp64 without FMA.  occ (nullable) is zeroed then set to 1 per occupied cell;
  * seed_packed (nullable) is set to EMPTY then self-seeded per occupied cell.
  * counters (device, int64[2]) receive [0] = triangles outside [lo, hi],
@@ -60,12 +60,12 @@ int rtsdf_voxelize(const double* verts, int64_t n_verts, const int32_t* tris, in
                    uint8_t* bad_flags, void* ws, size_t ws_bytes, void* stream);
 
 /* --------------------------------------------------------------------- JFA */
-/* Replaces jfa.py:98 (jfa_init): seed = packed(c) if occ[c] else EMPTY;
+/* Replaces jfa.py:47-55 (jfa_init): seed = packed(c) if occ[c] else EMPTY;
  * count (device int64, nullable) += occupied cells.                         */
 int rtsdf_jfa_init(const uint8_t* occ, int nx, int ny, int nz, int32_t* seed_packed,
                    int64_t* count, void* stream);
 
-/* Replaces jfa.py:180 (_jfa_step_kernel call): one 27-tap pass at `offset`.
+/* Replaces jfa.py:136 (_jfa_step_kernel call): one 27-tap pass at `offset`.
  * Adopt iff fp64 d2 (jfa.py:72-76, left to right, no FMA) is smaller, or equal
  * and the seed is lexicographically smaller (jfa.py:116-124).  (wx, wy, wz) > 0
  * asserts hx^2 : hy^2 : hz^2 == wx : wy : wz EXACTLY (host-checked with exact
@@ -105,7 +105,7 @@ int rtsdf_jfa_run_sdf(int32_t* buf_a, int32_t* buf_b, float* out, int nx, int ny
                       double hx, double hy, double hz, int wx, int wy, int wz, double beta,
                       int64_t* empty_count, void* ws, size_t ws_bytes, void* stream);
 
-/* Replaces jfa.py:224 (_seed_distance_kernel): out = f32(sqrt(d2_fp64) - beta).
+/* Replaces jfa.py:180 (_seed_distance_kernel call): out = f32(sqrt(d2_fp64) - beta).
  * empty_count (device int64, nullable) += EMPTY cells (NoSeedsError check,
  * jfa.py:176-177).                                                          */
 int rtsdf_seeds_to_sdf(const int32_t* seed_packed, float* out, int nx, int ny, int nz,
@@ -293,7 +293,7 @@ int rtsdf_sphere_trace(const float* field, int nx, int ny, int nz, const double*
                        double eps, int max_iter, double max_step, double t_max,
                        const double* t0 /*nullable*/, double k, int32_t* status, double* t,
                        int32_t* iters, double* min_term, void* stream);
-/* Replaces field.py:354-360 (_sample_many).                                */
+/* Replaces field.py:141-148 (_sample_many).                                */
 int rtsdf_trilinear_many(const float* field, int nx, int ny, int nz, const double* lo,
                          const double* h, const double* pts, int64_t n, double* out,
                          void* stream);
@@ -307,7 +307,7 @@ int rtsdf_gbuffer(const void* bvh_packed, int64_t n_nodes, const double* normals
 int rtsdf_compose(const double* g_nrm, const float* g_alb, const uint8_t* g_cov,
                   const double* occ, int height, int width, const double* light /*host[3]*/,
                   const double* background /*host[3]*/, float* out_rgb, void* stream);
-/* Replaces field.py:373 (apply_bias): out = data - f32(bias) in f32.       */
+/* Replaces field.py:155-161 (apply_bias): out = data - f32(bias) in f32.       */
 int rtsdf_apply_bias(const float* data, int64_t n, float bias, float* out, void* stream);
 
 #ifdef __cplusplus

@@ -6,7 +6,7 @@
 // keeps traversal order and best-t pruning identical, so closest hits,
 // facing and tie-breaks match the reference bit for bit even in the fp64
 // corner cases where a different tree could prune differently.  The build is
-// per scene view (static scenes build once, scenes.py:383-390); C++ makes the
+// per scene view (static scenes build once, scenes.py:56-63); C++ makes the
 // 1.31 M-triangle C4 mesh ~100x faster than the reference's recursive Python.
 #include <algorithm>
 #include <cmath>

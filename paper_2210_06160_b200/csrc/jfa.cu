@@ -207,87 +207,11 @@ __global__ void __launch_bounds__(256) jfa_seg_bitmap_kernel(const int32_t* __re
     if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(n_on, 1ull);  // "measured" (+1)
 }
 
-template <int MODE>
-__global__ void __launch_bounds__(256) jfa_sparse_kernel(const int32_t* __restrict__ src,
-                                                         int32_t* __restrict__ dst, JfaGeom g,
-                                                         const uint8_t* __restrict__ bm_in,
-                                                         uint8_t* __restrict__ bm_out,
-                                                         FastDiv dzb, FastDiv dny,
-                                                         unsigned long long* __restrict__ n_on) {
-    unsigned on_count = 0;
-    const int nzb = (int)dzb.d;
-    const uint32_t n_seg = (uint32_t)g.nx * g.ny * nzb;
-    const int lane = threadIdx.x & 31;
-    const int off = g.offset, kz = off >> 5;
-    const int64_t plane = (int64_t)g.ny * g.nz;
-    // lane t < 27 owns tap segment t = (di, dj, dk) + 1
-    const int tdi = (lane / 9 - 1) * off, tdj = ((lane / 3) % 3 - 1) * off, tdz = (lane % 3 - 1) * kz;
-    const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
-    // persistent warps: a ~1 M-segment grid of one-warp blocks is bound by
-    // block scheduling, not by the (mostly trivial) work
-    for (uint32_t seg = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; seg < n_seg; seg += nwarps) {
-        const uint32_t row = fdiv(seg, dzb);  // segments < 2^25
-        const int zb = (int)(seg - row * dzb.d);
-        const int i = (int)fdiv(row, dny), j = (int)(row - (uint32_t)i * dny.d);
-        bool tap = false;
-        if (lane < 27) {
-            const int qi = i + tdi, qj = j + tdj, qz = zb + tdz;
-            if (qi >= 0 && qi < g.nx && qj >= 0 && qj < g.ny && qz >= 0 && qz < nzb)
-                tap = __ldg(bm_in + ((int64_t)qi * g.ny + qj) * nzb + qz) != 0;
-        }
-        const int k = zb * 32 + lane;
-        const int64_t cell = (int64_t)i * plane + (int64_t)j * g.nz + k;
-        if (!__any_sync(0xffffffffu, tap)) {  // no seed can reach this segment
-            if (k < g.nz) dst[cell] = RTSDF_EMPTY;
-            if (bm_out && lane == 0) bm_out[seg] = 0;
-            continue;
-        }
-        int32_t out = RTSDF_EMPTY;
-        if (k < g.nz) {
-            Best<MODE> b;
-            b.p = __ldg(src + cell);
-            if (b.p != RTSDF_EMPTY) {
-                int dx = i - unpack_i(b.p), dy = j - unpack_j(b.p), dz = k - unpack_k(b.p);
-                if (MODE == JFA_INT) b.q = g.wx * dx * dx + g.wy * dy * dy + g.wz * dz * dz;
-                else b.d2 = center_d2(dx, dy, dz, g.hx, g.hy, g.hz);
-            } else {
-                b.q = 0x7fffffff;
-                b.d2 = 1e300;
-            }
-#pragma unroll
-            for (int di = -1; di <= 1; ++di) {
-                const int qi = i + di * off;
-                if (qi < 0 || qi >= g.nx) continue;
-#pragma unroll
-                for (int dj = -1; dj <= 1; ++dj) {
-                    const int qj = j + dj * off;
-                    if (qj < 0 || qj >= g.ny) continue;
-                    const int32_t* rw = src + (int64_t)qi * plane + (int64_t)qj * g.nz;
-#pragma unroll
-                    for (int dk = -1; dk <= 1; ++dk) {
-                        if (di == 0 && dj == 0 && dk == 0) continue;
-                        const int qk = k + dk * off;
-                        if (qk < 0 || qk >= g.nz) continue;
-                        consider<MODE>(b, __ldg(rw + qk), i, j, k, g);
-                    }
-                }
-            }
-            out = b.p;
-            dst[cell] = out;
-        }
-        const unsigned m = __ballot_sync(0xffffffffu, out != RTSDF_EMPTY);
-        if (bm_out && lane == 0) bm_out[seg] = m != 0;
-        on_count += m != 0;
-    }
-    if (n_on && lane == 0 && on_count) atomicAdd(n_on, (unsigned long long)on_count);
-    if (n_on && blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(n_on, 1ull);  // "measured" (+1)
-}
-
 // Two-phase sparse pass.  Phase 1, one THREAD per output segment: the 27 tap
 // segment bits (k a multiple of 32: whole segments) are OR-ed; a segment no
 // seed can reach is filled with EMPTY right away (vector stores, no tap loads)
 // and its output bit cleared, the others are appended to an active list.
-// Phase 2, one warp per active segment: jfa_sparse_kernel's per-cell rule.
+// Phase 2, one warp per active segment: the per-cell rule (jfa_step_kernel's).
 // The thread-per-segment test costs ~100 thread instructions per segment
 // where the warp-per-segment form spent ~90 warp instructions.
 __global__ void __launch_bounds__(256) jfa_sparse_fill_kernel(int32_t* __restrict__ dst, JfaGeom g,
@@ -486,8 +410,6 @@ static bool dims_ok(int nx, int ny, int nz) {
 // jfa2.cuh NAT: min over the grid of the virtual EMPTY seed's weighted d2
 // (taken at the far corner) > the largest real weighted d2 in the grid.
 static bool natural_empty_ok(const JfaGeom& g) {
-    static const bool off = getenv("RTSDF_JFA_NO_NAT") != nullptr;
-    if (off) return false;
     auto sq = [](double v) { return v * v; };
     const double e = g.wx * sq(4096.0 - g.nx) + g.wy * sq(1024.0 - g.ny) + g.wz * sq(1024.0 - g.nz);
     const double r = g.wx * sq(g.nx - 1.0) + g.wy * sq(g.ny - 1.0) + g.wz * sq(g.nz - 1.0);
@@ -509,16 +431,7 @@ static void launch_pass2(PlaneSrc s, int32_t* dst, float* dst_sdf, const JfaGeom
                          int64_t* empty_count, void* ws, cudaStream_t st) {
     const int k = g.offset;
     const int chain_y = (g.ny + k - 1) / k;  // longest j chain
-    static const int ry_max = [] {
-        const char* e = getenv("RTSDF_JFA_RY");
-        return e ? atoi(e) : 4;
-    }();
-    int ry = chain_y >= 4 ? 4 : (chain_y >= 2 ? 2 : 1);
-    if (ry > ry_max) ry = ry_max >= 2 ? 2 : 1;
-    static const int l_env = [] {
-        const char* e = getenv("RTSDF_JFA_L");
-        return e ? atoi(e) : 0;
-    }();
+    const int ry = chain_y >= 4 ? 4 : (chain_y >= 2 ? 2 : 1);
     // Segment length L: each unit re-loads 2 halo planes per L outputs, so
     // longer is cheaper (measured at C3: L = 24 is ~8 % faster than 8) as long
     // as the grid still fills the GPU for two waves (~16 resident warps / SM).
@@ -535,9 +448,9 @@ static void launch_pass2(PlaneSrc s, int32_t* dst, float* dst_sdf, const JfaGeom
     T.jgroups = (chain_y + ry - 1) / ry;
     T.ires = k < g.nxl ? k : g.nxl;
     const int chain_x = (g.nxl + k - 1) / k;
-    T.L = l_env > 0 ? l_env : 24;
+    T.L = 24;
     const int64_t want = (int64_t)num_sms() * 16 * 2;
-    while (l_env <= 0 && T.L > 4 &&
+    while (T.L > 4 &&
            (int64_t)T.nzb * T.jres * T.jgroups * T.ires * ((chain_x + T.L - 1) / T.L) < want)
         T.L /= 2;
     T.isegs = (chain_x + T.L - 1) / T.L;
@@ -801,15 +714,8 @@ static int run_schedule(int32_t* a, int32_t* b, float* sdf_out, int nx, int ny, 
     // non-empty segments of each pass input; the first call for a grid reads
     // them back at once (a small sync per eligible pass), later calls decide
     // from the previous call's counts (SparseHistory) without a sync.
-    static const int sparse_env = [] {
-        const char* e = getenv("RTSDF_JFA_SPARSE_K");
-        return e ? atoi(e) : -1;
-    }();
-    static const double sparse_frac = [] {
-        const char* e = getenv("RTSDF_JFA_SPARSE_FRAC");
-        return e ? atof(e) : 0.05;
-    }();
-    const int sparse_min_k = sparse_env >= 0 ? (sparse_env == 0 ? 1 << 30 : sparse_env) : 64;
+    const double sparse_frac = 0.05;
+    const int sparse_min_k = 64;
     const bool bm_room = ws_bytes >= rtsdf_jfa_ws_bytes(nx, ny, nz);
     const int nzb = (nz + 31) / 32;
     const int64_t n_seg = (int64_t)nx * ny * nzb;
@@ -840,6 +746,9 @@ static int run_schedule(int32_t* a, int32_t* b, float* sdf_out, int nx, int ny, 
     unsigned long long* slots = nullptr;  // per-pass input counts (1 + n), device
     if (bm_room) {
         slots = (unsigned long long*)(bm[1] + seg_bitmap_bytes(nx, ny, nz));
+        // the previous call's publish copy (side stream) reads these slots:
+        // the reset must come after it
+        if (hist && hist->valid) cudaStreamWaitEvent(st, hist->done, 0);
         cudaMemsetAsync(slots, 0, 32 * sizeof(unsigned long long), st);
     }
     bool bm_valid = false;  // bm[0] describes src
@@ -882,16 +791,7 @@ static int run_schedule(int32_t* a, int32_t* b, float* sdf_out, int nx, int ny, 
             // this pass's output bitmap (+ count) feeds the next pass's decision
             const bool next_sparse = off / 2 >= sparse_min_k && (off / 2) % 32 == 0 && pass + 1 < 32;
             unsigned long long* next_slot = next_sparse ? slots + pass + 1 : nullptr;
-            static const bool one_phase = getenv("RTSDF_JFA_SPARSE1") != nullptr;
-            if (one_phase) {
-                if (int_mode)
-                    jfa_sparse_kernel<JFA_INT><<<seg_blocks, 256, 0, st>>>(
-                        src, dst, g, bm[0], next_sparse ? bm[1] : nullptr, dzb, dny, next_slot);
-                else
-                    jfa_sparse_kernel<JFA_FP64><<<seg_blocks, 256, 0, st>>>(
-                        src, dst, g, bm[0], next_sparse ? bm[1] : nullptr, dzb, dny, next_slot);
-                count_launch();
-            } else {
+            {
                 // active list in the (not yet used) fix-up list area, its count in slot 0
                 unsigned long long* n_active = (unsigned long long*)ws;
                 int32_t* active = (int32_t*)((char*)ws + 256);

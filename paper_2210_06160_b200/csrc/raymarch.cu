@@ -4,7 +4,7 @@
 //
 // Restates raymarch.py:83-147 (_march / _shadow_one), render.py:75-152
 // (_gbuffer_kernel / _occlusion_kernel), render.py:186-192 (compose),
-// field.py:155-161 (apply_bias) and field.py:353-360 (_sample_many).  The march
+// field.py:155-161 (apply_bias) and field.py:141-148 (_sample_many).  The march
 // samples the f32 field with the reference's fp64 software trilinear: B200
 // texture filtering uses 8-bit fixed-point weights and would not match.
 #include "common.cuh"

@@ -2,14 +2,17 @@
 // combine/sign update.
 //
 // Restates raysample.py:132-176 (_sample_rays / _sample_masked_kernel),
-// rng.py:30-53 and raysample.py:215-244 (_update_masked_kernel).  Mapping:
-// a warp owns floor(32 / x) masked texels (or one texel in ceil(x / 32)
-// rounds when x > 32); each lane traces one ray of its texel through the
-// reference's own BVH in fp64; a segmented warp reduction produces
-// (min t, front, back) for each texel and the texel's first lane applies the
-// band reset + Eq. 1 + sign and writes the fine value.  Every texel is owned
-// by exactly one lane for the update, so no atomics are used anywhere and
-// the result is independent of scheduling.
+// rng.py:30-53 and raysample.py:215-244 (_update_masked_kernel).  Default
+// (wavefront) path: pass 1 traces every ray with a small BVH4 node budget and
+// merges finished rays into per-texel accumulators; rays out of budget are
+// queued, ordered by direction octant, and re-traced by pass 2; one thread
+// per texel then applies the band reset + Eq. 1 + sign.  The accumulators
+// combine with atomicMin on the fp64 bits of t (t >= 0: integer order is fp64
+// order) and atomicAdd on packed vote counts: min and integer sums are exact
+// and order-free, so the result does not depend on scheduling.  The
+// warp-per-texel kernel (sample_update_kernel) owns each texel with one lane
+// and uses no atomics; it serves texels beyond the wavefront workspace and
+// runs without a workspace.
 #include <cub/cub.cuh>
 
 #include "common.cuh"

@@ -376,7 +376,7 @@ extern "C" int rtsdf_resample_mask_range(const float* coarse, int cnx, int cny, 
     auto al = [](const void* q, uintptr_t a) { return ((uintptr_t)q & (a - 1)) == 0; };
     const bool vec = fnz % 4 == 0 && c0 % 4 == 0 && n_range % 4 == 0 &&
                      (int64_t)fny * fnz >= RS_CELLS_PER_BLOCK / RS_TAB + 1 && al(c_fine, 16) &&
-                     al(mask_new, 4) && al(mask_old, 4) && getenv("RTSDF_RS_SCALAR") == nullptr;
+                     al(mask_new, 4) && al(mask_old, 4);
     if (vec)
         resample_mask4_kernel<<<(unsigned)nb, RS_THREADS, 0, (cudaStream_t)stream>>>(
             P, c_fine, out_unmasked, mask_new, block_counts, mask_old, run_min, front, back);

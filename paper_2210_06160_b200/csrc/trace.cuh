@@ -319,93 +319,6 @@ __device__ __forceinline__ bool leaf_tris(const FastTri* __restrict__ tris, cons
     return improved;
 }
 
-// Resumable form of trace_fast4 for persistent threads: the traversal state
-// lives in this struct and step4() advances it by one node visit or one leaf.
-struct Trace4State {
-    double ox, oy, oz, dx, dy, dz;
-    RayF r;
-    float fdx, fdy, fdz, tb;
-    double best_t;
-    int32_t best_id;
-    int best_facing;
-    int32_t node;
-    int sp;
-};
-
-__device__ __forceinline__ void trace4_init(Trace4State& s, double ox, double oy, double oz,
-                                            double dx, double dy, double dz, double t_max) {
-    s.ox = ox;
-    s.oy = oy;
-    s.oz = oz;
-    s.dx = dx;
-    s.dy = dy;
-    s.dz = dz;
-    s.r.ix = clamp_inv(dx);
-    s.r.iy = clamp_inv(dy);
-    s.r.iz = clamp_inv(dz);
-    s.r.oix = (float)ox * s.r.ix;
-    s.r.oiy = (float)oy * s.r.iy;
-    s.r.oiz = (float)oz * s.r.iz;
-    s.fdx = (float)dx;
-    s.fdy = (float)dy;
-    s.fdz = (float)dz;
-    s.best_t = t_max;
-    s.best_id = -1;
-    s.best_facing = 0;
-    s.tb = t_max < 3.0e38 ? __double2float_ru(t_max) : RTSDF_FINF;
-    s.node = 0;
-    s.sp = 0;
-}
-
-// One node visit (4 slab tests) or one leaf; returns true when the ray is done.
-// Stack entries carry fp16 entry distances and are culled on pop (trace_fast4).
-__device__ __forceinline__ bool trace4_step(const FastBvh4& b, Trace4State& s, int32_t* stack,
-                                            __half* tstack, int stride) {
-    if (s.node >= 0) {
-        const FastNode4* nd = b.nodes + s.node;
-        const float4 lx = __ldg((const float4*)nd->lox), ly = __ldg((const float4*)nd->loy),
-                     lz = __ldg((const float4*)nd->loz), hx = __ldg((const float4*)nd->hix),
-                     hy = __ldg((const float4*)nd->hiy), hz = __ldg((const float4*)nd->hiz);
-        const int4 ch = __ldg((const int4*)nd->child);
-        float t[4];
-        t[0] = box_entry(lx.x, ly.x, lz.x, hx.x, hy.x, hz.x, s.r, s.tb);
-        t[1] = box_entry(lx.y, ly.y, lz.y, hx.y, hy.y, hz.y, s.r, s.tb);
-        t[2] = box_entry(lx.z, ly.z, lz.z, hx.z, hy.z, hz.z, s.r, s.tb);
-        t[3] = box_entry(lx.w, ly.w, lz.w, hx.w, hy.w, hz.w, s.r, s.tb);
-        const int32_t c[4] = {ch.x, ch.y, ch.z, ch.w};
-        int nearest = -1;
-        float tn = RTSDF_FINF;
-#pragma unroll
-        for (int q = 0; q < 4; ++q)
-            if (t[q] < tn) {
-                tn = t[q];
-                nearest = q;
-            }
-#pragma unroll
-        for (int q = 0; q < 4; ++q)
-            if (q != nearest && t[q] != RTSDF_FINF) {
-                stack[s.sp * stride] = c[q];
-                tstack[s.sp * stride] = __float2half_rd(t[q]);
-                ++s.sp;
-            }
-        if (nearest >= 0) {
-            s.node = c[nearest];
-            return false;
-        }
-    } else {
-        leaf_tris(b.tris, b.exact, s.node, s.ox, s.oy, s.oz, s.dx, s.dy, s.dz, s.fdx, s.fdy, s.fdz,
-                  s.best_t, s.best_id, s.best_facing, s.tb);
-    }
-    while (s.sp > 0) {
-        --s.sp;
-        if (__half2float(tstack[s.sp * stride]) <= s.tb) {
-            s.node = stack[s.sp * stride];
-            return false;
-        }
-    }
-    return true;
-}
-
 // Each stack entry carries its box entry distance (fp16, rounded down: a lower
 // bound), and a popped entry is skipped once it lies beyond the current best
 // hit's fp32 upper bound tb -- the same conservative test box_entry applied at
@@ -448,27 +361,6 @@ __device__ __forceinline__ double trace_fast4(const FastBvh4& b, double ox, doub
             t[2] = box_entry(lx.z, ly.z, lz.z, hx.z, hy.z, hz.z, r, tb);
             t[3] = box_entry(lx.w, ly.w, lz.w, hx.w, hy.w, hz.w, r, tb);
             int32_t c[4] = {ch.x, ch.y, ch.z, ch.w};
-#ifdef RTSDF_T4_SORT
-            // farthest first, so the nearest remaining hit is popped next
-#define T4_CE(a, b_)                                   \
-    if (t[a] < t[b_]) {                                \
-        const float tt = t[a];                         \
-        t[a] = t[b_];                                  \
-        t[b_] = tt;                                    \
-        const int32_t cc = c[a];                       \
-        c[a] = c[b_];                                  \
-        c[b_] = cc;                                    \
-    }
-            T4_CE(0, 1) T4_CE(2, 3) T4_CE(0, 2) T4_CE(1, 3) T4_CE(1, 2)
-#undef T4_CE
-#pragma unroll
-            for (int q = 0; q < 4; ++q)
-                if (t[q] != RTSDF_FINF) {
-                    stack[sp * stride] = c[q];
-                    tstack[sp * stride] = __float2half_rd(t[q]);
-                    ++sp;
-                }
-#else
             // nearest hit child is visited next; the other hits go on the stack
             int nearest = -1;
             float tn = RTSDF_FINF;
@@ -489,7 +381,6 @@ __device__ __forceinline__ double trace_fast4(const FastBvh4& b, double ox, doub
                 node = c[nearest];
                 continue;
             }
-#endif
         } else {
             RTSDF_TSTAT(1, 1);
             leaf_tris(b.tris, b.exact, node, ox, oy, oz, dx, dy, dz, fdx, fdy, fdz, best_t,
