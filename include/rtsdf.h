@@ -248,6 +248,23 @@ int rtsdf_sample_update(const void* bvh_packed, int64_t n_nodes, int64_t n_tris,
                         int32_t* front, int32_t* back, double alpha, float* out, void* ws,
                         size_t ws_bytes, void* stream);
 
+/* ---------------------------------------------------- K5 on the device    */
+/* Replaces geometry.py:202-267 (build_bvh) for the K6 search tree of dynamic
+ * scenes (scenes.py:56-93 rebuilds it every animated frame): a linear BVH
+ * (Karras radix tree over 30-bit Morton codes of the triangle-box centroids,
+ * one triangle per leaf) built on the device from device vertices (V, 3) f64,
+ * triangles (T, 3) i32 and unit normals (T, 3) f64 into the packed search
+ * layout (rtsdf_bvh_packed_bytes(rtsdf_lbvh_nodes(T), T) bytes).  refit = 1
+ * keeps the order and topology of the previous build in `ws` and recomputes
+ * the boxes and triangle records from new vertices (same triangle list).
+ * depth_out (device int32, nullable) receives max(depth) with atomicMax.
+ * Any tree gives the reference's closest hits (geometry.py:3-6).           */
+size_t rtsdf_lbvh_ws_bytes(int64_t n_tris);
+int64_t rtsdf_lbvh_nodes(int64_t n_tris);
+int rtsdf_lbvh_build(const double* verts, const int32_t* tris, const double* normals,
+                     int64_t n_tris, int refit, void* packed, size_t packed_bytes, void* ws,
+                     size_t ws_bytes, int32_t* depth_out, void* stream);
+
 /* ------------------------------------------------------ validation oracles */
 /* Replaces geometry.py:592 (_closest_many): exact unsigned point-to-mesh
  * distance per point (fp64 (n, 3) -> fp64 (n,)), over the reference-order
@@ -298,8 +315,11 @@ int rtsdf_trilinear_many(const float* field, int nx, int ny, int nz, const doubl
                          const double* h, const double* pts, int64_t n, double* out,
                          void* stream);
 /* Replaces render.py:123 (_gbuffer_kernel).  cam (host[12]) = pos, fwd,
- * right, up.                                                                */
-int rtsdf_gbuffer(const void* bvh_packed, int64_t n_nodes, const double* normals_orig,
+ * right, up.  fast = 0: the reference-order tree (_bvh_ray's traversal);
+ * fast = 1: the K6 search tree (trace_fast; the same closest hit, used for
+ * device-built trees of dynamic scenes).                                    */
+int rtsdf_gbuffer(const void* bvh_packed, int64_t n_nodes, int64_t n_tris, int fast,
+                  const double* normals_orig,
                   const float* albedo_orig, const double* cam, double half_w, double half_h,
                   int width, int height, double* out_pos, double* out_nrm, float* out_alb,
                   uint8_t* out_cov, void* stream);

@@ -78,7 +78,10 @@ SIGNATURES = {
                             F, P, P]),
     "rtsdf_sphere_trace": (I, [P, I, I, I, DP, DP, P, P, I64, D, I, D, D, P, D, P, P, P, P, P]),
     "rtsdf_trilinear_many": (I, [P, I, I, I, DP, DP, P, I64, P, P]),
-    "rtsdf_gbuffer": (I, [P, I64, P, P, DP, D, D, I, I, P, P, P, P, P]),
+    "rtsdf_gbuffer": (I, [P, I64, I64, I, P, P, DP, D, D, I, I, P, P, P, P, P]),
+    "rtsdf_lbvh_ws_bytes": (SZ, [I64]),
+    "rtsdf_lbvh_nodes": (I64, [I64]),
+    "rtsdf_lbvh_build": (I, [P, P, P, I64, I, P, SZ, P, SZ, P, P]),
     "rtsdf_compose": (I, [P, P, P, P, I, I, DP, DP, P, P]),
     "rtsdf_apply_bias": (I, [P, I64, F, P, P]),
 }

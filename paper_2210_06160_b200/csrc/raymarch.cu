@@ -8,6 +8,7 @@
 // samples the f32 field with the reference's fp64 software trilinear: B200
 // texture filtering uses 8-bit fixed-point weights and would not match.
 #include "common.cuh"
+#include "trace.cuh"
 
 namespace rtsdf {
 
@@ -114,6 +115,46 @@ __global__ void trilinear_many_kernel(FieldView f, const double* __restrict__ pt
 struct Cam {
     double pos[3], fwd[3], right[3], up[3];
 };
+
+// Primary rays through the K6 search tree (trace_fast): the same brute-force
+// closest hit (t, min id) as _bvh_ray, so the same G-buffer; used when the
+// view's tree was built on the device (dynamic scenes).
+__global__ void __launch_bounds__(128) gbuffer_fast_kernel(FastBvh b, const double* __restrict__ normals_orig,
+                                    const float* __restrict__ albedo_orig, Cam cam, double half_w,
+                                    double half_h, int width, int height, double* __restrict__ out_pos,
+                                    double* __restrict__ out_nrm, float* __restrict__ out_alb,
+                                    uint8_t* __restrict__ out_cov) {
+    __shared__ int32_t stack_mem[RTSDF_FAST_STACK * 128];
+    int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (p >= (int64_t)height * width) return;
+    int py = (int)(p / width), px = (int)(p % width);
+    double sy = 1.0 - 2.0 * ((double)py + 0.5) / height;
+    double sx = 2.0 * ((double)px + 0.5) / width - 1.0;
+    double dx = cam.fwd[0] + sx * half_w * cam.right[0] + sy * half_h * cam.up[0];
+    double dy = cam.fwd[1] + sx * half_w * cam.right[1] + sy * half_h * cam.up[1];
+    double dz = cam.fwd[2] + sx * half_w * cam.right[2] + sy * half_h * cam.up[2];
+    double inv = 1.0 / sqrt(dx * dx + dy * dy + dz * dz);
+    dx *= inv;
+    dy *= inv;
+    dz *= inv;
+    int32_t tid;
+    int facing;
+    double t = trace_fast(b, cam.pos[0], cam.pos[1], cam.pos[2], dx, dy, dz,
+                          __longlong_as_double(0x7ff0000000000000ll), stack_mem + threadIdx.x, 128,
+                          tid, facing);
+    if (tid < 0) {
+        out_cov[p] = 0;
+        return;
+    }
+    out_cov[p] = 1;
+    out_pos[3 * p] = cam.pos[0] + t * dx;
+    out_pos[3 * p + 1] = cam.pos[1] + t * dy;
+    out_pos[3 * p + 2] = cam.pos[2] + t * dz;
+    for (int c = 0; c < 3; ++c) {
+        out_nrm[3 * p + c] = normals_orig[3 * (int64_t)tid + c];
+        out_alb[3 * p + c] = albedo_orig[3 * (int64_t)tid + c];
+    }
+}
 
 __global__ void gbuffer_kernel(BvhView b, const double* __restrict__ normals_orig,
                                const float* __restrict__ albedo_orig, Cam cam, double half_w,
@@ -227,7 +268,8 @@ extern "C" int rtsdf_trilinear_many(const float* field, int nx, int ny, int nz, 
     return check_launch("trilinear_many");
 }
 
-extern "C" int rtsdf_gbuffer(const void* bvh_packed, int64_t n_nodes, const double* normals_orig,
+extern "C" int rtsdf_gbuffer(const void* bvh_packed, int64_t n_nodes, int64_t n_tris, int fast,
+                             const double* normals_orig,
                              const float* albedo_orig, const double* cam, double half_w,
                              double half_h, int width, int height, double* out_pos,
                              double* out_nrm, float* out_alb, uint8_t* out_cov, void* stream) {
@@ -240,9 +282,14 @@ extern "C" int rtsdf_gbuffer(const void* bvh_packed, int64_t n_nodes, const doub
         c.right[a] = cam[6 + a];
         c.up[a] = cam[9 + a];
     }
-    gbuffer_kernel<<<(unsigned)((n + 127) / 128), 128, 0, (cudaStream_t)stream>>>(
-        bvh_view(bvh_packed, n_nodes), normals_orig, albedo_orig, c, half_w, half_h, width,
-        height, out_pos, out_nrm, out_alb, out_cov);
+    if (fast)
+        gbuffer_fast_kernel<<<(unsigned)((n + 127) / 128), 128, 0, (cudaStream_t)stream>>>(
+            fast_bvh_view(bvh_packed, n_nodes, n_tris), normals_orig, albedo_orig, c, half_w,
+            half_h, width, height, out_pos, out_nrm, out_alb, out_cov);
+    else
+        gbuffer_kernel<<<(unsigned)((n + 127) / 128), 128, 0, (cudaStream_t)stream>>>(
+            bvh_view(bvh_packed, n_nodes), normals_orig, albedo_orig, c, half_w, half_h, width,
+            height, out_pos, out_nrm, out_alb, out_cov);
     count_launch();
     return check_launch("gbuffer");
 }

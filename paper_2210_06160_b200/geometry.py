@@ -249,6 +249,68 @@ def build_bvh(mesh: TriangleMesh) -> BvhIndex:
                     to_device(mesh.normals), search, int(ns), n4)
 
 
+class DeviceBvh:
+    """The K6 search tree built ON THE DEVICE (rtsdf_lbvh_build): the per-frame
+    tree of dynamic scenes (the reference rebuilds its tree in Python every
+    animated frame, scenes.py:56-93 -> geometry.py:202-267).  Same closest
+    hits as any other tree (geometry.py:3-6).  Rigid or deforming motion with
+    an unchanged triangle list refits the previous topology (boxes and
+    triangle records only); `rebuild_every` frames force a fresh build.
+
+    The reference-order tree (the validation APIs: ray_query fast=False,
+    exact_distance, reference_visibility) is built on the host on first use.
+    """
+
+    device_built = True
+    search_nodes4 = 0
+
+    def __init__(self, mesh: TriangleMesh, verts_dev, tris_dev, state: dict | None = None,
+                 rebuild_every: int = 8):
+        if mesh.num_triangles == 0:
+            raise EmptyMeshError("cannot build BVH over empty mesh")
+        L = _lib.lib()
+        T = int(mesh.num_triangles)
+        self.mesh = mesh
+        self.num_tris = T
+        self.search_nodes = int(L.rtsdf_lbvh_nodes(T))
+        self.normals_dev = to_device(mesh.normals)
+        dev = self.normals_dev.device
+        st = state if state is not None else {}
+        if st.get("T") != T:
+            st.clear()
+            st.update(T=T, ws=torch.empty(int(L.rtsdf_lbvh_ws_bytes(T)), dtype=torch.uint8, device=dev),
+                      bufs=[None, None], flip=0, age=None,
+                      depth=torch.zeros(1, dtype=torch.int32, device=dev), checked=False)
+        refit = st["age"] is not None and st["age"] < rebuild_every - 1
+        st["flip"] ^= 1
+        nbytes = int(L.rtsdf_bvh_packed_bytes(self.search_nodes, T))
+        if st["bufs"][st["flip"]] is None:
+            st["bufs"][st["flip"]] = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+        self.search = st["bufs"][st["flip"]]  # ping-pong: the previous view's tree stays valid
+        _lib.check(L.rtsdf_lbvh_build(_lib.ptr(verts_dev), _lib.ptr(tris_dev), _lib.ptr(self.normals_dev),
+                                      T, 1 if refit else 0, _lib.ptr(self.search), nbytes,
+                                      _lib.ptr(st["ws"]), st["ws"].numel(), _lib.ptr(st["depth"]),
+                                      _lib.stream()), "lbvh_build")
+        st["age"] = st["age"] + 1 if refit else 0
+        if not st["checked"]:  # once per scene: the traversal stack bounds the depth
+            if int(st["depth"].item()) >= 40:  # RTSDF_FAST_STACK (csrc/trace.cuh)
+                raise MeshError("device BVH deeper than the traversal stack (40 levels)")
+            st["checked"] = True
+        self.refit = refit
+        self._ref = None
+
+    def reference_tree(self) -> "BvhIndex":
+        if self._ref is None:
+            self._ref = build_bvh(self.mesh)
+        return self._ref
+
+    def __getattr__(self, name):
+        # node_lo / order / packed / num_nodes / ...: the reference-order tree
+        if name.startswith("_"):
+            raise AttributeError(name)
+        return getattr(self.reference_tree(), name)
+
+
 def _depth4(nodes4: np.ndarray) -> int:
     child = nodes4.view(np.int32).reshape(-1, 32)[:, 24:28]
     frontier, depth = np.array([0]), 0
@@ -348,5 +410,5 @@ def exact_distance(bvh: BvhIndex, point) -> float:
 
 __all__ = ["DEGENERATE_AREA", "FACING_NONE", "FACING_FRONT", "FACING_BACK", "MeshError",
            "MeshParseError", "EmptyMeshError", "TriangleMesh", "make_mesh", "load_mesh",
-           "identity_transform", "BvhIndex", "build_bvh", "RayHit", "ray_query",
+           "identity_transform", "BvhIndex", "DeviceBvh", "build_bvh", "RayHit", "ray_query",
            "ray_query_many", "to_numpy", "exact_distance", "exact_distance_many"]

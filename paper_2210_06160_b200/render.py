@@ -90,8 +90,12 @@ def camera_setup(camera: Camera):
 def launch_gbuffer(view, camera: Camera, gb: GBuffer, cam_setup=None):
     cam, half_w, half_h = cam_setup or camera_setup(camera)
     bvh = view.bvh
+    # device-built (dynamic-scene) trees carry only the search layout
+    fast = getattr(bvh, "device_built", False)
+    buf, nn = (bvh.search, bvh.search_nodes) if fast else (bvh.packed, bvh.num_nodes)
     _lib.check(_lib.lib().rtsdf_gbuffer(
-        _lib.ptr(bvh.packed), bvh.num_nodes, _lib.ptr(bvh.normals_dev), _lib.ptr(view.albedo_dev),
+        _lib.ptr(buf), nn, bvh.num_tris, 1 if fast else 0, _lib.ptr(bvh.normals_dev),
+        _lib.ptr(view.albedo_dev),
         cam, half_w, half_h, camera.width, camera.height, _lib.ptr(gb.position),
         _lib.ptr(gb.normal), _lib.ptr(gb.albedo), _lib.ptr(gb.coverage), _lib.stream()),
         "gbuffer")
