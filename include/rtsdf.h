@@ -44,6 +44,8 @@ const char* rtsdf_version(void);
 const char* rtsdf_last_error(void);
 /* number of kernel launches issued by this library since load (diagnostics) */
 int64_t rtsdf_launch_count(void);
+/* Adds n to the launch counter (a CUDA-graph replay of n counted launches). */
+void rtsdf_count_launches(int64_t n);
 
 /* ---------------------------------------------------------------- voxelize */
 /* Replaces voxel.py:179 (_voxelize_kernel call) + the OOB check voxel.py:168-175
@@ -242,7 +244,8 @@ size_t rtsdf_sample_ws_bytes(int64_t m_cap, int x);
 int rtsdf_sample_update(const void* bvh_packed, int64_t n_nodes, int64_t n_tris, int64_t n_nodes4,
                         const int64_t* idx,
                         const int64_t* count, int64_t m_cap, const rtsdf_resample_desc* rs,
-                        int x, uint64_t seed, int64_t frame, double t_max, const double* dirs,
+                        int x, uint64_t seed, int64_t frame, const int64_t* frame_dev /*nullable*/,
+                        double t_max, const double* dirs,
                         double* samp_min, int32_t* samp_front, int32_t* samp_back,
                         const float* prev, const uint8_t* mask_old, float* run_min,
                         int32_t* front, int32_t* back, double alpha, float* out, void* ws,

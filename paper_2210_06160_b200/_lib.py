@@ -41,6 +41,7 @@ SIGNATURES = {
     "rtsdf_version": (C.c_char_p, []),
     "rtsdf_last_error": (C.c_char_p, []),
     "rtsdf_launch_count": (I64, []),
+    "rtsdf_count_launches": (None, [I64]),
     "rtsdf_voxelize_ws_bytes": (SZ, [I64]),
     "rtsdf_voxelize": (I, [P, I64, P, I64, DP, DP, I, I, I, P, P, P, P, P, SZ, P]),
     "rtsdf_jfa_init": (I, [P, I, I, I, P, P, P]),
@@ -72,7 +73,7 @@ SIGNATURES = {
     "rtsdf_ray_query": (I, [P, I64, I64, I, P, P, I64, D, P, P, P, P]),
     "rtsdf_sample_ws_bytes": (SZ, [I64, I]),
     "rtsdf_bvh4_collapse_host": (I64, [P, P, P, P, I64, P, I64]),
-    "rtsdf_sample_update": (I, [P, I64, I64, I64, P, P, I64, C.POINTER(ResampleDesc), I, U64, I64, D, P,
+    "rtsdf_sample_update": (I, [P, I64, I64, I64, P, P, I64, C.POINTER(ResampleDesc), I, U64, I64, P, D, P,
                                 P, P, P, P, P, P, P, P, D, P, P, SZ, P]),
     "rtsdf_occlusion": (I, [P, I, I, I, DP, DP, P, P, P, I, I, DP, D, I, D, D, D, D, D, I, U64,
                             F, P, P]),

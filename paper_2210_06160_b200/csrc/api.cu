@@ -34,3 +34,5 @@ void count_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 extern "C" const char* rtsdf_version(void) { return "rtsdf-b200 0.1.0 (sm_100a)"; }
 extern "C" const char* rtsdf_last_error(void) { return rtsdf::g_err; }
 extern "C" int64_t rtsdf_launch_count(void) { return rtsdf::g_launches.load(); }
+// graph replays run kernels the library counted once, at capture
+extern "C" void rtsdf_count_launches(int64_t n) { rtsdf::count_launch((int)n); }

@@ -680,8 +680,14 @@ static SparseHistory* sparse_history(int nx, int ny, int nz) {
 
 // Copy this call's per-pass counts to the pinned history on the side stream
 // (after the compute stream's counting kernels; off the critical path).
+static bool capturing(cudaStream_t st) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(st, &cs);
+    return cs != cudaStreamCaptureStatusNone;
+}
+
 static void publish_counts(SparseHistory* h, const unsigned long long* slots, cudaStream_t st) {
-    if (!h || !slots) return;
+    if (!h || !slots || capturing(st)) return;  // a graph replays the captured decisions
     // the side stream's previous copy must finish before the pinned buffer is reused
     if (h->valid && cudaEventQuery(h->done) != cudaSuccess) return;
     cudaEventRecord(h->ready, st);
@@ -725,13 +731,16 @@ static int run_schedule(int32_t* a, int32_t* b, float* sdf_out, int nx, int ny, 
         bm[1] = bm[0] + seg_bitmap_bytes(nx, ny, nz);
     }
     bool sparse_on = true;  // until the first dense input
+    // inside a CUDA-graph capture: decide from the history as it stands (no
+    // event queries, no syncs, no publishing); every decision is exact anyway
+    const bool cap = capturing(st);
     SparseHistory* hist = bm_room ? sparse_history(nx, ny, nz) : nullptr;
     unsigned long long pred[32];
     bool predicted = false;
     if (hist) {
         // never wait for the previous call: use its counts if they have landed,
         // else the ones before (one call staler)
-        if (hist->valid && cudaEventQuery(hist->done) == cudaSuccess) {
+        if (!cap && hist->valid && cudaEventQuery(hist->done) == cudaSuccess) {
             for (int i = 0; i < 32; ++i) hist->last[i] = hist->counts[i];
             hist->have_last = true;
         }
@@ -741,14 +750,14 @@ static int run_schedule(int32_t* a, int32_t* b, float* sdf_out, int nx, int ny, 
         }
     }
     const bool big = (int64_t)nx * ny * nz >= ((int64_t)1 << 28);
-    if (predicted && big) predicted = false;  // large grids: the sync is noise, measure every call
+    if (predicted && big && !cap) predicted = false;  // large grids: the sync is noise, measure every call
     int pass = 0;
     unsigned long long* slots = nullptr;  // per-pass input counts (1 + n), device
     if (bm_room) {
         slots = (unsigned long long*)(bm[1] + seg_bitmap_bytes(nx, ny, nz));
         // the previous call's publish copy (side stream) reads these slots:
         // the reset must come after it
-        if (hist && hist->valid) cudaStreamWaitEvent(st, hist->done, 0);
+        if (hist && hist->valid && !cap) cudaStreamWaitEvent(st, hist->done, 0);
         cudaMemsetAsync(slots, 0, 32 * sizeof(unsigned long long), st);
     }
     bool bm_valid = false;  // bm[0] describes src
@@ -779,7 +788,9 @@ static int run_schedule(int32_t* a, int32_t* b, float* sdf_out, int nx, int ny, 
                                                                   (uint32_t)n_seg, slots + pass);
                 count_launch();
             }
-            if (!predicted) {  // first call for this grid (or a big grid): measure now
+            if (!predicted && cap) {
+                sparse = false;  // no history to decide from and no sync in a capture: dense
+            } else if (!predicted) {  // first call for this grid (or a big grid): measure now
                 unsigned long long v = 0;
                 cudaMemcpyAsync(&v, slots + pass, sizeof(v), cudaMemcpyDeviceToHost, st);
                 cudaStreamSynchronize(st);

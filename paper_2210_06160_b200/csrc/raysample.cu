@@ -34,6 +34,7 @@ struct SampleParams {
     FastDiv div_x, div_ny, div_nz;  // wavefront ray-index decode
     uint64_t seed;
     int64_t frame;
+    const int64_t* frame_dev;  // non-null: the frame number is read on the device (graph replays)
     double t_max;
     float tb;  // tmax_bound(t_max), computed once on the host
     const double* dirs;
@@ -73,7 +74,8 @@ __global__ void __launch_bounds__(SAMPLE_THREADS) sample_update_kernel(SamplePar
         double px = P.coarse.lox + ((double)i + 0.5) * P.fhx;
         double py = P.coarse.loy + ((double)j + 0.5) * P.fhy;
         double pz = P.coarse.loz + ((double)k + 0.5) * P.fhz;
-        uint64_t key = stream_key(P.seed, (uint64_t)lin, (uint64_t)P.frame);
+        uint64_t key = stream_key(P.seed, (uint64_t)lin,
+                                  (uint64_t)(P.frame_dev ? *P.frame_dev : P.frame));
         double best = __longlong_as_double(0x7ff0000000000000ll);  // +inf
         int fr = 0, bk = 0;
         for (int rd = 0; rd < rounds; ++rd) {
@@ -208,6 +210,7 @@ __global__ void wf_init_kernel(SampleParams P, WfBuffers B) {
 // (raysample.py:170, rng.py:30-35).
 __global__ void __launch_bounds__(WF_THREADS) wf_setup_kernel(SampleParams P, WfBuffers B) {
     const int64_t M = min(*P.count, P.m_cap);
+    const uint64_t frame = (uint64_t)(P.frame_dev ? *P.frame_dev : P.frame);
     for (int64_t n = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; n < M;
          n += (int64_t)gridDim.x * blockDim.x) {
         // 32-bit index math: cells <= 1024^3
@@ -219,7 +222,7 @@ __global__ void __launch_bounds__(WF_THREADS) wf_setup_kernel(SampleParams P, Wf
         t.x = P.coarse.lox + ((double)i + 0.5) * P.fhx;
         t.y = P.coarse.loy + ((double)j + 0.5) * P.fhy;
         t.z = P.coarse.loz + ((double)k + 0.5) * P.fhz;
-        t.w = __longlong_as_double((long long)stream_key(P.seed, (uint64_t)lin, (uint64_t)P.frame));
+        t.w = __longlong_as_double((long long)stream_key(P.seed, (uint64_t)lin, frame));
         B.tex[n] = t;
     }
 }
@@ -556,7 +559,8 @@ extern "C" int rtsdf_sample_update(const void* bvh_packed, int64_t n_nodes, int6
                                    const int64_t* idx,
                                    const int64_t* count, int64_t m_cap,
                                    const rtsdf_resample_desc* rs, int x, uint64_t seed,
-                                   int64_t frame, double t_max, const double* dirs,
+                                   int64_t frame, const int64_t* frame_dev, double t_max,
+                                   const double* dirs,
                                    double* samp_min, int32_t* samp_front, int32_t* samp_back,
                                    const float* prev, const uint8_t* mask_old, float* run_min,
                                    int32_t* front, int32_t* back, double alpha, float* out,
@@ -590,6 +594,7 @@ extern "C" int rtsdf_sample_update(const void* bvh_packed, int64_t n_nodes, int6
     P.div_nz = make_fastdiv((uint32_t)rs->fnz);
     P.seed = seed;
     P.frame = frame;
+    P.frame_dev = frame_dev;
     P.t_max = t_max;
     P.tb = tmax_bound(t_max);
     P.dirs = dirs;

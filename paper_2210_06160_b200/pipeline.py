@@ -54,6 +54,9 @@ class PipelineConfig:
     # (the flood's streaming grids would evict them: C4's 180 MB tree ran
     # 112-117 ms/frame overlapped vs 110 serial; C3's 0.2 MB tree 8.70 vs 9.00)
     overlap_frames: bool | None = None
+    # static scenes, timing=False: from frame 2 on, replay each frame as one
+    # CUDA graph (one per frame parity, render flag and camera); bit-identical
+    cuda_graphs: bool = True
 
     def __post_init__(self):
         for f, c in zip(self.fine_dims, self.coarse_dims):
@@ -142,6 +145,7 @@ class FramePipeline:
         self._jf_ws = None
         self._flood_marked = {}  # id -> tensor already recorded on the flood stream
         self._m_cap = None  # sampler workspace texel capacity (grow-only, _sample_capacity)
+        self._frame_dev = None  # graph replays: the RNG frame number on the device
         self._count_host = None
         self._count_pending = None
         # cfg.overlap_frames (None = auto), switchable between frames: off when the caller
@@ -319,13 +323,13 @@ class FramePipeline:
         (never waited on).  Texels beyond the capacity are still sampled, by the
         workspace-free tail kernel (rtsdf_sample_update), so the capacity only
         steers speed, never the result."""
-        if self._m_cap is None:
-            self._m_cap = max(int(cb.count.item()), 1)  # frame 0: one sync
+        if self._m_cap is None:  # frame 0: one sync; 25 % headroom
+            self._m_cap = int(max(int(cb.count.item()), 1) * 1.25) + 1
             return self._m_cap
         pend = self._count_pending
         if pend is not None and pend[1].query():
             seen = int(pend[0][0])
-            if seen > 0.9 * self._m_cap:
+            if seen > self._m_cap:  # that frame ran texels through the tail kernel
                 self._m_cap = int(seen * 1.25) + 1
             self._count_pending = None
         return self._m_cap
@@ -339,9 +343,10 @@ class FramePipeline:
             ev.record()
             self._count_pending = (self._count_host, ev)
 
-    def _rt_pass(self, view, frame, b):
+    def _rt_pass(self, view, frame, b, frame_dev=None):
         """RT: resample + mask + band reset (K4), compaction, fused sample + Eq. 1
-        (K6/K7); returns the new mask buffer."""
+        (K6/K7); returns the new mask buffer.  frame_dev: the frame number as a
+        device scalar (graph replays)."""
         cfg = self.cfg
         g = _rs._RsGeom(self.coarse, tuple(cfg.fine_dims))
         mask_new = b["mask_b"] if self.accum.mask is b["mask_a"] else b["mask_a"]
@@ -360,11 +365,12 @@ class FramePipeline:
             dirs = to_device(np.ascontiguousarray(self.direction_fn(idx, frame), dtype=np.float64))
             m_cap = max(m, 1)
         elif cfg.sampling.rays_per_frame > 0:
-            m_cap = self._sample_capacity(cb)
+            m_cap = self._m_cap if frame_dev is not None else self._sample_capacity(cb)
         _rs.launch_sample_update(view.bvh, g, cb, cfg.sampling, frame, t_max, dirs=dirs,
                                  prev=self.fine.data, accum=self.accum, out=self.fine.data,
-                                 m_cap=m_cap if m_cap is not None else 1)
-        self._note_count(cb)
+                                 m_cap=m_cap if m_cap is not None else 1, frame_dev=frame_dev)
+        if frame_dev is None:
+            self._note_count(cb)
         return mask_new
 
     def advance(self, render=False, camera=None, timing=True) -> FrameRecord:
@@ -380,6 +386,9 @@ class FramePipeline:
         view = self.scene.view(frame)
         b = self._buffers()
         lo, hi = self.scene.lo, self.scene.hi
+        if self._graph_ok(view, timing):
+            return self._advance_graphed(view, render, camera)
+        self._graph_flooded = False
         timer = _Timer(timing, cfg.repeats)
 
         # DL's G-buffer depends only on mesh + camera: it runs on a side stream
@@ -472,6 +481,117 @@ class FramePipeline:
         self.records.append(rec)
         self.frame += 1
         return rec
+
+    # ------------------------------------------------------------ CUDA graphs
+    def _graph_ok(self, view, timing) -> bool:
+        cfg = self.cfg
+        return (cfg.cuda_graphs and not timing and not self.scene.animated and self.frame >= 2
+                and self.direction_fn is None and cfg.sampling.rays_per_frame > 0
+                and self._m_cap is not None)
+
+    def _advance_graphed(self, view, render, camera) -> FrameRecord:
+        """One frame as a CUDA-graph replay.  Graph (parity p = frame % 2, render,
+        camera, overlap): [G-buffer on the side stream] || [with overlap: V + JF of
+        frame + 1 into JF set 1 - p on the flood stream] || [RT of the frame from
+        JF set p (without overlap: V + JF first), DL], all joined at the end.  The
+        RNG frame number is a device scalar written before each replay; every
+        buffer is the one the eager frame of the same parity would use, so the
+        replay is the eager frame bit for bit."""
+        cfg = self.cfg
+        frame = self.frame
+        p = frame % 2
+        b = self._buffers()
+        cam = (camera or self.scene.camera) if render else None
+        overlap = self._overlap_for(view)
+        main = torch.cuda.current_stream()
+        if self._prefetch is not None:  # the eager frame before flooded this one
+            main.wait_event(self._prefetch[2])
+            pre_set = self._prefetch[1]
+            self._prefetch = None
+        else:
+            pre_set = None
+        if overlap and pre_set is None and not getattr(self, "_graph_flooded", False):
+            # the previous frame did not flood this one (e.g. it was serial):
+            # flood set p eagerly once
+            self._jf_set(p)
+            self._coarse_pass(view, p)
+        if self._frame_dev is None:
+            self._frame_dev = torch.zeros(1, dtype=torch.int64, device=b["masked"].device)
+        if render:
+            dl = self._dl_buffers(cam)
+        for s_ in (0, 1):
+            self._jf_set(s_)
+        m_cap = self._m_cap
+        _rs.sample_workspace(m_cap, cfg.sampling.rays_per_frame)  # no growth inside a capture
+        key = (p, bool(render), cam, overlap, m_cap)
+        graphs = self.__dict__.setdefault("_graphs", {})
+        self._frame_dev.fill_(frame)
+        mask_old = b["mask_a"] if p == 0 else b["mask_b"]  # eager: frame f reads mask (f - 1) % 2
+        mask_new = b["mask_b"] if p == 0 else b["mask_a"]
+        if self.accum.mask is not mask_old:
+            raise RuntimeError("graph replay out of step with the temporal state")
+        coarse_buf = self._jf_set(p)["coarse"] if overlap else b["jf"][0]["coarse"]
+        self.coarse = DistanceField(coarse_buf, np.asarray(self.scene.lo, np.float64),
+                                    np.asarray(self.scene.hi, np.float64), beta=cfg.beta)
+        entry = graphs.get(key)
+        if entry is None:
+            g = torch.cuda.CUDAGraph()
+            cap_stream = self.__dict__.setdefault("_cap_stream", torch.cuda.Stream())
+            n0 = _lib.launch_count()
+            with torch.cuda.graph(g, stream=cap_stream):
+                self._graph_body(view, frame, p, render, cam, overlap, b)
+            entry = graphs[key] = (g, _lib.launch_count() - n0)
+        else:
+            _lib.lib().rtsdf_count_launches(entry[1])
+        entry[0].replay()
+        self._graph_flooded = overlap
+        self.accum.mask = mask_new
+        self.accum.frames_seen += 1
+        self.fine = DistanceField(self.fine.data, self.coarse.lo, self.coarse.hi,
+                                  beta=self.coarse.beta, bias=self.fine.bias, frame=frame)
+        self.last_image = None
+        if render:
+            self.last_occlusion = dl["occ"]
+            self.last_image = dl["img"]
+        rec = FrameRecord(frame, {q: 0 for q in PASSES}, b["compact"].count.clone(),
+                          cfg.sampling.rays_per_frame, None)
+        self.records.append(rec)
+        self.frame += 1
+        return rec
+
+    def _graph_body(self, view, frame, p, render, cam, overlap, b):
+        """The launches of one graph-mode frame (captured once per key)."""
+        cfg = self.cfg
+        main = torch.cuda.current_stream()
+        gb_done = None
+        if render:
+            dl = self._dl_buffers(cam)
+            side = self._side_stream()
+            side.wait_stream(main)
+            with torch.cuda.stream(side):
+                _render.launch_gbuffer(view, cam, dl["gb"], dl["cam"])
+                gb_done = torch.cuda.Event()
+                gb_done.record(side)
+        flood_done = None
+        if overlap:
+            flood = self._flood_stream()
+            flood.wait_stream(main)
+            with torch.cuda.stream(flood):
+                self._coarse_pass(view, 1 - p)  # V + JF of frame + 1 (static scene)
+                flood_done = torch.cuda.Event()
+                flood_done.record(flood)
+        else:
+            self._coarse_pass(view, 0)
+        self._rt_pass(view, frame, b, frame_dev=self._frame_dev)
+        if render:
+            main.wait_event(gb_done)
+            light = self.scene.light.unit()
+            _render.launch_occlusion(dl["gb"], self.fine, light, self.march_params(),
+                                     cfg.shade_draws, cfg.sampling.seed, dl["occ"],
+                                     sample_bias=cfg.bias)
+            _render.launch_compose(dl["gb"], dl["occ"], light, (0.05, 0.07, 0.10), dl["img"])
+        if flood_done is not None:
+            main.wait_event(flood_done)
 
     def run(self, frames: int, render_last=False, camera=None):
         for i in range(frames):

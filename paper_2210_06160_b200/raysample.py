@@ -172,7 +172,8 @@ def sample_workspace(m: int, x: int) -> torch.Tensor:
 
 def launch_sample_update(bvh: BvhIndex, g: _RsGeom, cb: CompactBuffers, params: SamplingParams,
                          frame: int, t_max: float, dirs=None, samp=None, prev=None,
-                         accum: AccumulatorField | None = None, out=None, m_cap=None):
+                         accum: AccumulatorField | None = None, out=None, m_cap=None,
+                         frame_dev=None):
     """m_cap: texel capacity; when None the masked count is read back (one
     sync) so the wavefront workspace can be sized to the actual rays."""
     desc = g.desc()
@@ -184,7 +185,8 @@ def launch_sample_update(bvh: BvhIndex, g: _RsGeom, cb: CompactBuffers, params: 
         _lib.ptr(bvh.search), bvh.search_nodes, bvh.num_tris, bvh.search_nodes4, _lib.ptr(cb.idx),
         _lib.ptr(cb.count),
         int(m_cap), desc, int(params.rays_per_frame),
-        int(params.seed) & 0xFFFFFFFFFFFFFFFF, int(frame), float(t_max), _lib.ptr(dirs),
+        int(params.seed) & 0xFFFFFFFFFFFFFFFF, int(frame), _lib.ptr(frame_dev), float(t_max),
+        _lib.ptr(dirs),
         _lib.ptr(samp[0]), _lib.ptr(samp[1]), _lib.ptr(samp[2]),
         _lib.ptr(prev), _lib.ptr(accum.mask if accum else None),
         _lib.ptr(accum.min_dist if accum else None), _lib.ptr(accum.front if accum else None),

@@ -158,13 +158,16 @@ def test_sampler_capacity_tail_exact(rt):
         assert digest(_np(pipe.accum.back)) == g["back"]
 
 
-def test_frame_is_sync_free_after_the_first(rt, monkeypatch):
-    """advance() after frame 0 never blocks the host on the device (no .item(),
-    no synchronize): every device->host read is replaced by a failing stub."""
-    pc = rt.PipelineConfig(coarse_dims=C1["dims"], fine_dims=C1["dims"],
+@pytest.mark.parametrize("graphs", [False, True])
+def test_frame_is_sync_free_after_the_first(rt, monkeypatch, graphs):
+    """advance() after the first frames (capacity, graph captures) never blocks
+    the host on the device (no .item(), no synchronize): every device->host
+    read is replaced by a failing stub."""
+    pc = rt.PipelineConfig(coarse_dims=C1["dims"], fine_dims=C1["dims"], cuda_graphs=graphs,
                            sampling=rt.SamplingParams(rays_per_frame=C1["x"]))
     pipe = rt.FramePipeline(rt.get_scene(C1["scene"]), pc)
-    pipe.advance(render=True, timing=False)
+    for _ in range(4):  # frame 0 (capacity), frames 2 / 3 capture their CUDA graphs
+        pipe.advance(render=True, timing=False)
     torch.cuda.synchronize()
 
     def boom(*a, **k):
@@ -178,3 +181,33 @@ def test_frame_is_sync_free_after_the_first(rt, monkeypatch):
         pipe.advance(render=True, timing=False)
     monkeypatch.undo()
     assert pipe.records[-1].masked_texels == golden()["c1.frame0"]["masked"]
+
+
+@pytest.mark.parametrize("case,frames", [("c1", 6), ("c3", 4)])
+def test_cuda_graph_frames_bit_identical(rt, case, frames):
+    """Frames replayed as CUDA graphs (frame >= 2, static scene) == the eager
+    frames: coarse, fine, accumulator, masked count and the shaded image."""
+    cfg = C1 if case == "c1" else C3
+    outs = []
+    for graphs in (False, True):
+        pc = rt.PipelineConfig(coarse_dims=cfg["dims"], fine_dims=cfg["dims"], cuda_graphs=graphs,
+                               sampling=rt.SamplingParams(rays_per_frame=cfg["x"]))
+        pipe = rt.FramePipeline(rt.get_scene(cfg["scene"]), pc)
+        seq = []
+        for f in range(frames):
+            rec = pipe.advance(render=(f % 2 == 1), timing=False)
+            pipe.join()
+            seq.append((rec.masked_texels, _np(pipe.coarse.data), _np(pipe.fine.data),
+                        _np(pipe.accum.min_dist), _np(pipe.accum.front), _np(pipe.accum.back),
+                        None if pipe.last_image is None else _np(pipe.last_image)))
+        if graphs:
+            assert len(pipe._graphs) == 2  # (parity, render) pairs captured once each
+        outs.append(seq)
+        del pipe
+    for a, b in zip(*outs):
+        assert a[0] == b[0]
+        for x, y in zip(a[1:], b[1:]):
+            if x is None:
+                assert y is None
+            else:
+                np.testing.assert_array_equal(x, y)
