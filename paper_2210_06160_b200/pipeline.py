@@ -323,14 +323,14 @@ class FramePipeline:
         (never waited on).  Texels beyond the capacity are still sampled, by the
         workspace-free tail kernel (rtsdf_sample_update), so the capacity only
         steers speed, never the result."""
-        if self._m_cap is None:  # frame 0: one sync; 25 % headroom
-            self._m_cap = int(max(int(cb.count.item()), 1) * 1.25) + 1
+        if self._m_cap is None:  # frame 0: one sync; 25 % headroom (<= every cell)
+            self._m_cap = min(int(max(int(cb.count.item()), 1) * 1.25) + 1, cb.n)
             return self._m_cap
         pend = self._count_pending
         if pend is not None and pend[1].query():
             seen = int(pend[0][0])
             if seen > self._m_cap:  # that frame ran texels through the tail kernel
-                self._m_cap = int(seen * 1.25) + 1
+                self._m_cap = min(int(seen * 1.25) + 1, cb.n)
             self._count_pending = None
         return self._m_cap
 
