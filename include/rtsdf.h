@@ -84,13 +84,29 @@ size_t rtsdf_jfa_ws_bytes(int nx, int ny, int nz);
 /* Slab form for z-slab (outer-axis) sharding across GPUs: this rank owns global
  * planes [x0, x0 + nxl) of an nx-plane grid in `local`; halo_lo holds global
  * planes [lo_first, lo_first + n_lo) and halo_hi [hi_first, hi_first + n_hi)
- * (received from other ranks).  Output: dst (nxl planes).  Every plane a
- * cell needs must be present; the host schedules the exchange.              */
+ * (received from other ranks).  Output planes [out_first, out_first +
+ * out_count) (inside the owned range; dst points at plane out_first), so the
+ * interior planes [x0 + k, x0 + nxl - k) -- which read only local planes -- can
+ * run while the halo exchange is in flight and the boundary planes after it.
+ * Every plane an output cell needs must be present; the host schedules the
+ * exchange.                                                                 */
 int rtsdf_jfa_step_slab(const int32_t* local, const int32_t* halo_lo, const int32_t* halo_hi,
                         int32_t* dst, int nx, int x0, int nxl, int lo_first, int n_lo,
                         int hi_first, int n_hi, int ny, int nz, int offset, double hx,
-                        double hy, double hz, int wx, int wy, int wz, void* ws,
-                        size_t ws_bytes, void* stream);
+                        double hy, double hz, int wx, int wy, int wz, int out_first,
+                        int out_count, void* ws, size_t ws_bytes, void* stream);
+/* Compressed halo planes (sparse early passes of the slab schedule): n_el
+ * int32 seeds as a bitmap of their non-EMPTY 32-cell segments
+ * (rtsdf_halo_bitmap_words(n_el) words) + those segments packed in order
+ * (payload capacity n_el; *total (device) = packed segments).  decompress
+ * expands (bits, payload) into dst, EMPTY elsewhere.  ws:
+ * rtsdf_halo_ws_bytes(n_el).  Exact: every non-EMPTY value is transmitted. */
+int64_t rtsdf_halo_bitmap_words(int64_t n_el);
+size_t rtsdf_halo_ws_bytes(int64_t n_el);
+int rtsdf_halo_compress(const int32_t* src, int64_t n_el, uint32_t* bits, int32_t* payload,
+                        int64_t* total, void* ws, size_t ws_bytes, void* stream);
+int rtsdf_halo_decompress(const uint32_t* bits, const int32_t* payload, int64_t n_el, int32_t* dst,
+                          void* ws, size_t ws_bytes, void* stream);
 
 /* Replaces jfa.py:140-145 (jfa_run's pass loop): runs the whole schedule
  * n/2 .. 1 ping-ponging between buf_a (holding the init seeds) and buf_b.
@@ -300,10 +316,13 @@ int rtsdf_glibc_sincos(const double* x, int64_t n, double* s, double* c, void* s
 /* Replaces render.py:167 (_occlusion_kernel): per covered pixel fp64 sphere
  * trace with the triangulated cone term (raymarch.py:83-147).  sample_bias:
  * apply_bias (field.py:155-161) fused into every trilinear sample as an f32
- * subtraction, so shading needs no biased copy of the field (0 = none).     */
+ * subtraction, so shading needs no biased copy of the field (0 = none).
+ * Only rows [row0, row0 + nrows) are shaded (pixel-sharded DL; the RNG stream
+ * stays the global pixel index py * W + px, render.py:145).                 */
 int rtsdf_occlusion(const float* field, int nx, int ny, int nz, const double* lo /*host[3]*/,
                     const double* h /*host[3]*/, const double* g_pos, const double* g_nrm,
-                    const uint8_t* g_cov, int height, int width, const double* light /*host[3]*/,
+                    const uint8_t* g_cov, int height, int width, int row0, int nrows,
+                    const double* light /*host[3]*/,
                     double eps, int max_iter, double max_step, double t_max, double k,
                     double jitter, double offset, int draws, uint64_t seed, float sample_bias,
                     double* out, void* stream);

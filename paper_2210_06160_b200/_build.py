@@ -18,8 +18,8 @@ PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB = PKG / "librtsdf.so"
-SOURCES = ["api.cu", "voxel.cu", "jfa.cu", "resample.cu", "bvh.cu", "lbvh.cu", "raysample.cu",
-           "raymarch.cu", "validate.cu"]
+SOURCES = ["api.cu", "voxel.cu", "jfa.cu", "halo.cu", "resample.cu", "bvh.cu", "lbvh.cu",
+           "raysample.cu", "raymarch.cu", "validate.cu"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

@@ -47,8 +47,12 @@ SIGNATURES = {
     "rtsdf_jfa_init": (I, [P, I, I, I, P, P, P]),
     "rtsdf_jfa_ws_bytes": (SZ, [I, I, I]),
     "rtsdf_jfa_step": (I, [P, P, I, I, I, I, D, D, D, I, I, I, P, SZ, P]),
-    "rtsdf_jfa_step_slab": (I, [P, P, P, P, I, I, I, I, I, I, I, I, I, I, D, D, D, I, I, I, P, SZ,
-                                P]),
+    "rtsdf_jfa_step_slab": (I, [P, P, P, P, I, I, I, I, I, I, I, I, I, I, D, D, D, I, I, I, I, I, P,
+                                SZ, P]),
+    "rtsdf_halo_bitmap_words": (I64, [I64]),
+    "rtsdf_halo_ws_bytes": (SZ, [I64]),
+    "rtsdf_halo_compress": (I, [P, I64, P, P, P, P, SZ, P]),
+    "rtsdf_halo_decompress": (I, [P, P, I64, P, P, SZ, P]),
     "rtsdf_jfa_run": (I, [P, P, I, I, I, D, D, D, I, I, I, C.POINTER(I), P, SZ, P]),
     "rtsdf_jfa_run_sdf": (I, [P, P, P, I, I, I, D, D, D, I, I, I, D, P, P, SZ, P]),
     "rtsdf_seeds_to_sdf": (I, [P, P, I, I, I, D, D, D, D, P, P]),
@@ -75,8 +79,8 @@ SIGNATURES = {
     "rtsdf_bvh4_collapse_host": (I64, [P, P, P, P, I64, P, I64]),
     "rtsdf_sample_update": (I, [P, I64, I64, I64, P, P, I64, C.POINTER(ResampleDesc), I, U64, I64, P, D, P,
                                 P, P, P, P, P, P, P, P, D, P, P, SZ, P]),
-    "rtsdf_occlusion": (I, [P, I, I, I, DP, DP, P, P, P, I, I, DP, D, I, D, D, D, D, D, I, U64,
-                            F, P, P]),
+    "rtsdf_occlusion": (I, [P, I, I, I, DP, DP, P, P, P, I, I, I, I, DP, D, I, D, D, D, D, D, I,
+                            U64, F, P, P]),
     "rtsdf_sphere_trace": (I, [P, I, I, I, DP, DP, P, P, I64, D, I, D, D, P, D, P, P, P, P, P]),
     "rtsdf_trilinear_many": (I, [P, I, I, I, DP, DP, P, I64, P, P]),
     "rtsdf_gbuffer": (I, [P, I64, I64, I, P, P, DP, D, D, I, I, P, P, P, P, P]),

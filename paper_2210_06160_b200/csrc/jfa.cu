@@ -33,6 +33,8 @@ struct JfaGeom {
     double hx, hy, hz;
     int wx, wy, wz;
     bool exact;  // fp64 d2 exact for these spacings (fp64_exact): ties resolve in the pass
+    int ox0, onx;  // output planes [ox0, ox0 + onx) (a sub-range of the owned planes;
+                   // dst points at plane ox0): interior / boundary launches of a slab
 };
 
 // True when every fp64 operation of center_d2 (jfa.py:72-76) is exact for all
@@ -132,13 +134,13 @@ __global__ void __launch_bounds__(256) jfa_step_kernel(PlaneSrc src, int32_t* __
                                                        JfaGeom g) {
     const int k = blockIdx.x * 32 + threadIdx.x;
     const int j = blockIdx.y * 8 + threadIdx.y;
-    const int il = blockIdx.z;  // local plane
+    const int il = blockIdx.z;  // output plane (relative to g.ox0)
     if (k >= g.nz || j >= g.ny) return;
-    const int i = g.x0 + il;
+    const int i = g.ox0 + il;
     const int64_t plane = (int64_t)g.ny * g.nz;
     const int off = g.offset;
     Best<MODE> b;
-    b.p = __ldg(src.local + (int64_t)il * plane + (int64_t)j * g.nz + k);
+    b.p = __ldg(src.local + (int64_t)(i - g.x0) * plane + (int64_t)j * g.nz + k);
     if (b.p != RTSDF_EMPTY) {
         int dx = i - unpack_i(b.p), dy = j - unpack_j(b.p), dz = k - unpack_k(b.p);
         if (MODE == JFA_INT) b.q = g.wx * dx * dx + g.wy * dy * dy + g.wz * dz * dz;
@@ -446,15 +448,15 @@ static void launch_pass2(PlaneSrc s, int32_t* dst, float* dst_sdf, const JfaGeom
     T.nzb = (g.nz + 31) / 32;
     T.jres = k < g.ny ? k : g.ny;
     T.jgroups = (chain_y + ry - 1) / ry;
-    T.ires = k < g.nxl ? k : g.nxl;
-    const int chain_x = (g.nxl + k - 1) / k;
+    T.ires = k < g.onx ? k : g.onx;
+    const int chain_x = (g.onx + k - 1) / k;
     T.L = 24;
     const int64_t want = (int64_t)num_sms() * 16 * 2;
     while (T.L > 4 &&
            (int64_t)T.nzb * T.jres * T.jgroups * T.ires * ((chain_x + T.L - 1) / T.L) < want)
         T.L /= 2;
     T.isegs = (chain_x + T.L - 1) / T.L;
-    JfaFixList fix = fix_list(ws, (int64_t)g.nxl * g.ny * g.nz);
+    JfaFixList fix = fix_list(ws, (int64_t)g.onx * g.ny * g.nz);
     cudaMemsetAsync(fix.count, 0, sizeof(int64_t), st);
     int64_t warps = (int64_t)T.nzb * T.jres * T.jgroups * T.ires * T.isegs;
     unsigned blocks = (unsigned)((warps + 3) / 4);
@@ -501,8 +503,8 @@ static void launch_pass4(PlaneSrc s, int32_t* dst, float* dst_sdf, const JfaGeom
     if (T.nlong > k) T.nlong = k;
     T.jres = k < g.ny ? k : g.ny;
     T.jgroups = (chain_y + ry - 1) / ry;
-    T.ires = k < g.nxl ? k : g.nxl;
-    const int chain_x = (g.nxl + k - 1) / k;
+    T.ires = k < g.onx ? k : g.onx;
+    const int chain_x = (g.onx + k - 1) / k;
     // segment length L: 2 halo planes per L outputs; halve while the grid
     // would not fill the GPU for two waves (~16 resident warps / SM)
     T.L = 24;
@@ -512,7 +514,7 @@ static void launch_pass4(PlaneSrc s, int32_t* dst, float* dst_sdf, const JfaGeom
     T.isegs = (chain_x + T.L - 1) / T.L;
     const int64_t warps = (int64_t)T.zw * T.jres * T.jgroups * T.ires * T.isegs;
     const unsigned blocks = (unsigned)((warps + 3) / 4);
-    JfaFixList fix = fix_list(ws, (int64_t)g.nxl * g.ny * g.nz);
+    JfaFixList fix = fix_list(ws, (int64_t)g.onx * g.ny * g.nz);
     if (!g.exact) cudaMemsetAsync(fix.count, 0, sizeof(int64_t), st);
 #define RTSDF_P4(RYV, EX, NA) \
     jfa_pass4_kernel<RYV, FINAL, SLAB, EX, NA><<<blocks, 128, 0, st>>>(s, dst, dst_sdf, g, T, beta, empty_count, fix)
@@ -545,7 +547,7 @@ static bool use_v4(const JfaGeom& g) { return g.exact; }
 static int launch_step(PlaneSrc s, int32_t* dst, const JfaGeom& g, bool slab, void* ws,
                        cudaStream_t st) {
     dim3 block(32, 8, 1);
-    dim3 grid((g.nz + 31) / 32, (g.ny + 7) / 8, g.nxl);
+    dim3 grid((g.nz + 31) / 32, (g.ny + 7) / 8, g.onx);
     bool int_mode = g.wx > 0 && g.wy > 0 && g.wz > 0;
     int mdim = g.nx > g.ny ? g.nx : g.ny;
     if (g.nz > mdim) mdim = g.nz;
@@ -621,7 +623,7 @@ extern "C" int rtsdf_jfa_step(const int32_t* src, int32_t* dst, int nx, int ny, 
     }
     if (!ws_ok(ws, ws_bytes, (int64_t)nx * ny * nz)) return RTSDF_ERR_WORKSPACE;
     JfaGeom g{nx, ny, nz, 0, nx, 0, 0, 0, 0, offset, hx, hy, hz, wx, wy, wz,
-              wx > 0 && fp64_exact(hx, hy, hz, nx, ny, nz)};
+              wx > 0 && fp64_exact(hx, hy, hz, nx, ny, nz), 0, nx};
     PlaneSrc s{src, nullptr, nullptr};
     return launch_step(s, dst, g, false, ws, (cudaStream_t)stream);
 }
@@ -630,15 +632,18 @@ extern "C" int rtsdf_jfa_step_slab(const int32_t* local, const int32_t* halo_lo,
                                    const int32_t* halo_hi, int32_t* dst, int nx, int x0, int nxl,
                                    int lo_first, int n_lo, int hi_first, int n_hi, int ny, int nz,
                                    int offset, double hx, double hy, double hz, int wx, int wy,
-                                   int wz, void* ws, size_t ws_bytes, void* stream) {
+                                   int wz, int out_first, int out_count, void* ws, size_t ws_bytes,
+                                   void* stream) {
     if (!dims_ok(nx, ny, nz)) return RTSDF_ERR_DIMS;
-    if (offset < 1 || nxl < 1 || x0 < 0 || x0 + nxl > nx || !weights_ok(nx, ny, nz, wx, wy, wz)) {
-        set_error("jfa_step_slab: bad slab/offset/weights");
+    if (offset < 1 || nxl < 1 || x0 < 0 || x0 + nxl > nx || !weights_ok(nx, ny, nz, wx, wy, wz) ||
+        out_first < x0 || out_count < 0 || out_first + out_count > x0 + nxl) {
+        set_error("jfa_step_slab: bad slab/offset/weights/output range");
         return RTSDF_ERR_INVALID;
     }
+    if (out_count == 0) return RTSDF_OK;
     if (!ws_ok(ws, ws_bytes, (int64_t)nxl * ny * nz)) return RTSDF_ERR_WORKSPACE;
     JfaGeom g{nx,     ny,    nz, x0, nxl, lo_first, n_lo, hi_first, n_hi, offset, hx, hy, hz,
-              wx,     wy,    wz, wx > 0 && fp64_exact(hx, hy, hz, nx, ny, nz)};
+              wx,     wy,    wz, wx > 0 && fp64_exact(hx, hy, hz, nx, ny, nz), out_first, out_count};
     PlaneSrc s{local, halo_lo, halo_hi};
     return launch_step(s, dst, g, true, ws, (cudaStream_t)stream);
 }
@@ -768,7 +773,7 @@ static int run_schedule(int32_t* a, int32_t* b, float* sdf_out, int nx, int ny, 
     const unsigned seg_blocks = (unsigned)(seg_need < (int64_t)num_sms() * 16 ? seg_need : (int64_t)num_sms() * 16);
     const FastDiv dzb = make_fastdiv((uint32_t)nzb), dny = make_fastdiv((uint32_t)ny);
     for (int off = n / 2; off >= 1; off /= 2) {
-        JfaGeom g{nx, ny, nz, 0, nx, 0, 0, 0, 0, off, hx, hy, hz, wx, wy, wz, exact};
+        JfaGeom g{nx, ny, nz, 0, nx, 0, 0, 0, 0, off, hx, hy, hz, wx, wy, wz, exact, 0, nx};
         PlaneSrc s{src, nullptr, nullptr};
         if (sdf_out && off == 1 && int_mode) {  // last pass writes the SDF directly
             if (use_v4(g)) launch_pass4<true, false>(s, nullptr, sdf_out, g, beta, empty_count, ws, st);

@@ -114,8 +114,8 @@ __global__ void __launch_bounds__(128) jfa_pass2_kernel(PlaneSrc src, int32_t* _
     const int ri = islot % T.ires, si = islot / T.ires;
     const int k = g.offset;
     const int L = T.L;
-    const int i_first = g.x0 + ri + si * L * k;  // global plane of output a = 0
-    const int i_end = g.x0 + g.nxl;              // outputs only on owned planes
+    const int i_first = g.ox0 + ri + si * L * k;  // global plane of output a = 0
+    const int i_end = g.ox0 + g.onx;              // outputs only on owned planes
     if (i_first >= i_end) return;
     const int z = zb * 32 + lane;
     const bool zok = z < g.nz;
@@ -275,7 +275,7 @@ __global__ void __launch_bounds__(128) jfa_pass2_kernel(PlaneSrc src, int32_t* _
             for (int b = 0; b < RY; ++b) {
                 const int oj = j_base + b * k;
                 const bool live = zok && oj < g.ny;
-                const int64_t cell = (int64_t)(oi - g.x0) * plane + (int64_t)oj * g.nz + z;
+                const int64_t cell = (int64_t)(oi - g.ox0) * plane + (int64_t)oj * g.nz + z;
                 const int32_t wt = W[0][b];
                 const bool tie = !EXACT && wt != RTSDF_EMPTY && (Km[0][b] & 1);
                 const int32_t w = wt;
@@ -348,7 +348,7 @@ __global__ void __launch_bounds__(128, JFA_FIX_MINB) jfa_fixup_kernel(PlaneSrc s
         const int z = (int)(cell - row * dnz.d);
         const uint32_t il = fdiv(row, dny);
         const int j = (int)(row - il * dny.d);
-        const int i = g.x0 + (int)il;
+        const int i = g.ox0 + (int)il;
         const int32_t* pl[3];
 #pragma unroll
         for (int di = 0; di < 3; ++di) {

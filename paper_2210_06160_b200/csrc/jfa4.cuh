@@ -121,7 +121,7 @@ __device__ __forceinline__ void jfa4_flush(const PlaneSrc& src, int32_t* dst, fl
         const int il = (int)(cell / plane);
         const int rem = (int)(cell - (int64_t)il * plane);
         const int j = rem / g.nz, z = rem - j * g.nz;
-        const int i = g.x0 + il;
+        const int i = g.ox0 + il;
         const int32_t w = jfa4_exact_cell<SLAB>(src, g, i, j, z);
         jfa4_store<FINAL>(dst, dst_sdf, g, cell, i, j, z, w, beta);
     }
@@ -149,8 +149,8 @@ __global__ void __launch_bounds__(128, 4) jfa_pass4_kernel(PlaneSrc src, int32_t
     const int ri = islot % T.ires, si = islot / T.ires;
     const int k = g.offset;
     const int L = T.L;
-    const int i_first = g.x0 + ri + si * L * k;
-    const int i_end = g.x0 + g.nxl;
+    const int i_first = g.ox0 + ri + si * L * k;
+    const int i_end = g.ox0 + g.onx;
     if (i_first >= i_end) return;
 
     // ---- z: chain position of this lane
@@ -275,7 +275,7 @@ __global__ void __launch_bounds__(128, 4) jfa_pass4_kernel(PlaneSrc src, int32_t
         const int oa = a - 1;
         if (oa >= 0) {
             const int oi = i_first + oa * k;
-            const int64_t cbase = (int64_t)(oi - g.x0) * plane + z;
+            const int64_t cbase = (int64_t)(oi - g.ox0) * plane + z;
 #pragma unroll
             for (int b = 0; b < RY; ++b) {
                 const int oj = j_base + b * k;

@@ -64,11 +64,12 @@ __device__ int march(const FieldView& f, double ox, double oy, double oz, double
 
 __global__ void occlusion_kernel(FieldView f, const double* __restrict__ g_pos,
                                  const double* __restrict__ g_nrm, const uint8_t* __restrict__ g_cov,
-                                 int height, int width, double lx, double ly, double lz, MarchArgs a,
-                                 double jitter, double offset, int draws, uint64_t seed,
-                                 double* __restrict__ out) {
-    int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (p >= (int64_t)height * width) return;
+                                 int height, int width, int row0, int nrows, double lx, double ly,
+                                 double lz, MarchArgs a, double jitter, double offset, int draws,
+                                 uint64_t seed, double* __restrict__ out) {
+    // pixels of rows [row0, row0 + nrows) (a pixel-sharded band or the image)
+    int64_t p = (int64_t)row0 * width + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (p >= (int64_t)(row0 + nrows) * width || p >= (int64_t)height * width) return;
     if (!g_cov[p]) {
         out[p] = 0.0;
         return;
@@ -227,20 +228,20 @@ using namespace rtsdf;
 
 extern "C" int rtsdf_occlusion(const float* field, int nx, int ny, int nz, const double* lo,
                                const double* h, const double* g_pos, const double* g_nrm,
-                               const uint8_t* g_cov, int height, int width, const double* light,
-                               double eps, int max_iter, double max_step, double t_max, double k,
-                               double jitter, double offset, int draws, uint64_t seed,
-                               float sample_bias, double* out, void* stream) {
-    if (draws < 1 || max_iter < 1) {
-        set_error("occlusion: draws and max_iter must be >= 1");
+                               const uint8_t* g_cov, int height, int width, int row0, int nrows,
+                               const double* light, double eps, int max_iter, double max_step,
+                               double t_max, double k, double jitter, double offset, int draws,
+                               uint64_t seed, float sample_bias, double* out, void* stream) {
+    if (draws < 1 || max_iter < 1 || row0 < 0 || nrows < 0 || row0 + nrows > height) {
+        set_error("occlusion: draws and max_iter must be >= 1, rows inside the image");
         return RTSDF_ERR_INVALID;
     }
-    int64_t n = (int64_t)height * width;
+    int64_t n = (int64_t)nrows * width;
     if (n <= 0) return RTSDF_OK;
     MarchArgs a{eps, max_iter, max_step, t_max, k};
     occlusion_kernel<<<(unsigned)((n + 127) / 128), 128, 0, (cudaStream_t)stream>>>(
-        fview(field, nx, ny, nz, lo, h, sample_bias), g_pos, g_nrm, g_cov, height, width, light[0], light[1],
-        light[2], a, jitter, offset, draws, seed, out);
+        fview(field, nx, ny, nz, lo, h, sample_bias), g_pos, g_nrm, g_cov, height, width, row0, nrows,
+        light[0], light[1], light[2], a, jitter, offset, draws, seed, out);
     count_launch();
     return check_launch("occlusion");
 }

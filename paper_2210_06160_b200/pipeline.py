@@ -485,9 +485,11 @@ class FramePipeline:
     # ------------------------------------------------------------ CUDA graphs
     def _graph_ok(self, view, timing) -> bool:
         cfg = self.cfg
+        # a view not validated yet (first frame of a new SceneView) runs eagerly:
+        # its voxelization checks read back
         return (cfg.cuda_graphs and not timing and not self.scene.animated and self.frame >= 2
                 and self.direction_fn is None and cfg.sampling.rays_per_frame > 0
-                and self._m_cap is not None)
+                and self._m_cap is not None and self._checked_view is view)
 
     def _advance_graphed(self, view, render, camera) -> FrameRecord:
         """One frame as a CUDA-graph replay.  Graph (parity p = frame % 2, render,
@@ -521,9 +523,11 @@ class FramePipeline:
             dl = self._dl_buffers(cam)
         for s_ in (0, 1):
             self._jf_set(s_)
+        view.mesh_buffers()  # every buffer the graph touches exists before the capture
         m_cap = self._m_cap
         _rs.sample_workspace(m_cap, cfg.sampling.rays_per_frame)  # no growth inside a capture
-        key = (p, bool(render), cam, overlap, m_cap)
+        # the view is part of the key: a graph references its mesh / BVH buffers
+        key = (p, bool(render), cam, overlap, m_cap, id(view))
         graphs = self.__dict__.setdefault("_graphs", {})
         self._frame_dev.fill_(frame)
         mask_old = b["mask_a"] if p == 0 else b["mask_b"]  # eager: frame f reads mask (f - 1) % 2
@@ -540,7 +544,9 @@ class FramePipeline:
             n0 = _lib.launch_count()
             with torch.cuda.graph(g, stream=cap_stream):
                 self._graph_body(view, frame, p, render, cam, overlap, b)
-            entry = graphs[key] = (g, _lib.launch_count() - n0)
+            while len(graphs) >= 8:  # drop the oldest graph (and its view's buffers)
+                graphs.pop(next(iter(graphs)))
+            entry = graphs[key] = (g, _lib.launch_count() - n0, view)
         else:
             _lib.lib().rtsdf_count_launches(entry[1])
         entry[0].replay()

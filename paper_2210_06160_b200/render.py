@@ -109,15 +109,18 @@ def rasterize_gbuffer(view, camera: Camera) -> GBuffer:
 
 
 def launch_occlusion(gbuffer: GBuffer, fld: DistanceField, light_unit, params: MarchParams,
-                     draws, seed, out, sample_bias: float = 0.0):
-    """sample_bias: shade `fld` biased by that much (apply_bias fused, f32)."""
+                     draws, seed, out, sample_bias: float = 0.0, rows=None):
+    """sample_bias: shade `fld` biased by that much (apply_bias fused, f32).
+    rows = (row0, nrows): shade only that band of the image (pixel-sharded DL)."""
     h, w = gbuffer.shape
+    row0, nrows = rows if rows is not None else (0, h)
     nx, ny, nz = fld.dims
     offset = 2.0 * params.epsilon + (fld.bias + sample_bias)  # render.py:165
     _lib.check(_lib.lib().rtsdf_occlusion(
         _lib.ptr(fld.data), nx, ny, nz, (_lib.D * 3)(*fld.lo), (_lib.D * 3)(*fld.cell_size),
         _lib.ptr(gbuffer.position), _lib.ptr(gbuffer.normal), _lib.ptr(gbuffer.coverage), h, w,
-        (_lib.D * 3)(*light_unit), float(params.epsilon), int(params.max_iterations),
+        int(row0), int(nrows), (_lib.D * 3)(*light_unit), float(params.epsilon),
+        int(params.max_iterations),
         float(params.max_step), float(params.t_max), params.cone_k, float(params.jitter),
         float(offset), max(1, int(draws)), int(seed) & 0xFFFFFFFFFFFFFFFF,
         float(np.float32(sample_bias)), _lib.ptr(out), _lib.stream()), "occlusion")

@@ -13,7 +13,10 @@ rank's slab of planes [x0, x0 + nxl) of the outermost axis.
         rtsdf_*_range and rtsdf_sample_update with global-indexed slab
         buffers, so texel indices, RNG streams and ray origins are the
         single-GPU ones);
-    DL  the fine slabs are gathered on rank 0, which shades the image.
+    DL  the fine slabs are all-gathered (every rank holds the whole field),
+        each rank shades its band of image rows (G-buffer + soft-shadow
+        march; RNG streams stay the global pixel index) and rank 0 gathers
+        the occlusion bands and composes the image.
 
 Every per-cell computation is the single-GPU kernel's, so the sharded frame is
 bit-identical to FramePipeline by construction (tests: LoopbackCluster runs W
@@ -153,29 +156,45 @@ class ShardedFramePipeline:
         self.mask_cur = 1 - self.mask_cur
         return cb.count
 
-    def stage_dl(self, fine_full: torch.Tensor, camera=None):
-        """Rank 0: G-buffer + soft-shadow march + compose on the gathered fine field."""
-        cfg = self.cfg
-        cam = camera or self.scene.camera
-        view = self.scene.view(self.frame)
+    def _dl_state(self, cam):
         if self._dl is None or self._dl["cam"] is not cam:
             gb = _render.GBuffer.empty(cam.height, cam.width)
             dev = gb.position.device
             self._dl = dict(cam=cam, gb=gb, setup=_render.camera_setup(cam),
-                            occ=torch.empty((cam.height, cam.width), dtype=torch.float64, device=dev),
+                            occ=torch.zeros((cam.height, cam.width), dtype=torch.float64, device=dev),
                             img=torch.empty((cam.height, cam.width, 3), dtype=torch.float32, device=dev))
-        dl = self._dl
+        return self._dl
+
+    def stage_dl_band(self, fine_full: torch.Tensor, rows, camera=None):
+        """G-buffer + soft-shadow march of image rows [rows[0], rows[0] + rows[1])
+        over the full fine field (pixel-sharded DL); returns the (H, W) occlusion
+        buffer, valid on the band."""
+        cfg = self.cfg
+        cam = camera or self.scene.camera
+        view = self.scene.view(self.frame)
+        dl = self._dl_state(cam)
         fld = DistanceField(fine_full, np.asarray(self.scene.lo, np.float64),
                             np.asarray(self.scene.hi, np.float64), beta=cfg.beta, frame=self.frame)
         mp = MarchParams.for_field(fld, max_step=cfg.max_step, max_iterations=cfg.max_iterations,
                                    jitter=cfg.jitter, light_angle=self.scene.light.angular_radius)
         _render.launch_gbuffer(view, cam, dl["gb"], dl["setup"])
-        light = self.scene.light.unit()
-        _render.launch_occlusion(dl["gb"], fld, light, mp, cfg.shade_draws, cfg.sampling.seed,
-                                 dl["occ"], sample_bias=cfg.bias)
-        _render.launch_compose(dl["gb"], dl["occ"], light, (0.05, 0.07, 0.10), dl["img"])
+        _render.launch_occlusion(dl["gb"], fld, self.scene.light.unit(), mp, cfg.shade_draws,
+                                 cfg.sampling.seed, dl["occ"], sample_bias=cfg.bias, rows=rows)
+        return dl["occ"]
+
+    def stage_compose(self, occ: torch.Tensor, camera=None):
+        """Lambert compose of the G-buffer with the full occlusion image."""
+        cam = camera or self.scene.camera
+        dl = self._dl_state(cam)
+        _render.launch_compose(dl["gb"], occ, self.scene.light.unit(), (0.05, 0.07, 0.10), dl["img"])
         self.last_image = dl["img"]
         return dl["img"]
+
+    def stage_dl(self, fine_full: torch.Tensor, camera=None):
+        """The whole image on one rank (G-buffer + march + compose)."""
+        cam = camera or self.scene.camera
+        occ = self.stage_dl_band(fine_full, (0, cam.height), cam)
+        return self.stage_compose(occ, cam)
 
     # ---------------------------------------------------- distributed frame
     def advance(self, render=False, group=None):
@@ -189,13 +208,19 @@ class ShardedFramePipeline:
         count = self.stage_rt()
         img = None
         if render:
-            if self._gather_buf is None and self.rank == 0:
+            # every rank gets the whole fine field (all-gather over NVLink) and
+            # shades its band of image rows; rank 0 gathers the bands and composes
+            if self._gather_buf is None:
                 nmax = max(n for _, n in self.bounds)
                 self._gather_buf = torch.empty((nmax * self.world,) + self.dims[1:],
                                                dtype=self.fine.dtype, device=self.fine.device)
-            full = gather_slabs(self.fine, self.bounds, self.rank, group, out=self._gather_buf)
+            full = allgather_slabs(self.fine, self.bounds, group, out=self._gather_buf)
+            cam = self.scene.camera
+            rows = row_bands(cam.height, self.world)[self.rank]
+            occ = self.stage_dl_band(full, rows)
+            occ_full = gather_rows(occ, row_bands(cam.height, self.world), self.rank, group)
             if self.rank == 0:
-                img = self.stage_dl(full)
+                img = self.stage_compose(occ_full)
             # no per-frame barrier: the next frame's collectives order the
             # ranks on the device, and the host may run ahead
         self.frame += 1
@@ -217,6 +242,39 @@ def exchange_coarse_halo(coarse_h: torch.Tensor, rank: int, world: int, group=No
     if ops:
         for req in dist.batch_isend_irecv(ops):
             req.wait()
+
+
+def row_bands(height: int, world: int):
+    """[(row0, nrows)] per rank: the pixel-sharded DL bands (slab_bounds of rows)."""
+    return _slab.slab_bounds(height, world)
+
+
+def allgather_slabs(local: torch.Tensor, bounds, group=None, out=None):
+    """The concatenated slabs on EVERY rank (all-gather, slabs padded to the
+    largest); `out`: a persistent (world * nmax, ...) buffer."""
+    import torch.distributed as dist
+
+    nmax = max(n for _, n in bounds)
+    rest = tuple(local.shape[1:])
+    send = local.contiguous()
+    if local.shape[0] < nmax:
+        send = torch.zeros((nmax,) + rest, dtype=local.dtype, device=local.device)
+        send[: local.shape[0]] = local
+    if out is None:
+        out = torch.empty((nmax * len(bounds),) + rest, dtype=local.dtype, device=local.device)
+    dist.all_gather_into_tensor(out, send, group=group)
+    if all(n == nmax for _, n in bounds):
+        return out
+    return torch.cat([out[r * nmax: r * nmax + n] for r, (_, n) in enumerate(bounds)])
+
+
+def gather_rows(img: torch.Tensor, bands, rank: int, group=None):
+    """Rank 0 receives every rank's band of rows of an (H, W) image (None elsewhere)."""
+    import torch.distributed as dist
+
+    r0, n = bands[rank]
+    band = img[r0: r0 + n]
+    return gather_slabs(band, bands, rank, group)
 
 
 def gather_slabs(local: torch.Tensor, bounds, rank: int, group=None, out=None):
@@ -271,11 +329,18 @@ class LoopbackCluster:
             if i < self.world - 1:
                 r.coarse_h[r.nxl + 1].copy_(self.ranks[i + 1].coarse_h[1])
         counts = [r.stage_rt() for r in self.ranks]
-        if render:
-            self.last_image = r0.stage_dl(self.fine)
+        if render:  # pixel-sharded DL: every rank shades its band, rank 0 composes
+            full = self.fine
+            cam = r0.scene.camera
+            occ = torch.zeros((cam.height, cam.width), dtype=torch.float64, device=full.device)
+            for r, (row0, n) in zip(self.ranks, row_bands(cam.height, self.world)):
+                band = r.stage_dl_band(full, (row0, n))
+                occ[row0: row0 + n] = band[row0: row0 + n]
+            self.last_image = r0.stage_compose(occ)
         for r in self.ranks:
             r.frame += 1
         return int(sum(int(c.item()) for c in counts))
 
 
-__all__ = ["ShardedFramePipeline", "LoopbackCluster", "exchange_coarse_halo", "gather_slabs"]
+__all__ = ["ShardedFramePipeline", "LoopbackCluster", "exchange_coarse_halo", "gather_slabs",
+           "allgather_slabs", "gather_rows", "row_bands"]

@@ -78,9 +78,12 @@ def plan_pass(nx: int, bounds, k: int):
     return plan
 
 
-def exchange(local: torch.Tensor, halo_lo: torch.Tensor, halo_hi: torch.Tensor, plan, rank: int,
-             bounds, group=None):
-    """Run this rank's sends/receives of one pass (torch.distributed P2P)."""
+def exchange_async(local: torch.Tensor, halo_lo: torch.Tensor, halo_hi: torch.Tensor, plan,
+                   rank: int, bounds, group=None):
+    """Post this rank's sends/receives of one pass (torch.distributed P2P, NCCL
+    over NVLink) and return the work handles: work.wait() makes the CURRENT
+    stream wait for them (no host block), so kernels that need no halo plane
+    can run while the planes are in flight."""
     import torch.distributed as dist
 
     x0 = bounds[rank][0]
@@ -92,27 +95,153 @@ def exchange(local: torch.Tensor, halo_lo: torch.Tensor, halo_hi: torch.Tensor, 
         elif t.dst == rank and t.src != rank:
             buf = halo_lo if t.side == "lo" else halo_hi
             ops.append(dist.P2POp(dist.irecv, buf[t.offset: t.offset + t.count], t.src, group))
+    return dist.batch_isend_irecv(ops) if ops else []
+
+
+def exchange(local: torch.Tensor, halo_lo: torch.Tensor, halo_hi: torch.Tensor, plan, rank: int,
+             bounds, group=None):
+    """Run this rank's sends/receives of one pass and wait for them."""
+    for req in exchange_async(local, halo_lo, halo_hi, plan, rank, bounds, group):
+        req.wait()
+
+
+class HaloCodec:
+    """Bitmap + packed-segment compression of halo plane ranges (csrc/halo.cu)."""
+
+    def __init__(self, device):
+        self.device = device
+        self._ws = {}
+
+    def ws(self, n_el):
+        w = self._ws.get(n_el)
+        if w is None:
+            w = self._ws[n_el] = torch.empty(int(_lib.lib().rtsdf_halo_ws_bytes(n_el)),
+                                             dtype=torch.uint8, device=self.device)
+        return w
+
+    def words(self, n_el):
+        return int(_lib.lib().rtsdf_halo_bitmap_words(n_el))
+
+    def compress(self, planes: torch.Tensor):
+        n_el = planes.numel()
+        bits = torch.empty(self.words(n_el), dtype=torch.int32, device=self.device)
+        payload = torch.empty(n_el, dtype=torch.int32, device=self.device)
+        total = torch.zeros(1, dtype=torch.int64, device=self.device)
+        ws = self.ws(n_el)
+        _lib.check(_lib.lib().rtsdf_halo_compress(_lib.ptr(planes), n_el, _lib.ptr(bits),
+                                                  _lib.ptr(payload), _lib.ptr(total), _lib.ptr(ws),
+                                                  ws.numel(), _lib.stream()), "halo_compress")
+        return bits, payload, total
+
+    def decompress(self, bits, payload, out: torch.Tensor):
+        n_el = out.numel()
+        ws = self.ws(n_el)
+        _lib.check(_lib.lib().rtsdf_halo_decompress(_lib.ptr(bits), _lib.ptr(payload), n_el,
+                                                    _lib.ptr(out), _lib.ptr(ws), ws.numel(),
+                                                    _lib.stream()), "halo_decompress")
+
+
+def exchange_compressed(local: torch.Tensor, halo_lo: torch.Tensor, halo_hi: torch.Tensor, plan,
+                        rank: int, bounds, codec: HaloCodec, group=None):
+    """One pass's halo exchange with every plane range compressed (sparse early
+    passes): phase 1 sends each range's segment bitmap and packed-segment count,
+    phase 2 the packed segments (sizes now known: one host read of the counts),
+    then the receiver expands them into the halo buffers.  Returns the number
+    of int32 words received (bitmaps + payloads) for accounting."""
+    import torch.distributed as dist
+
+    x0 = bounds[rank][0]
+    sends, recvs = [], []
+    ops = []
+    for t in plan:
+        if t.src == rank and t.dst != rank:
+            planes = local[t.first - x0: t.first - x0 + t.count]
+            bits, payload, total = codec.compress(planes)
+            sends.append((t, payload, total))
+            ops += [dist.P2POp(dist.isend, bits, t.dst, group),
+                    dist.P2POp(dist.isend, total, t.dst, group)]
+        elif t.dst == rank and t.src != rank:
+            buf = halo_lo if t.side == "lo" else halo_hi
+            out = buf[t.offset: t.offset + t.count]
+            bits = torch.empty(codec.words(out.numel()), dtype=torch.int32, device=codec.device)
+            total = torch.zeros(1, dtype=torch.int64, device=codec.device)
+            recvs.append((t, out, bits, total))
+            ops += [dist.P2POp(dist.irecv, bits, t.src, group),
+                    dist.P2POp(dist.irecv, total, t.src, group)]
     if ops:
         for req in dist.batch_isend_irecv(ops):
             req.wait()
+    ops, got, words = [], [], 0
+    for t, payload, total in sends:
+        n = int(total.item()) * 32  # host read: the payload length of this message
+        if n:
+            ops.append(dist.P2POp(dist.isend, payload[:n], t.dst, group))
+    for t, out, bits, total in recvs:
+        n = int(total.item()) * 32
+        payload = torch.empty(max(n, 1), dtype=torch.int32, device=codec.device)
+        got.append((out, bits, payload))
+        words += bits.numel() + n
+        if n:
+            ops.append(dist.P2POp(dist.irecv, payload[:n], t.src, group))
+    if ops:
+        for req in dist.batch_isend_irecv(ops):
+            req.wait()
+    for out, bits, payload in got:
+        codec.decompress(bits, payload, out)
+    return words
 
 
-def launch_step_slab(local, halo_lo, halo_hi, dst, nx, x0, k, h, w, lo, hi):
+def interior_range(nx: int, x0: int, nxl: int, k: int):
+    """[a, b): the owned output planes whose +-k taps are all local (or outside
+    the grid) -- computable before the halo planes arrive."""
+    (lo_a, lo_n), (hi_a, hi_n) = halo_ranges(nx, x0, nxl, k)
+    a = max(x0, lo_a + lo_n + k) if lo_n else x0
+    b = min(x0 + nxl, hi_a - k) if hi_n else x0 + nxl
+    return (a, b) if a < b else (x0, x0)
+
+
+def launch_step_slab(local, halo_lo, halo_hi, dst, nx, x0, k, h, w, lo, hi, out=None):
+    """One pass on the slab; out = (first, count): the output planes to compute
+    (default: every owned plane); dst is the whole slab's output buffer."""
     nxl, ny, nz = local.shape
+    first, count = out if out is not None else (x0, nxl)
+    if count <= 0:
+        return
     ws = _jfa.workspace(nxl, ny, nz)
     _lib.check(_lib.lib().rtsdf_jfa_step_slab(
-        _lib.ptr(local), _lib.ptr(halo_lo), _lib.ptr(halo_hi), _lib.ptr(dst), nx, x0, nxl,
-        lo[0], lo[1], hi[0], hi[1], ny, nz, int(k), float(h[0]), float(h[1]), float(h[2]), *w,
-        _lib.ptr(ws), ws.numel(), _lib.stream()), "jfa_step_slab")
+        _lib.ptr(local), _lib.ptr(halo_lo), _lib.ptr(halo_hi), _lib.ptr(dst[first - x0:]), nx, x0,
+        nxl, lo[0], lo[1], hi[0], hi[1], ny, nz, int(k), float(h[0]), float(h[1]), float(h[2]), *w,
+        int(first), int(count), _lib.ptr(ws), ws.numel(), _lib.stream()), "jfa_step_slab")
+
+
+def launch_split(local, halo_lo, halo_hi, dst, nx, x0, k, h, w, lo, hi, wait=None):
+    """Interior planes first, then (after `wait()`, the halo's arrival on the
+    stream) the boundary planes below and above it."""
+    nxl = local.shape[0]
+    a, b = interior_range(nx, x0, nxl, k)
+    launch_step_slab(local, halo_lo, halo_hi, dst, nx, x0, k, h, w, lo, hi, out=(a, b - a))
+    if wait is not None:
+        wait()
+    if a == b:  # no interior: every owned plane reads a halo plane
+        launch_step_slab(local, halo_lo, halo_hi, dst, nx, x0, k, h, w, lo, hi)
+        return
+    launch_step_slab(local, halo_lo, halo_hi, dst, nx, x0, k, h, w, lo, hi, out=(x0, a - x0))
+    launch_step_slab(local, halo_lo, halo_hi, dst, nx, x0, k, h, w, lo, hi, out=(b, x0 + nxl - b))
 
 
 _PLANS: dict = {}
 
 
-def flood_slab(local: torch.Tensor, nx: int, rank: int, world: int, h, group=None) -> torch.Tensor:
+COMPRESS_MIN_K = 64  # passes whose input is (almost) all EMPTY: k >= 64 at C3 / C5
+
+
+def flood_slab(local: torch.Tensor, nx: int, rank: int, world: int, h, group=None,
+               compress_min_k: int = COMPRESS_MIN_K) -> torch.Tensor:
     """Full JFA schedule on this rank's slab (init seeds in `local`, global
     packed coordinates); returns the flooded slab.  Collective: every rank of
-    the group must call it with its own slab."""
+    the group must call it with its own slab.  Passes with k >= compress_min_k
+    send their halo planes compressed (HaloCodec); the others send them raw
+    and overlap the transfer with the slab's interior planes."""
     bounds = slab_bounds(nx, world)
     x0, nxl = bounds[rank]
     _, ny, nz = local.shape
@@ -122,14 +251,26 @@ def flood_slab(local: torch.Tensor, nx: int, rank: int, world: int, h, group=Non
     halo_lo = torch.empty((max_halo, ny, nz), dtype=torch.int32, device=local.device)
     halo_hi = torch.empty_like(halo_lo)
     src, dst = local, torch.empty_like(local)
+    codec = HaloCodec(local.device)
     for k in _jfa.jfa_offsets(dims):
         key = (nx, world, k)
         plan = _PLANS.get(key)
         if plan is None:  # pure host logic: once per (grid, world, offset)
             plan = _PLANS[key] = plan_pass(nx, bounds, k)
-        exchange(src, halo_lo, halo_hi, plan, rank, bounds, group)
         lo, hi = halo_ranges(nx, x0, nxl, k)
-        launch_step_slab(src, halo_lo, halo_hi, dst, nx, x0, k, h, w, lo, hi)
+        if k >= compress_min_k:
+            exchange_compressed(src, halo_lo, halo_hi, plan, rank, bounds, codec, group)
+            launch_step_slab(src, halo_lo, halo_hi, dst, nx, x0, k, h, w, lo, hi)
+            src, dst = dst, src
+            continue
+        works = exchange_async(src, halo_lo, halo_hi, plan, rank, bounds, group)
+
+        def wait(works=works):
+            for req in works:
+                req.wait()
+
+        # the interior planes overlap the NCCL transfers; the boundary ones follow
+        launch_split(src, halo_lo, halo_hi, dst, nx, x0, k, h, w, lo, hi, wait=wait)
         src, dst = dst, src
     return src
 
@@ -144,14 +285,26 @@ def flood_loopback(seed: torch.Tensor, world: int, h) -> torch.Tensor:
     dims = (nx, ny, nz)
     w = _jfa.integer_weights(float(h[0]), float(h[1]), float(h[2]), dims)
     cur = seed.clone()
+    codec = HaloCodec(seed.device)
+
+    def halo(a, n):  # the sparse passes' halos take the compressed route, as in flood_slab
+        if not n:
+            return cur[:1].clone()
+        planes = cur[a: a + n].contiguous()
+        if k < COMPRESS_MIN_K:
+            return planes
+        bits, payload, _ = codec.compress(planes)
+        out = torch.empty_like(planes)
+        codec.decompress(bits, payload, out)
+        return out
+
     for k in _jfa.jfa_offsets(dims):
         nxt = torch.empty_like(cur)
         for r, (x0, nxl) in enumerate(bounds):
             lo, hi = halo_ranges(nx, x0, nxl, k)
-            halo_lo = cur[lo[0]: lo[0] + lo[1]].contiguous() if lo[1] else cur[:1].clone()
-            halo_hi = cur[hi[0]: hi[0] + hi[1]].contiguous() if hi[1] else cur[:1].clone()
-            launch_step_slab(cur[x0: x0 + nxl], halo_lo, halo_hi, nxt[x0: x0 + nxl], nx, x0, k,
-                             h, w, lo, hi)
+            halo_lo, halo_hi = halo(*lo), halo(*hi)
+            launch_split(cur[x0: x0 + nxl], halo_lo, halo_hi, nxt[x0: x0 + nxl], nx, x0, k, h, w,
+                         lo, hi)
         torch.cuda.current_stream().synchronize()
         cur = nxt
     return cur
@@ -168,5 +321,6 @@ def halo_volume(nx: int, ny: int, nz: int, world: int):
     return planes, planes * ny * nz * 4
 
 
-__all__ = ["slab_bounds", "owner_of", "halo_ranges", "plan_pass", "exchange", "flood_slab",
-           "flood_loopback", "halo_volume", "Transfer"]
+__all__ = ["slab_bounds", "owner_of", "halo_ranges", "plan_pass", "exchange", "exchange_async",
+           "exchange_compressed", "HaloCodec", "COMPRESS_MIN_K",
+           "interior_range", "launch_split", "flood_slab", "flood_loopback", "halo_volume", "Transfer"]
