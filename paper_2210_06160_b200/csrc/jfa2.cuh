@@ -27,6 +27,9 @@
 #ifndef JFA2_FULL_LOADS
 #define JFA2_FULL_LOADS 0
 #endif
+#ifndef JFA2_MINB
+#define JFA2_MINB 1
+#endif
 #ifndef JFA2_SKIP_MODE
 #define JFA2_SKIP_MODE 1
 #endif
@@ -97,7 +100,7 @@ struct JfaFixList {
 // the grid (jfa.cu natural_empty_ok), so an EMPTY tap needs no select: it can
 // neither win nor tie, and a run of EMPTY taps leaves (Km, W) = (init, EMPTY).
 template <int RY, bool FINAL, bool SLAB, bool EXACT, bool NAT = false>
-__global__ void __launch_bounds__(128) jfa_pass2_kernel(PlaneSrc src, int32_t* __restrict__ dst,
+__global__ void __launch_bounds__(128, JFA2_MINB) jfa_pass2_kernel(PlaneSrc src, int32_t* __restrict__ dst,
                                                         float* __restrict__ dst_sdf, JfaGeom g,
                                                         Jfa2Task T, double beta,
                                                         int64_t* __restrict__ empty_count,
