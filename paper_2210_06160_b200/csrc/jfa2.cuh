@@ -28,8 +28,9 @@
 #define JFA2_FULL_LOADS 0
 #endif
 #ifndef JFA2_MINB
-#define JFA2_MINB 1
+#define JFA2_MINB 4  // 128 registers: 4 resident 128-thread blocks per SM
 #endif
+
 #ifndef JFA2_SKIP_MODE
 #define JFA2_SKIP_MODE 1
 #endif
@@ -95,6 +96,92 @@ struct JfaFixList {
     int64_t cap;
 };
 
+// Integer-tie cells of the v4 pass (jfa4.cuh) are queued per warp and
+// re-decided at the end of its task (a full queue spills to the global list
+// drained by jfa_fixup_kernel).  The same end-of-task queue in v2 measured
+// slower than v2's separate fix-up kernel (C3 schedule 4.40 vs 3.66 ms: the
+// latency-bound gathers stall warps that hold the SM), so v2 keeps the kernel.
+#define JFA_TIEQ 256
+
+// jfa.py:108-124 on the 27 taps of one cell, integer pre-filter (jfa2.cuh
+// jfa_fixup_kernel's rule); returns the reference's seed.
+template <bool SLAB>
+__device__ __forceinline__ int32_t jfa_exact_cell(const PlaneSrc& src, const JfaGeom& g, int i,
+                                                   int j, int z) {
+    const int64_t plane = (int64_t)g.ny * g.nz;
+    const int k = g.offset;
+    const int32_t* pl[3];
+#pragma unroll
+    for (int di = 0; di < 3; ++di) {
+        const int qi = i + (di - 1) * k;
+        pl[di] = nullptr;
+        if (qi >= 0 && qi < g.nx)
+            pl[di] = SLAB ? plane_ptr(src, g, qi, plane) : src.local + (int64_t)qi * plane;
+    }
+    const bool jok[3] = {j - k >= 0, true, j + k < g.ny};
+    const bool zok[3] = {z - k >= 0, true, z + k < g.nz};
+    int32_t c[27];
+#pragma unroll
+    for (int di = 0; di < 3; ++di)
+#pragma unroll
+        for (int dj = 0; dj < 3; ++dj)
+#pragma unroll
+            for (int dk = 0; dk < 3; ++dk) {
+                const bool ok = pl[di] != nullptr && jok[dj] && zok[dk];
+                const int off = (j + (dj - 1) * k) * g.nz + z + (dk - 1) * k;
+                c[(di * 3 + dj) * 3 + dk] = ok ? __ldg(pl[di] + off) : RTSDF_EMPTY;
+            }
+    auto ikey = [&](int32_t v) {
+        const int dx = i - unpack_i(v), dy = j - unpack_j(v), dz = z - unpack_k(v);
+        return v == RTSDF_EMPTY ? 0x7fffffff : g.wx * dx * dx + g.wy * dy * dy + g.wz * dz * dz;
+    };
+    int km = 0x7fffffff;
+#pragma unroll
+    for (int t = 0; t < 27; ++t) km = min(km, ikey(c[t]));
+    int32_t best = RTSDF_EMPTY;
+    double bd = 1e300;
+#pragma unroll
+    for (int t = 0; t < 27; ++t) {
+        if (c[t] == RTSDF_EMPTY || c[t] == best || ikey(c[t]) != km) continue;
+        const double d2 = center_d2(i - unpack_i(c[t]), j - unpack_j(c[t]), z - unpack_k(c[t]),
+                                    g.hx, g.hy, g.hz);
+        if (d2 < bd || (d2 == bd && best != RTSDF_EMPTY && c[t] < best)) {
+            best = c[t];
+            bd = d2;
+        }
+    }
+    return best;
+}
+
+template <bool FINAL>
+__device__ __forceinline__ void jfa_store_out(int32_t* dst, float* dst_sdf, const JfaGeom& g,
+                                           int64_t cell, int i, int j, int z, int32_t w,
+                                           double beta) {
+    if (FINAL) {
+        const double d2 = center_d2(i - unpack_i(w), j - unpack_j(w), z - unpack_k(w), g.hx, g.hy, g.hz);
+        dst_sdf[cell] = (float)__dsub_rn(__dsqrt_rn(d2), beta);
+    } else {
+        dst[cell] = w;
+    }
+}
+
+template <bool FINAL, bool SLAB>
+__device__ __forceinline__ void jfa_flush_ties(const PlaneSrc& src, int32_t* dst, float* dst_sdf,
+                                           const JfaGeom& g, double beta, const int32_t* q, int n,
+                                           int lane) {
+    const int64_t plane = (int64_t)g.ny * g.nz;
+    for (int t = lane; t < n; t += 32) {
+        const int32_t cell = q[t];  // slab-local linear cell (< 2^31)
+        const int il = (int)(cell / plane);
+        const int rem = (int)(cell - (int64_t)il * plane);
+        const int j = rem / g.nz, z = rem - j * g.nz;
+        const int i = g.ox0 + il;
+        const int32_t w = jfa_exact_cell<SLAB>(src, g, i, j, z);
+        jfa_store_out<FINAL>(dst, dst_sdf, g, cell, i, j, z, w, beta);
+    }
+    __syncwarp();
+}
+
 // NAT: the host proved that the packed EMPTY (-1) decodes to a virtual seed
 // (4095, 1023, 1023) whose key exceeds every real seed's key at every cell of
 // the grid (jfa.cu natural_empty_ok), so an EMPTY tap needs no select: it can
@@ -106,6 +193,7 @@ __global__ void __launch_bounds__(128, JFA2_MINB) jfa_pass2_kernel(PlaneSrc src,
                                                         int64_t* __restrict__ empty_count,
                                                         JfaFixList fix) {
     const int lane = threadIdx.x & 31;
+
     int64_t t = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t total = (int64_t)T.nzb * T.jres * T.jgroups * T.ires * T.isegs;
     if (t >= total) return;

@@ -36,7 +36,6 @@
 namespace rtsdf {
 
 #define JFA4_KINIT 0x7ffffffe  // even, above every real (doubled) key (< 2^29)
-#define JFA4_FIXQ 256          // per-warp queue of integer-tie cells (overflow: global list)
 
 struct Jfa4Task {
     int nz_pos;   // positions = nz (all residue chains end to end)
@@ -49,92 +48,13 @@ struct Jfa4Task {
     int skip;     // warp-uniform all-EMPTY value skip (sparse inputs, k >= 16)
 };
 
-// jfa.py:108-124 on the 27 taps of one cell, integer pre-filter (jfa2.cuh
-// jfa_fixup_kernel's rule); returns the reference's seed.
-template <bool SLAB>
-__device__ __forceinline__ int32_t jfa4_exact_cell(const PlaneSrc& src, const JfaGeom& g, int i,
-                                                   int j, int z) {
-    const int64_t plane = (int64_t)g.ny * g.nz;
-    const int k = g.offset;
-    const int32_t* pl[3];
-#pragma unroll
-    for (int di = 0; di < 3; ++di) {
-        const int qi = i + (di - 1) * k;
-        pl[di] = nullptr;
-        if (qi >= 0 && qi < g.nx)
-            pl[di] = SLAB ? plane_ptr(src, g, qi, plane) : src.local + (int64_t)qi * plane;
-    }
-    const bool jok[3] = {j - k >= 0, true, j + k < g.ny};
-    const bool zok[3] = {z - k >= 0, true, z + k < g.nz};
-    int32_t c[27];
-#pragma unroll
-    for (int di = 0; di < 3; ++di)
-#pragma unroll
-        for (int dj = 0; dj < 3; ++dj)
-#pragma unroll
-            for (int dk = 0; dk < 3; ++dk) {
-                const bool ok = pl[di] != nullptr && jok[dj] && zok[dk];
-                const int off = (j + (dj - 1) * k) * g.nz + z + (dk - 1) * k;
-                c[(di * 3 + dj) * 3 + dk] = ok ? __ldg(pl[di] + off) : RTSDF_EMPTY;
-            }
-    auto ikey = [&](int32_t v) {
-        const int dx = i - unpack_i(v), dy = j - unpack_j(v), dz = z - unpack_k(v);
-        return v == RTSDF_EMPTY ? 0x7fffffff : g.wx * dx * dx + g.wy * dy * dy + g.wz * dz * dz;
-    };
-    int km = 0x7fffffff;
-#pragma unroll
-    for (int t = 0; t < 27; ++t) km = min(km, ikey(c[t]));
-    int32_t best = RTSDF_EMPTY;
-    double bd = 1e300;
-#pragma unroll
-    for (int t = 0; t < 27; ++t) {
-        if (c[t] == RTSDF_EMPTY || c[t] == best || ikey(c[t]) != km) continue;
-        const double d2 = center_d2(i - unpack_i(c[t]), j - unpack_j(c[t]), z - unpack_k(c[t]),
-                                    g.hx, g.hy, g.hz);
-        if (d2 < bd || (d2 == bd && best != RTSDF_EMPTY && c[t] < best)) {
-            best = c[t];
-            bd = d2;
-        }
-    }
-    return best;
-}
-
-template <bool FINAL>
-__device__ __forceinline__ void jfa4_store(int32_t* dst, float* dst_sdf, const JfaGeom& g,
-                                           int64_t cell, int i, int j, int z, int32_t w,
-                                           double beta) {
-    if (FINAL) {
-        const double d2 = center_d2(i - unpack_i(w), j - unpack_j(w), z - unpack_k(w), g.hx, g.hy, g.hz);
-        dst_sdf[cell] = (float)__dsub_rn(__dsqrt_rn(d2), beta);
-    } else {
-        dst[cell] = w;
-    }
-}
-
-template <bool FINAL, bool SLAB>
-__device__ __forceinline__ void jfa4_flush(const PlaneSrc& src, int32_t* dst, float* dst_sdf,
-                                           const JfaGeom& g, double beta, const int32_t* q, int n,
-                                           int lane) {
-    const int64_t plane = (int64_t)g.ny * g.nz;
-    for (int t = lane; t < n; t += 32) {
-        const int32_t cell = q[t];  // slab-local linear cell (< 2^31)
-        const int il = (int)(cell / plane);
-        const int rem = (int)(cell - (int64_t)il * plane);
-        const int j = rem / g.nz, z = rem - j * g.nz;
-        const int i = g.ox0 + il;
-        const int32_t w = jfa4_exact_cell<SLAB>(src, g, i, j, z);
-        jfa4_store<FINAL>(dst, dst_sdf, g, cell, i, j, z, w, beta);
-    }
-    __syncwarp();
-}
-
 template <int RY, bool FINAL, bool SLAB, bool EXACT, bool NAT>
 __global__ void __launch_bounds__(128, 4) jfa_pass4_kernel(PlaneSrc src, int32_t* __restrict__ dst,
                                                            float* __restrict__ dst_sdf, JfaGeom g,
                                                            Jfa4Task T, double beta,
                                                            int64_t* __restrict__ empty_count,
                                                            JfaFixList overflow) {
-    __shared__ int32_t fixq_all[4][JFA4_FIXQ];
+    __shared__ int32_t fixq_all[4][JFA_TIEQ];
     const int lane = threadIdx.x & 31;
     int32_t* fixq = fixq_all[(threadIdx.x >> 5) & 3];
     int nfix = 0;  // warp-uniform
@@ -285,7 +205,7 @@ __global__ void __launch_bounds__(128, 4) jfa_pass4_kernel(PlaneSrc src, int32_t
                 const int64_t cell = cbase + (int64_t)oj * g.nz;
                 if (live && !tie) {
                     if (FINAL) empties += w == RTSDF_EMPTY;
-                    jfa4_store<FINAL>(dst, dst_sdf, g, cell, oi, oj, z, w, beta);
+                    jfa_store_out<FINAL>(dst, dst_sdf, g, cell, oi, oj, z, w, beta);
                 }
                 if (!EXACT) {
                     // queue the tie cells; a full queue spills to the global list
@@ -294,7 +214,7 @@ __global__ void __launch_bounds__(128, 4) jfa_pass4_kernel(PlaneSrc src, int32_t
                     const unsigned m = __ballot_sync(0xffffffffu, tie);
                     if (m) {
                         const int before = __popc(m & ((1u << lane) - 1));
-                        if (nfix + __popc(m) <= JFA4_FIXQ) {
+                        if (nfix + __popc(m) <= JFA_TIEQ) {
                             if (tie) fixq[nfix + before] = (int32_t)cell;
                             nfix += __popc(m);
                         } else {
@@ -324,7 +244,7 @@ __global__ void __launch_bounds__(128, 4) jfa_pass4_kernel(PlaneSrc src, int32_t
     }
     if (!EXACT && nfix) {
         __syncwarp();
-        jfa4_flush<FINAL, SLAB>(src, dst, dst_sdf, g, beta, fixq, nfix, lane);
+        jfa_flush_ties<FINAL, SLAB>(src, dst, dst_sdf, g, beta, fixq, nfix, lane);
     }
     if (FINAL && empty_count) {
         for (int o = 16; o; o >>= 1) empties += __shfl_xor_sync(0xffffffffu, empties, o);
