@@ -250,14 +250,14 @@ def run_ours(args, rank, world, local_rank):
     h2d = hv.numel() * 8 + ht.numel() * 4
     d2h = img_host.numel() * 4 + 8
 
-    if not sharded:
-        # every e2e frame consumes its own upload: no flood-ahead of frame f+1
-        pipe.overlap_frames = False
-        torch.cuda.synchronize()  # the flooded-ahead frame has read the mesh buffers
-
     def e2e_step():
-        mb.verts.copy_(hv, non_blocking=True)
-        mb.tris.copy_(ht, non_blocking=True)
+        if not sharded:
+            # pipelined input: frame f + 1's mesh goes up while frame f traces, and
+            # frame f + 1's V + JF (flooded ahead during frame f) reads that upload
+            pipe.upload_mesh(pipe.frame + 1, hv, ht)
+        else:
+            mb.verts.copy_(hv, non_blocking=True)
+            mb.tris.copy_(ht, non_blocking=True)
         if sharded:
             cnt, img = sp.advance(render=True)
             if img is not None:
@@ -286,7 +286,9 @@ def run_ours(args, rank, world, local_rank):
            "d2h_bytes_per_step": d2h,
            "path": ("pinned mesh H2D -> ShardedFramePipeline.advance(render=True) on every rank -> "
                     "image (rank 0) + masked-count D2H") if sharded else
-                   "pinned mesh H2D -> FramePipeline.advance(render=True) -> image + masked-count D2H"}
+                   ("pinned mesh H2D of frame f+1 (FramePipeline.upload_mesh) -> "
+                    "FramePipeline.advance(render=True) of frame f (floods f+1 from that upload) -> "
+                    "image + masked-count D2H")}
     if sharded:  # kernel-level detail below runs on a single-GPU pipeline per rank
         del sp
         torch.cuda.empty_cache()
@@ -367,8 +369,8 @@ def run_ours(args, rank, world, local_rank):
                    "frame_overlap": (None if sharded else
                                      "V + JF of frame f+1 on a flood stream during frame f's RT/DL "
                                      "(static scene, BVH <= 16 MB, double-buffered); frame_stages_ms "
-                                     "come from one serial event-timed frame; off for e2e, whose every "
-                                     "frame uploads its mesh")},
+                                     "come from one serial event-timed frame; e2e uploads frame f+1's "
+                                     "mesh while frame f traces (upload_mesh)")},
         "frame_stages_ms": {k: round(v, 4) for k, v in stages_ms.items()},
         "masked_texels": masked, "rays_per_frame": rays,
         "rays_per_s": round(rays / (sample_ms * 1e-3), 1),

@@ -223,17 +223,52 @@ class FramePipeline:
         return apply_bias(self.coarse, self.cfg.bias)
 
     # --------------------------------------------------------------- frame
-    def _coarse_pass(self, view, s, timer=None):
-        """V (K1) + JF (K2, K3 fused) of `view` into JF buffer set s, on the
-        current stream; returns the coarse SDF buffer."""
+    def upload_mesh(self, frame: int, vertices, triangles):
+        """Stage frame `frame`'s device mesh (static-topology scenes): copies the
+        host arrays (pinned tensors copy asynchronously) into one of two staged
+        buffer sets (frame parity) that that frame's V reads instead of the view's
+        mesh buffers -- so a caller streaming a new mesh every frame can upload
+        frame f + 1 while frame f traces and keep the cross-frame flood overlap.
+        Must be called before the call to advance() that floods `frame` (i.e.
+        before advance(frame - 1) when the overlap is on)."""
+        view = self.scene.view(frame)
+        ref = view.mesh_buffers()
+        st = self.__dict__.setdefault("_staged", [None, None])
+        sf = self.__dict__.setdefault("_staged_frame", [None, None])
+        p = frame % 2
+        if st[p] is None:
+            from .voxel import _MeshBuffers
+
+            st[p] = _MeshBuffers(view.mesh.vertices, view.mesh.triangles)
+        v = vertices if isinstance(vertices, torch.Tensor) else torch.from_numpy(
+            np.ascontiguousarray(vertices, dtype=np.float64))
+        t = triangles if isinstance(triangles, torch.Tensor) else torch.from_numpy(
+            np.ascontiguousarray(triangles, dtype=np.int32))
+        if v.shape != ref.verts.shape or t.shape != ref.tris.shape:
+            raise ValueError("upload_mesh: the staged mesh must match the scene's topology")
+        st[p].verts.copy_(v, non_blocking=True)
+        st[p].tris.copy_(t, non_blocking=True)
+        sf[p] = frame
+
+    def _mesh_for(self, view, frame):
+        sf = self.__dict__.get("_staged_frame")
+        if frame is not None and sf is not None and sf[frame % 2] == frame:
+            return self._staged[frame % 2]
+        return view.mesh_buffers()
+
+    def _coarse_pass(self, view, s, timer=None, frame=None):
+        """V (K1) + JF (K2, K3 fused) of `view` (the staged mesh of `frame` when
+        one was uploaded) into JF buffer set s, on the current stream; returns
+        the coarse SDF buffer."""
         cfg = self.cfg
         timer = timer or _Timer(False, 1)
         js = self._jf_set(s)
+        mb_in = self._mesh_for(view, frame)
         first = self._checked_view is not view
 
         def vox(rep):
             return _voxel.voxelize_seeds(view.mesh, cfg.coarse_dims, (self.scene.lo, self.scene.hi),
-                                         check=first and rep == 0, buffers=view.mesh_buffers(),
+                                         check=first and rep == 0, buffers=mb_in,
                                          out=js["seed_a"])
 
         vox_res = timer.run("V", vox)
@@ -245,7 +280,7 @@ class FramePipeline:
         def flood(rep):
             if rep:  # the flood consumed seed_a: re-voxelize outside the JF timing
                 _voxel.voxelize_seeds(view.mesh, cfg.coarse_dims, (self.scene.lo, self.scene.hi),
-                                      check=False, buffers=view.mesh_buffers(), out=js["seed_a"])
+                                      check=False, buffers=mb_in, out=js["seed_a"])
             return None
 
         def jf(rep):
@@ -264,8 +299,7 @@ class FramePipeline:
         if cur == getattr(self, "_flood", None):
             # buffers allocated on the caller's stream and written here: the
             # allocator must not hand them out again before this work is done
-            mb = view.mesh_buffers()
-            for t in (*js.values(), self._jf_ws, *vars(mb).values()):
+            for t in (*js.values(), self._jf_ws, *vars(mb_in).values()):
                 if isinstance(t, torch.Tensor) and id(t) not in self._flood_marked:
                     t.record_stream(cur)
                     self._flood_marked[id(t)] = t
@@ -298,7 +332,7 @@ class FramePipeline:
         view.mesh_buffers()  # allocated on the caller's stream (see _coarse_pass)
         self._jf_set(frame % 2)
         with torch.cuda.stream(flood):
-            self._coarse_pass(view, frame % 2)
+            self._coarse_pass(view, frame % 2, frame=frame)
             ev = torch.cuda.Event()
             ev.record(flood)
         self._prefetch = (frame, frame % 2, ev)
@@ -424,13 +458,13 @@ class FramePipeline:
             flood.wait_stream(main)
             self._jf_set(frame % 2)
             with torch.cuda.stream(flood):
-                self._coarse_pass(view, frame % 2)
+                self._coarse_pass(view, frame % 2, frame=frame)
                 ev = torch.cuda.Event()
                 ev.record(flood)
             main.wait_event(ev)
             coarse_buf = self._jf_set(frame % 2)["coarse"]
         else:
-            coarse_buf = self._coarse_pass(view, 0, timer)
+            coarse_buf = self._coarse_pass(view, 0, timer, frame=frame)
         self.coarse = DistanceField(coarse_buf, np.asarray(lo, np.float64), np.asarray(hi, np.float64),
                                     beta=cfg.beta)
         if overlap:
@@ -516,7 +550,7 @@ class FramePipeline:
             # the previous frame did not flood this one (e.g. it was serial):
             # flood set p eagerly once
             self._jf_set(p)
-            self._coarse_pass(view, p)
+            self._coarse_pass(view, p, frame=frame)
         if self._frame_dev is None:
             self._frame_dev = torch.zeros(1, dtype=torch.int64, device=b["masked"].device)
         if render:
@@ -527,7 +561,9 @@ class FramePipeline:
         m_cap = self._m_cap
         _rs.sample_workspace(m_cap, cfg.sampling.rays_per_frame)  # no growth inside a capture
         # the view is part of the key: a graph references its mesh / BVH buffers
-        key = (p, bool(render), cam, overlap, m_cap, id(view))
+        staged = self._mesh_for(view, frame + 1) is not view.mesh_buffers() if overlap else \
+            self._mesh_for(view, frame) is not view.mesh_buffers()
+        key = (p, bool(render), cam, overlap, m_cap, id(view), staged)
         graphs = self.__dict__.setdefault("_graphs", {})
         self._frame_dev.fill_(frame)
         mask_old = b["mask_a"] if p == 0 else b["mask_b"]  # eager: frame f reads mask (f - 1) % 2
@@ -543,7 +579,7 @@ class FramePipeline:
             cap_stream = self.__dict__.setdefault("_cap_stream", torch.cuda.Stream())
             n0 = _lib.launch_count()
             with torch.cuda.graph(g, stream=cap_stream):
-                self._graph_body(view, frame, p, render, cam, overlap, b)
+                self._graph_body(view, frame, p, render, cam, overlap, b, staged)
             while len(graphs) >= 8:  # drop the oldest graph (and its view's buffers)
                 graphs.pop(next(iter(graphs)))
             entry = graphs[key] = (g, _lib.launch_count() - n0, view)
@@ -565,7 +601,7 @@ class FramePipeline:
         self.frame += 1
         return rec
 
-    def _graph_body(self, view, frame, p, render, cam, overlap, b):
+    def _graph_body(self, view, frame, p, render, cam, overlap, b, staged=False):
         """The launches of one graph-mode frame (captured once per key)."""
         cfg = self.cfg
         main = torch.cuda.current_stream()
@@ -583,11 +619,12 @@ class FramePipeline:
             flood = self._flood_stream()
             flood.wait_stream(main)
             with torch.cuda.stream(flood):
-                self._coarse_pass(view, 1 - p)  # V + JF of frame + 1 (static scene)
+                # V + JF of frame + 1 (static scene; its staged upload when `staged`)
+                self._coarse_pass(view, 1 - p, frame=frame + 1 if staged else None)
                 flood_done = torch.cuda.Event()
                 flood_done.record(flood)
         else:
-            self._coarse_pass(view, 0)
+            self._coarse_pass(view, 0, frame=frame if staged else None)
         self._rt_pass(view, frame, b, frame_dev=self._frame_dev)
         if render:
             main.wait_event(gb_done)

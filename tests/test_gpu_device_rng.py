@@ -211,3 +211,33 @@ def test_cuda_graph_frames_bit_identical(rt, case, frames):
                 assert y is None
             else:
                 np.testing.assert_array_equal(x, y)
+
+
+def test_staged_mesh_uploads_pipelined_frames(rt):
+    """upload_mesh(f + 1, ...) before advance(f) (the pipelined e2e input):
+    every frame voxelizes its own uploaded mesh, in eager and graph frames,
+    with the flood overlap on -- and equals the reference digests (C1)."""
+    G = golden()
+    scene = rt.get_scene(C1["scene"])
+    pc = rt.PipelineConfig(coarse_dims=C1["dims"], fine_dims=C1["dims"],
+                           sampling=rt.SamplingParams(rays_per_frame=C1["x"]))
+    pipe = rt.FramePipeline(scene, pc)
+    mesh = scene.view(0).mesh
+    hv = torch.from_numpy(mesh.vertices.copy()).pin_memory()
+    ht = torch.from_numpy(mesh.triangles.copy()).pin_memory()
+    pipe.upload_mesh(0, hv, ht)
+    for f in range(6):
+        pipe.upload_mesh(f + 1, hv, ht)
+        rec = pipe.advance(render=f % 2 == 1, timing=False)
+        if f < 3:
+            g = G[f"c1.frame{f}"]
+            assert rec.masked_texels == g["masked"]
+            assert digest(_np(pipe.fine.data)) == g["fine"], f
+    # a staged mesh is really what V reads: a shifted upload changes the field
+    bad = hv.clone() * 1.1  # a larger sphere (a whole-cell shift would keep the count)
+    pipe.upload_mesh(pipe.frame + 1, bad, ht)
+    pipe.advance(timing=False)
+    pipe.join()
+    rec = pipe.advance(timing=False)
+    pipe.join()
+    assert rec.masked_texels != G["c1.frame0"]["masked"]
