@@ -398,6 +398,7 @@ __global__ void linear_to_packed_kernel(const int32_t* __restrict__ l, int32_t* 
 
 #include "jfa2.cuh"
 #include "jfa4.cuh"
+#include "jfa5.cuh"
 
 namespace rtsdf {
 
@@ -535,6 +536,55 @@ static void launch_pass4(PlaneSrc s, int32_t* dst, float* dst_sdf, const JfaGeom
     count_launch(1);
 }
 
+// K2 v5 launch (INT mode, NAT grids): 3-D register tiles (jfa5.cuh), then
+// the exact re-decision of the integer-tie cells (non-EXACT only).
+#ifndef JFA5_RY
+#define JFA5_RY 2
+#endif
+#ifndef JFA5_ZT
+#define JFA5_ZT 2
+#endif
+template <bool FINAL, bool SLAB>
+static void launch_pass5(PlaneSrc s, int32_t* dst, float* dst_sdf, const JfaGeom& g, double beta,
+                         int64_t* empty_count, void* ws, cudaStream_t st) {
+    const int k = g.offset;
+    Jfa5Task T;
+    T.zres = k < g.nz ? k : g.nz;
+    T.zgroups = ((g.nz + k - 1) / k + JFA5_ZT - 1) / JFA5_ZT;
+    T.jres = k < g.ny ? k : g.ny;
+    T.jgroups = ((g.ny + k - 1) / k + JFA5_RY - 1) / JFA5_RY;
+    T.ires = k < g.onx ? k : g.onx;
+    const int64_t nthr = (int64_t)T.zres * T.zgroups * T.jres * T.jgroups;
+    T.tpb = (int)((nthr + 31) / 32 * 32);
+    T.one = 1;
+    T.zero = 0;
+    const int chain_x = (g.onx + k - 1) / k;
+    // segment length L: 2 halo planes per L outputs; halve while the grid
+    // would not fill the GPU for two waves
+    T.L = 24;
+    const int64_t want = (int64_t)num_sms() * 128 * JFA5_MINB * 2;
+    while (T.L > 4 && (int64_t)T.tpb * T.ires * ((chain_x + T.L - 1) / T.L) < want) T.L /= 2;
+    T.isegs = (chain_x + T.L - 1) / T.L;
+    const int64_t threads = (int64_t)T.tpb * T.ires * T.isegs;
+    const unsigned blocks = (unsigned)((threads + 127) / 128);
+    JfaFixList fix = fix_list(ws, (int64_t)g.onx * g.ny * g.nz);
+    if (g.exact) {
+        jfa_pass5_kernel<JFA5_RY, JFA5_ZT, FINAL, SLAB, true><<<blocks, 128, 0, st>>>(s, dst, dst_sdf, g, T, beta, empty_count, fix);
+        count_launch(1);
+        return;
+    }
+    cudaMemsetAsync(fix.count, 0, sizeof(int64_t), st);
+    jfa_pass5_kernel<JFA5_RY, JFA5_ZT, FINAL, SLAB, false><<<blocks, 128, 0, st>>>(s, dst, dst_sdf, g, T, beta, empty_count, fix);
+    jfa_fixup_kernel<FINAL, SLAB><<<(unsigned)(num_sms() * 16), 128, 0, st>>>(
+        s, dst, dst_sdf, g, beta, fix, make_fastdiv((uint32_t)g.nz), make_fastdiv((uint32_t)g.ny));
+    count_launch(2);
+}
+
+#ifndef JFA5_MAXK
+#define JFA5_MAXK 16
+#endif
+static bool use_v5(const JfaGeom& g) { return !g.exact && g.offset <= JFA5_MAXK && natural_empty_ok(g); }
+
 // v4 (jfa4.cuh) vs v2 (jfa2.cuh), measured on B200 (tools/jfa_time.py):
 // EXACT (dyadic spacings, ties resolved in the pass) C4 512^3 late passes
 // 1.21 vs 1.32 ms -> v4.  Non-EXACT C3 (1:4:1) dense passes 0.69 vs 0.56 ms ->
@@ -557,6 +607,9 @@ static int launch_step(PlaneSrc s, int32_t* dst, const JfaGeom& g, bool slab, vo
         if (slab) jfa_step_kernel<JFA_INT, true><<<grid, block, 0, st>>>(s, dst, g);
         else jfa_step_kernel<JFA_INT, false><<<grid, block, 0, st>>>(s, dst, g);
         count_launch();
+    } else if (int_mode && use_v5(g)) {
+        if (slab) launch_pass5<false, true>(s, dst, nullptr, g, 0.0, nullptr, ws, st);
+        else launch_pass5<false, false>(s, dst, nullptr, g, 0.0, nullptr, ws, st);
     } else if (int_mode && use_v4(g)) {
         if (slab) launch_pass4<false, true>(s, dst, nullptr, g, 0.0, nullptr, ws, st);
         else launch_pass4<false, false>(s, dst, nullptr, g, 0.0, nullptr, ws, st);
@@ -776,7 +829,8 @@ static int run_schedule(int32_t* a, int32_t* b, float* sdf_out, int nx, int ny, 
         JfaGeom g{nx, ny, nz, 0, nx, 0, 0, 0, 0, off, hx, hy, hz, wx, wy, wz, exact, 0, nx};
         PlaneSrc s{src, nullptr, nullptr};
         if (sdf_out && off == 1 && int_mode) {  // last pass writes the SDF directly
-            if (use_v4(g)) launch_pass4<true, false>(s, nullptr, sdf_out, g, beta, empty_count, ws, st);
+            if (use_v5(g)) launch_pass5<true, false>(s, nullptr, sdf_out, g, beta, empty_count, ws, st);
+            else if (use_v4(g)) launch_pass4<true, false>(s, nullptr, sdf_out, g, beta, empty_count, ws, st);
             else launch_pass2<true, false>(s, nullptr, sdf_out, g, beta, empty_count, ws, st);
             publish_counts(hist, slots, st);
             return check_launch("jfa_run_sdf");
