@@ -479,8 +479,14 @@ static void launch_pass2(PlaneSrc s, int32_t* dst, float* dst_sdf, const JfaGeom
         jfa_pass2_kernel<2, FINAL, SLAB, false><<<blocks, 128, 0, st>>>(s, dst, dst_sdf, g, T, beta, empty_count, fix);
     else
         jfa_pass2_kernel<1, FINAL, SLAB, false><<<blocks, 128, 0, st>>>(s, dst, dst_sdf, g, T, beta, empty_count, fix);
-    jfa_fixup_kernel<FINAL, SLAB><<<(unsigned)(num_sms() * 16), 128, 0, st>>>(
-        s, dst, dst_sdf, g, beta, fix, make_fastdiv((uint32_t)g.nz), make_fastdiv((uint32_t)g.ny));
+    // a flagged cell's seed output holds a tied winner (a seed at its minimum
+    // key): the one-loop fix-up; the FINAL pass writes no seeds -> the full one
+    if (FINAL)
+        jfa_fixup_kernel<FINAL, SLAB><<<(unsigned)(num_sms() * 16), 128, 0, st>>>(
+            s, dst, dst_sdf, g, beta, fix, make_fastdiv((uint32_t)g.nz), make_fastdiv((uint32_t)g.ny));
+    else
+        jfa_fixup_w_kernel<FINAL, SLAB><<<(unsigned)(num_sms() * 16), 128, 0, st>>>(
+            s, dst, dst_sdf, g, beta, fix, make_fastdiv((uint32_t)g.nz), make_fastdiv((uint32_t)g.ny));
     count_launch(2);
 }
 
@@ -575,7 +581,7 @@ static void launch_pass5(PlaneSrc s, int32_t* dst, float* dst_sdf, const JfaGeom
     }
     cudaMemsetAsync(fix.count, 0, sizeof(int64_t), st);
     jfa_pass5_kernel<JFA5_RY, JFA5_ZT, FINAL, SLAB, false><<<blocks, 128, 0, st>>>(s, dst, dst_sdf, g, T, beta, empty_count, fix);
-    jfa_fixup_kernel<FINAL, SLAB><<<(unsigned)(num_sms() * 16), 128, 0, st>>>(
+    jfa_fixup_w_kernel<FINAL, SLAB><<<(unsigned)(num_sms() * 16), 128, 0, st>>>(
         s, dst, dst_sdf, g, beta, fix, make_fastdiv((uint32_t)g.nz), make_fastdiv((uint32_t)g.ny));
     count_launch(2);
 }
@@ -829,7 +835,8 @@ static int run_schedule(int32_t* a, int32_t* b, float* sdf_out, int nx, int ny, 
         JfaGeom g{nx, ny, nz, 0, nx, 0, 0, 0, 0, off, hx, hy, hz, wx, wy, wz, exact, 0, nx};
         PlaneSrc s{src, nullptr, nullptr};
         if (sdf_out && off == 1 && int_mode) {  // last pass writes the SDF directly
-            if (use_v5(g)) launch_pass5<true, false>(s, nullptr, sdf_out, g, beta, empty_count, ws, st);
+            // v5 leaves the tied winners of the flagged cells in the free buffer
+            if (use_v5(g)) launch_pass5<true, false>(s, dst, sdf_out, g, beta, empty_count, ws, st);
             else if (use_v4(g)) launch_pass4<true, false>(s, nullptr, sdf_out, g, beta, empty_count, ws, st);
             else launch_pass2<true, false>(s, nullptr, sdf_out, g, beta, empty_count, ws, st);
             publish_counts(hist, slots, st);

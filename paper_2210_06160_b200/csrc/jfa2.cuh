@@ -490,4 +490,74 @@ __global__ void __launch_bounds__(128, JFA_FIX_MINB) jfa_fixup_kernel(PlaneSrc s
     }
 }
 
+// Re-decide the flagged cells of the v5 pass (jfa5.cuh).  The pass stored, for
+// each flagged cell, W = a seed at the cell's minimum integer key K* (in the
+// seed output; the FINAL pass in the free ping-pong buffer), so one loop over
+// the 27 taps suffices: the candidates at K* are the seeds with that key, and
+// the reference's rule (fp64 d2, then lexicographic; jfa.py:108-124) picks
+// among them -- a strictly larger integer key is a strictly larger exact d2,
+// which fp64 rounding cannot invert.  About a third of jfa_fixup_kernel's
+// instructions (no separate minimum pass).
+template <bool FINAL, bool SLAB>
+__global__ void __launch_bounds__(128, JFA_FIX_MINB) jfa_fixup_w_kernel(PlaneSrc src, int32_t* __restrict__ wbuf,
+                                                         float* __restrict__ dst_sdf, JfaGeom g,
+                                                         double beta, JfaFixList fix, FastDiv dnz,
+                                                         FastDiv dny) {
+    const int64_t n = min(*fix.count, fix.cap);
+    const int64_t plane = (int64_t)g.ny * g.nz;
+    const int k = g.offset;
+    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n;
+         q += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t cell = (uint32_t)fix.cells[q];
+        const uint32_t row = fdiv(cell, dnz);
+        const int z = (int)(cell - row * dnz.d);
+        const uint32_t il = fdiv(row, dny);
+        const int j = (int)(row - il * dny.d);
+        const int i = g.ox0 + (int)il;
+        const int32_t w0 = wbuf[cell];
+        const int32_t* pl[3];
+#pragma unroll
+        for (int di = 0; di < 3; ++di) {
+            const int qi = i + (di - 1) * k;
+            pl[di] = nullptr;
+            if (qi >= 0 && qi < g.nx)
+                pl[di] = SLAB ? plane_ptr(src, g, qi, plane) : src.local + (int64_t)qi * plane;
+        }
+        const bool jok[3] = {j - k >= 0, true, j + k < g.ny};
+        const bool zok[3] = {z - k >= 0, true, z + k < g.nz};
+        int32_t c[27];
+#pragma unroll
+        for (int di = 0; di < 3; ++di)
+#pragma unroll
+            for (int dj = 0; dj < 3; ++dj)
+#pragma unroll
+                for (int dk = 0; dk < 3; ++dk) {
+                    const bool ok = pl[di] != nullptr && jok[dj] && zok[dk];
+                    const int off = (j + (dj - 1) * k) * g.nz + z + (dk - 1) * k;
+                    c[(di * 3 + dj) * 3 + dk] = ok ? __ldg(pl[di] + off) : RTSDF_EMPTY;
+                }
+        auto ikey = [&](int32_t v) {
+            const int dx = i - unpack_i(v), dy = j - unpack_j(v), dz = z - unpack_k(v);
+            return g.wx * dx * dx + g.wy * dy * dy + g.wz * dz * dz;
+        };
+        const int ks = ikey(w0);
+        int32_t best = w0;
+        double bd = center_d2(i - unpack_i(w0), j - unpack_j(w0), z - unpack_k(w0), g.hx, g.hy, g.hz);
+#pragma unroll
+        for (int t = 0; t < 27; ++t) {
+            const int32_t v = c[t];
+            if (v == RTSDF_EMPTY || v == best || ikey(v) != ks) continue;
+            const double d2 = center_d2(i - unpack_i(v), j - unpack_j(v), z - unpack_k(v), g.hx, g.hy, g.hz);
+            if (d2 < bd || (d2 == bd && v < best)) {
+                best = v;
+                bd = d2;
+            }
+        }
+        if (FINAL)
+            dst_sdf[cell] = (float)__dsub_rn(__dsqrt_rn(bd), beta);
+        else
+            wbuf[cell] = best;
+    }
+}
+
 }  // namespace rtsdf

@@ -25,7 +25,9 @@
 // real key (natural_empty_ok), so EMPTY taps need no test either.
 //
 // Integer ties between distinct seeds mark the output (odd Km) and are
-// re-decided by jfa2.cuh's jfa_fixup_kernel with the reference's fp64 rule.
+// re-decided by jfa2.cuh's jfa_fixup_w_kernel with the reference's fp64 rule;
+// the pass leaves the cell's tied winner W (a seed at the minimum key) in the
+// seed output for it (FINAL: in the free ping-pong buffer `dst`).
 #pragma once
 #include "jfa2.cuh"
 
@@ -231,6 +233,14 @@ __global__ void __launch_bounds__(128, JFA5_MINB)
                     if (!EXACT) tie |= (unsigned)(w != RTSDF_EMPTY && (Km[0][b][m] & 1)) << (b * ZT + m);
                 }
             tie &= okmask;
+            if (FINAL && !EXACT && tie) {
+                // the fix-up's witness of K* (a tied winner), in the free ping-pong buffer
+#pragma unroll
+                for (int b = 0; b < RY; ++b)
+#pragma unroll
+                    for (int m = 0; m < ZT; ++m)
+                        if ((tie >> (b * ZT + m)) & 1u) dplane[(unsigned)(b * kz + m * k)] = W[0][b][m];
+            }
             // integer ties between distinct seeds: one warp-aggregated append
             if (!EXACT && __any_sync(0xffffffffu, tie != 0)) {
                 const int cnt = __popc(tie);
