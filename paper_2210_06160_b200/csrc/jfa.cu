@@ -567,9 +567,12 @@ static void launch_pass5(PlaneSrc s, int32_t* dst, float* dst_sdf, const JfaGeom
     const int chain_x = (g.onx + k - 1) / k;
     // segment length L: 2 halo planes per L outputs; halve while the grid
     // would not fill the GPU for two waves
-    T.L = 24;
+    // balanced segments of <= 32 planes (each costs L + 2 plane steps), more
+    // of them while the grid would not fill the GPU for two waves
     const int64_t want = (int64_t)num_sms() * 128 * JFA5_MINB * 2;
-    while (T.L > 4 && (int64_t)T.tpb * T.ires * ((chain_x + T.L - 1) / T.L) < want) T.L /= 2;
+    T.isegs = (chain_x + 31) / 32;
+    while ((chain_x + T.isegs - 1) / T.isegs > 4 && (int64_t)T.tpb * T.ires * T.isegs < want) ++T.isegs;
+    T.L = (chain_x + T.isegs - 1) / T.isegs;
     T.isegs = (chain_x + T.L - 1) / T.L;
     const int64_t threads = (int64_t)T.tpb * T.ires * T.isegs;
     const unsigned blocks = (unsigned)((threads + 127) / 128);
@@ -587,7 +590,7 @@ static void launch_pass5(PlaneSrc s, int32_t* dst, float* dst_sdf, const JfaGeom
 }
 
 #ifndef JFA5_MAXK
-#define JFA5_MAXK 16
+#define JFA5_MAXK 16  // k = 32 / 64 inputs still hold EMPTY regions: v2's all-EMPTY tap votes win there (measured)
 #endif
 static bool use_v5(const JfaGeom& g) { return !g.exact && g.offset <= JFA5_MAXK && natural_empty_ok(g); }
 
