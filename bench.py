@@ -116,7 +116,9 @@ def peaks():
     return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-PROFILE = ROOT / "profiles" / "r2_frame_kernels_summary.csv"  # ncu --set full, one C3 frame
+PROFILE = ROOT / "profiles" / "r2x_frame_kernels_summary.csv"  # ncu --set full, one C3 frame
+DENSE_KERNEL = "jfa_pass5_kernel<2, 2, 0"  # K2 v5 (jfa5.cuh), the dense passes k <= 16
+DENSE_MAX_K = 16
 
 
 def _profile_rows(prefix):
@@ -130,9 +132,9 @@ def _profile_rows(prefix):
 
 
 def jfa_traffic():
-    """DRAM bytes (read + write) per dense JFA pass launch (v2, k <= 64) from the
+    """DRAM bytes (read + write) per dense JFA pass launch (v5, k <= 16) from the
     committed ncu --set full capture of one frame."""
-    head, rows = _profile_rows("jfa_pass2_kernel<4, 0")
+    head, rows = _profile_rows(DENSE_KERNEL)
     if not rows:
         return None, None
     rd, wr = head.index("dram_rd[MB]"), head.index("dram_wr[MB]")
@@ -144,7 +146,7 @@ def issue_roofline(n_cells, pass_ms, ck):
     """The JFA pass's binding limit: instruction issue.  Warp instructions per
     dense pass launch from the committed capture; peak = 148 SMs x 4 schedulers
     x 1 warp instruction per clock at the measured SM clock."""
-    head, rows = _profile_rows("jfa_pass2_kernel<4, 0")
+    head, rows = _profile_rows(DENSE_KERNEL)
     if not rows:
         return None
     ii = head.index("inst")
@@ -333,8 +335,8 @@ def run_ours(args, rank, world, local_rank):
     jfa_ms = float(np.median(sched))
     n_cells = int(np.prod(DIMS))
     gvox = n_cells * len(offs) / (jfa_ms * 1e-3) / 1e9
-    # roofline of the pass kernel: its dense launches (k <= 64, v2 + tie fix-up)
-    dense = [float(t) for off, t in zip(offs, per_pass) if off <= 64]
+    # roofline of the pass kernel: its dense launches (k <= 16: v5 + its tie fix-up)
+    dense = [float(t) for off, t in zip(offs, per_pass) if off <= DENSE_MAX_K]
     pass_ms = float(np.mean(dense)) if dense else float(np.mean(per_pass))
     hbm, hbm_src = peaks()
     jfa_gbs = gvox * 8.0
@@ -381,7 +383,8 @@ def run_ours(args, rank, world, local_rank):
                 "gvox_pass_per_s": round(gvox, 2), "achieved_gbs": round(jfa_gbs, 1),
                 "hbm_frac": round(jfa_gbs / hbm, 4), "weights": list(w),
                 "algorithmic_bytes_per_voxel_pass": 8},
-        "roofline": {"kernel": "jfa_pass2_kernel (K2, dense passes k <= 64)", "bound": "hbm",
+        "roofline": {"kernel": "jfa_pass5_kernel (K2 v5, dense passes k <= 16; launch_ms includes "
+                               "its tie fix-up kernel)", "bound": "hbm",
                      "binding_limit": "instruction issue (see issue_roofline)",
                      "achieved": round(n_cells * 8 / (pass_ms * 1e-3) / 1e9, 1),
                      "peak": hbm, "unit": "GB/s",
@@ -392,9 +395,10 @@ def run_ours(args, rank, world, local_rank):
                      "algorithmic_bytes_per_launch": n_cells * 8, "peak_source": hbm_src,
                      "dominant_kernel": dominant,
                      "issue_roofline": issue_roofline(n_cells, pass_ms, ck),
-                     "note": "frac is against HBM as the contract asks; the pass is instruction-issue "
-                             "bound: 27 exact candidates per cell at >= 6 instructions each "
-                             "(candidate_floor_instr_per_cell) put its issue floor far above the "
+                     "note": "frac is against HBM as the contract asks; the pass is bound by its two "
+                             "half-rate integer pipes (ALU + FMA, ~85 % issue): 27 exact candidates "
+                             "per cell at 6 instructions each, 3 per pipe "
+                             "(candidate_floor_instr_per_cell), put its issue floor far above the "
                              "HBM floor (DESIGN.md section 7)"},
         "roofline_sampler": sampler_roofline(rays, sample_ms),
         "kernels_ms": {k: round(v, 4) for k, v in kernels_ms.items()},
