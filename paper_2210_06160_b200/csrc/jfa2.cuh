@@ -503,6 +503,7 @@ __global__ void __launch_bounds__(128, JFA_FIX_MINB) jfa_fixup_w_kernel(PlaneSrc
                                                          float* __restrict__ dst_sdf, JfaGeom g,
                                                          double beta, JfaFixList fix, FastDiv dnz,
                                                          FastDiv dny) {
+    __shared__ int32_t fix_lst[26 * 128];  // per-thread list of tied seeds (stride 128)
     const int64_t n = min(*fix.count, fix.cap);
     const int64_t plane = (int64_t)g.ny * g.nz;
     const int k = g.offset;
@@ -541,12 +542,21 @@ __global__ void __launch_bounds__(128, JFA_FIX_MINB) jfa_fixup_w_kernel(PlaneSrc
             return g.wx * dx * dx + g.wy * dy * dy + g.wz * dz * dz;
         };
         const int ks = ikey(w0);
-        int32_t best = w0;
-        double bd = center_d2(i - unpack_i(w0), j - unpack_j(w0), z - unpack_k(w0), g.hx, g.hy, g.hz);
+        // the other seeds at K* (integer filter, uniform over the warp), listed in
+        // shared memory; then the fp64 rule over the short list -- the divergent
+        // fp64 work runs max-over-warp(list length) times, not once per tap
+        int32_t* lst = fix_lst + threadIdx.x;
+        int nl = 0;
 #pragma unroll
         for (int t = 0; t < 27; ++t) {
             const int32_t v = c[t];
-            if (v == RTSDF_EMPTY || v == best || ikey(v) != ks) continue;
+            const bool m = v != RTSDF_EMPTY && v != w0 && ikey(v) == ks;
+            if (m) lst[(nl++) * 128] = v;
+        }
+        int32_t best = w0;
+        double bd = center_d2(i - unpack_i(w0), j - unpack_j(w0), z - unpack_k(w0), g.hx, g.hy, g.hz);
+        for (int q = 0; q < nl; ++q) {
+            const int32_t v = lst[q * 128];
             const double d2 = center_d2(i - unpack_i(v), j - unpack_j(v), z - unpack_k(v), g.hx, g.hy, g.hz);
             if (d2 < bd || (d2 == bd && v < best)) {
                 best = v;
