@@ -315,7 +315,7 @@ __global__ void __launch_bounds__(128) ray_query_fast_kernel(
 
 __global__ void __launch_bounds__(128) ray_query_fast4_kernel(
     FastBvh4 b, const double* __restrict__ orig, const double* __restrict__ dirs, int64_t n,
-    double t_max, double* __restrict__ out_t, int32_t* __restrict__ out_id,
+    double t_max, float tb, double* __restrict__ out_t, int32_t* __restrict__ out_id,
     int32_t* __restrict__ out_facing) {
     __shared__ int32_t stack_mem[RTSDF_FAST_STACK * 128];
     __shared__ __half tstack_mem[RTSDF_FAST_STACK * 128];
@@ -326,7 +326,7 @@ __global__ void __launch_bounds__(128) ray_query_fast4_kernel(
     // the long-ray traversal of the sampler's pass 2 (brute-force-equivalence tested)
     double t = trace_fast4_ww(b, orig[3 * q], orig[3 * q + 1], orig[3 * q + 2], dirs[3 * q],
                               dirs[3 * q + 1], dirs[3 * q + 2], t_max, stack_mem + threadIdx.x,
-                              tstack_mem + threadIdx.x, 128, id, facing);
+                              tstack_mem + threadIdx.x, 128, id, facing, tb);
     out_t[q] = t;
     out_id[q] = id;
     out_facing[q] = facing;
@@ -539,7 +539,7 @@ extern "C" int rtsdf_ray_query(const void* packed, int64_t n_nodes, int64_t n_tr
     if (n <= 0) return RTSDF_OK;
     if (fast == 2)
         ray_query_fast4_kernel<<<(unsigned)((n + 127) / 128), 128, 0, (cudaStream_t)stream>>>(
-            fast_bvh4_view(packed, n_nodes, n_tris), origins, dirs, n, t_max, out_t, out_id,
+            fast_bvh4_view(packed, n_nodes, n_tris), origins, dirs, n, t_max, tmax_bound(t_max), out_t, out_id,
             out_facing);
     else if (fast)
         ray_query_fast_kernel<<<(unsigned)((n + 127) / 128), 128, 0, (cudaStream_t)stream>>>(

@@ -255,7 +255,7 @@ __device__ __forceinline__ double wf_trace(const SampleParams& P, double ox, dou
                                            bool* done) {
     if (WIDE)
         return trace_fast4(P.bvh4, ox, oy, oz, dx, dy, dz, P.t_max, stack, tstack, WF_THREADS, id,
-                           facing, budget, done, P.tb);
+                           facing, P.tb, budget, done);
     return trace_fast(P.bvh, ox, oy, oz, dx, dy, dz, P.t_max, stack, WF_THREADS, id, facing,
                       budget, done);
 }

@@ -326,8 +326,8 @@ __device__ __forceinline__ bool leaf_tris(const FastTri* __restrict__ tris, cons
 __device__ __forceinline__ double trace_fast4(const FastBvh4& b, double ox, double oy, double oz,
                                               double dx, double dy, double dz, double t_max,
                                               int32_t* stack, __half* tstack, int stride,
-                                              int32_t& out_id, int& out_facing, int budget = 0,
-                                              bool* complete = nullptr, float tb0 = -1.0f) {
+                                              int32_t& out_id, int& out_facing, float tb0,
+                                              int budget = 0, bool* complete = nullptr) {
     RayF r;
     r.ix = clamp_inv(dx);
     r.iy = clamp_inv(dy);
@@ -339,7 +339,7 @@ __device__ __forceinline__ double trace_fast4(const FastBvh4& b, double ox, doub
     double best_t = t_max;
     int32_t best_id = -1;
     int best_facing = 0;
-    float tb = tb0 >= 0.0f ? tb0 : tmax_bound(t_max);
+    float tb = tb0;  // tmax_bound(t_max), computed once by the caller
     int sp = 0;
     int32_t node = 0;
     if (complete) *complete = true;
@@ -414,7 +414,7 @@ __device__ __forceinline__ double trace_fast4_ww(const FastBvh4& b, double ox, d
                                                  double oz, double dx, double dy, double dz,
                                                  double t_max, int32_t* stack, __half* tstack,
                                                  int stride, int32_t& out_id, int& out_facing,
-                                                 float tb0 = -1.0f) {
+                                                 float tb0) {
     RayF r;
     r.ix = clamp_inv(dx);
     r.iy = clamp_inv(dy);
@@ -426,7 +426,7 @@ __device__ __forceinline__ double trace_fast4_ww(const FastBvh4& b, double ox, d
     double best_t = t_max;
     int32_t best_id = -1;
     int best_facing = 0;
-    float tb = tb0 >= 0.0f ? tb0 : tmax_bound(t_max);
+    float tb = tb0;  // tmax_bound(t_max), computed once by the caller
     int sp = 0;
     auto pop = [&]() -> int32_t {
         while (sp > 0) {
