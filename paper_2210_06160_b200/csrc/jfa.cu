@@ -592,15 +592,20 @@ static void launch_pass5(PlaneSrc s, int32_t* dst, float* dst_sdf, const JfaGeom
 #ifndef JFA5_MAXK
 #define JFA5_MAXK 16  // k = 32 / 64 inputs still hold EMPTY regions: v2's all-EMPTY tap votes win there (measured)
 #endif
-static bool use_v5(const JfaGeom& g) { return !g.exact && g.offset <= JFA5_MAXK && natural_empty_ok(g); }
+#ifndef JFA5_MAXK_EXACT
+#define JFA5_MAXK_EXACT 32  // dyadic grids (no tie fix-up): v5 measured ahead of v4 up to k = 32
+#endif
+static bool use_v5(const JfaGeom& g) {
+    return g.offset <= (g.exact ? JFA5_MAXK_EXACT : JFA5_MAXK) && natural_empty_ok(g);
+}
 
-// v4 (jfa4.cuh) vs v2 (jfa2.cuh), measured on B200 (tools/jfa_time.py):
-// EXACT (dyadic spacings, ties resolved in the pass) C4 512^3 late passes
-// 1.21 vs 1.32 ms -> v4.  Non-EXACT C3 (1:4:1) dense passes 0.69 vs 0.56 ms ->
-// v2: both sit at the ~6-instruction-per-candidate floor (27 per cell), and
-// v4's saving on loads / decode (own column only) is outweighed by its halo
-// lanes, its in-kernel tie fix-ups and instruction-cache misses
-// (profiles/r2_jfa_v4_vs_v2.txt).
+// Pass kernel by offset and grid, measured on B200 (tools/jfa_time.py):
+//   v5 (jfa5.cuh, 2 x 2 register tiles): k <= 16 (non-EXACT; C3 0.34 ms per
+//      dense pass vs v2's 0.46) and k <= 32 on EXACT (dyadic) grids (C4 late
+//      passes 1.01 vs v4's 1.21 ms, C5 7.8 vs 9.2 ms);
+//   v2 (jfa2.cuh): non-EXACT k >= 32, whose inputs still hold EMPTY regions
+//      (its all-EMPTY tap votes: C3 k = 32 0.375 vs v5's 0.403 ms);
+//   v4 (jfa4.cuh): EXACT k >= 64 (C4 k = 64 1.04 vs v5's 1.19 ms).
 static bool use_v4(const JfaGeom& g) { return g.exact; }
 
 static int launch_step(PlaneSrc s, int32_t* dst, const JfaGeom& g, bool slab, void* ws,
