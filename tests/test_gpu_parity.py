@@ -134,6 +134,11 @@ def test_jfa_every_pass_matches_oracle(rt, name, dims):
     ((64, 48, 80), (0.512, 0.768, 0.64), 0.01, (1, 4, 1)),
     # dyadic spacing 1/128: fp64 d2 exact -> EXACT mode (64-bit lexicographic test)
     ((64, 48, 80), (0.5, 0.375, 0.625), 0.01, (1, 1, 1)),
+    # ragged grids for v5's 2 x 2 register tiles (jfa5.cuh): chains shorter than a
+    # tile, odd extents, offsets beyond an axis -- every clamped tap and masked output
+    ((37, 23, 51), (0.37, 0.46, 0.51), 0.02, (1, 4, 1)),
+    ((5, 70, 3), (0.05, 1.4, 0.03), 0.05, (1, 4, 1)),
+    ((3, 41, 66), (0.096, 1.312, 2.112), 0.03, (1, 1, 1)),
 ])
 def test_jfa_random_occupancy_every_pass_and_schedule(rt, dims, hi, frac, weights):
     """Random seeds, non-dyadic spacings (INT mode with tie marks + fix-ups):
