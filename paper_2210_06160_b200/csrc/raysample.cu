@@ -171,6 +171,9 @@ struct WfBuffers {
     uint32_t* votes;           // [m_cap]
     int32_t* queue;            // [R] rays needing the full search
     int64_t* qcount;
+    const int64_t* texels;      // the masked-texel count (device): chunks of rays beyond
+    int64_t m_cap;              // min(count, m_cap) * x were not written by this call's pass 1
+    int x;
     bool aligned;              // x divides 32: a warp of pass 1 holds whole texels
     double4* tex;              // [m_cap] per texel: origin xyz + RNG stream key (bits)
     // Pass-2 order: the long rays sorted by (direction octant, ray id).  Pass 1
@@ -349,6 +352,14 @@ __global__ void __launch_bounds__(WF_THREADS, WF_MINB) wf_pass1_kernel(SamplePar
     }
 }
 
+// chunks this call's pass 1 wrote: the workspace is sized for the capacity,
+// and records beyond the actual rays are stale (an earlier call's or never
+// written) -- they must not enter the queue
+__device__ __forceinline__ int64_t wf_live_chunks(const WfBuffers& B, int64_t n_chunks) {
+    const int64_t R = min(*B.texels, B.m_cap) * B.x;
+    return min(n_chunks, (R + 31) / 32);
+}
+
 // long rays of a chunk in octant o
 __device__ __forceinline__ unsigned oct_mask(const uint4& c, int o) {
     return c.x & (o & 1 ? c.y : ~c.y) & (o & 2 ? c.z : ~c.z) & (o & 4 ? c.w : ~c.w);
@@ -390,7 +401,7 @@ __global__ void __launch_bounds__(WF_OCT_THREADS) wf_oct_count_kernel(int64_t n_
     __shared__ int warp_tot[8 * (WF_OCT_THREADS / 32)];
     __shared__ int tot[8];
     const int64_t c = (int64_t)blockIdx.x * WF_OCT_THREADS + threadIdx.x;
-    const uint4 ch = c < n_chunks ? B.chunk[c] : make_uint4(0, 0, 0, 0);
+    const uint4 ch = c < wf_live_chunks(B, n_chunks) ? B.chunk[c] : make_uint4(0, 0, 0, 0);
     int cnt[8], excl[8];
 #pragma unroll
     for (int o = 0; o < 8; ++o) cnt[o] = __popc(oct_mask(ch, o));
@@ -427,7 +438,7 @@ __global__ void __launch_bounds__(WF_OCT_THREADS) wf_oct_scatter_kernel(int64_t 
     __shared__ int tot[8];
     __shared__ int32_t stage[WF_OCT_THREADS * 32];
     const int64_t c = (int64_t)blockIdx.x * WF_OCT_THREADS + threadIdx.x;
-    const uint4 ch = c < n_chunks ? B.chunk[c] : make_uint4(0, 0, 0, 0);
+    const uint4 ch = c < wf_live_chunks(B, n_chunks) ? B.chunk[c] : make_uint4(0, 0, 0, 0);
     int cnt[8], excl[8];
     unsigned om[8];
 #pragma unroll
@@ -644,6 +655,9 @@ extern "C" int rtsdf_sample_update(const void* bvh_packed, int64_t n_nodes, int6
         p += (nob * 8 * sizeof(int32_t) + 255) / 256 * 256;
         B.scan_tmp = p;
         B.scan_tmp_bytes = oct_scan_temp_bytes(nob);
+        B.texels = count;
+        B.m_cap = m_cap;
+        B.x = x;
         B.aligned = 32 % x == 0;
         cudaMemsetAsync(B.qcount, 0, sizeof(int64_t), st);
         int64_t blocks = (R + WF_THREADS - 1) / WF_THREADS;
