@@ -155,7 +155,9 @@ __global__ void __launch_bounds__(SAMPLE_THREADS) sample_update_kernel(SamplePar
 #define WF_MINB 6  // resident blocks per SM the tracer kernels are compiled for
 #endif
 #define WF_BUDGET 4   // binary search tree: internal-node visits in pass 1
-#define WF_BUDGET4 2  // BVH4: root only (ground-plane leaves finish in pass 1)
+#ifndef WF_BUDGET4
+#define WF_BUDGET4 2  // BVH4: root only (ground-plane leaves finish in pass 1); C3 pass 1 + 2:
+#endif                // budget 2 5.16 ms, 3 5.31, 4 5.35, 6 5.80 (measured)
 #ifndef WF_B2_PER_SM
 #define WF_B2_PER_SM 12  // pass-2 blocks per SM (grid-stride over the long-ray queue)
 #endif
@@ -268,7 +270,7 @@ __device__ __forceinline__ double wf_trace(const SampleParams& P, double ox, dou
 // shared stack suffices (measured: no change at 6 / 7 / 8 resident blocks; a
 // two-chunk form that generates both chunks' directions before tracing, for
 // fp64 ILP, measured 2.55 -> 2.69 ms).
-#define WF1_STACK 4
+#define WF1_STACK (3 * (WF_BUDGET4 - 1) > WF_BUDGET - 1 ? 3 * (WF_BUDGET4 - 1) : WF_BUDGET - 1)
 static_assert(WF1_STACK >= WF_BUDGET - 1 && WF1_STACK >= 3 * (WF_BUDGET4 - 1), "pass-1 stack");
 template <bool WIDE>
 __global__ void __launch_bounds__(WF_THREADS, WF_MINB) wf_pass1_kernel(SampleParams P, WfBuffers B, int budget) {
