@@ -253,11 +253,81 @@ __device__ __forceinline__ void wf_ray(const SampleParams& P, const WfBuffers& B
     }
 }
 
+// Pass 1 on a BVH4 with budget 2 (root only), without trace_fast4's stack,
+// pops and budget bookkeeping: the root's four child boxes, then its children
+// in near-first order while within reach (entry <= the best hit so far): a
+// leaf is tested, an inner child ends pass 1 for the ray (pass 2 traces it
+// from the root) -- trace_fast4's order and outcome with node budget 2.  A box
+// entry is a lower bound on every hit inside it, so the unreached children
+// cannot hold a closer hit than the one found.
+__device__ __forceinline__ double wf_trace4_root(const SampleParams& P, double ox, double oy, double oz,
+                                                 double dx, double dy, double dz, int32_t& out_id,
+                                                 int& out_facing, bool* done) {
+    RayF r;
+    r.ix = clamp_inv(dx);
+    r.iy = clamp_inv(dy);
+    r.iz = clamp_inv(dz);
+    r.oix = (float)ox * r.ix;
+    r.oiy = (float)oy * r.iy;
+    r.oiz = (float)oz * r.iz;
+    const float fdx = (float)dx, fdy = (float)dy, fdz = (float)dz;
+    double best_t = P.t_max;
+    int32_t best_id = -1;
+    int best_facing = 0;
+    float tb = P.tb;
+    const FastNode4* nd = P.bvh4.nodes;
+    const float4 lx = __ldg((const float4*)nd->lox), ly = __ldg((const float4*)nd->loy),
+                 lz = __ldg((const float4*)nd->loz), hx = __ldg((const float4*)nd->hix),
+                 hy = __ldg((const float4*)nd->hiy), hz = __ldg((const float4*)nd->hiz);
+    const int4 ch = __ldg((const int4*)nd->child);
+    float t[4];
+    t[0] = box_entry(lx.x, ly.x, lz.x, hx.x, hy.x, hz.x, r, tb);
+    t[1] = box_entry(lx.y, ly.y, lz.y, hx.y, hy.y, hz.y, r, tb);
+    t[2] = box_entry(lx.z, ly.z, lz.z, hx.z, hy.z, hz.z, r, tb);
+    t[3] = box_entry(lx.w, ly.w, lz.w, hx.w, hy.w, hz.w, r, tb);
+    const int32_t c[4] = {ch.x, ch.y, ch.z, ch.w};
+    // near-first over the reachable children: an inner child first in line ends
+    // pass 1 for this ray (pass 2 traces it from the root); a leaf is tested
+    bool need = false;
+#pragma unroll
+    for (int it = 0; it < 4; ++it) {
+        int qn = -1;
+        float tn = RTSDF_FINF;
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+            if (t[q] < tn) {
+                tn = t[q];
+                qn = q;
+            }
+        if (qn < 0 || !(tn <= tb)) break;
+        int32_t cn = c[0];
+#pragma unroll
+        for (int q = 1; q < 4; ++q) cn = qn == q ? c[q] : cn;
+        if (cn >= 0) {
+            need = true;
+            break;
+        }
+        leaf_tris(P.bvh4.tris, P.bvh4.exact, cn, ox, oy, oz, dx, dy, dz, fdx, fdy, fdz, best_t, best_id,
+                  best_facing, tb);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) t[q] = qn == q ? RTSDF_FINF : t[q];
+    }
+    *done = !need;
+    out_id = best_id;
+    out_facing = best_facing;
+    return best_id < 0 ? -1.0 : best_t;
+}
+
 template <bool WIDE>
 __device__ __forceinline__ double wf_trace(const SampleParams& P, double ox, double oy, double oz,
                                            double dx, double dy, double dz, int32_t* stack,
                                            __half* tstack, int32_t& id, int& facing, int budget,
                                            bool* done) {
+#ifndef WF1_ROOT
+#define WF1_ROOT 1
+#endif
+    if (WIDE && WF1_ROOT && budget == 2)
+        return wf_trace4_root(P, ox, oy, oz, dx, dy, dz, id, facing, done);
     if (WIDE)
         return trace_fast4(P.bvh4, ox, oy, oz, dx, dy, dz, P.t_max, stack, tstack, WF_THREADS, id,
                            facing, P.tb, budget, done);
