@@ -241,3 +241,47 @@ def test_staged_mesh_uploads_pipelined_frames(rt):
     rec = pipe.advance(timing=False)
     pipe.join()
     assert rec.masked_texels != G["c1.frame0"]["masked"]
+
+
+def test_sampler_capacity_headroom_after_a_larger_call(rt):
+    """The wavefront workspace is sized for a texel CAPACITY; records beyond the
+    actual rays hold whatever an earlier, larger call left there.  A call with
+    headroom (m_cap > count) after a larger one must ignore them (the octant
+    queue reads only the chunks this call's pass 1 wrote) and still equal the
+    oracle bit for bit."""
+    from paper_2210_06160_b200 import raysample as RS
+
+    # a larger call first: fills the shared workspace with its chunk records
+    big, _ = scene_mesh("sphere_plane")
+    dims_big = (128, 128, 128)
+    view = big.view(0)
+    occ = O.voxelize(view.mesh.vertices, view.mesh.triangles, dims_big, big.bounds)
+    hb = (big.hi - big.lo) / np.array(dims_big, dtype=np.float64)
+    coarse_b = rt.make_field(O.seeds_to_sdf(O.jfa_run(occ, hb), hb), big.lo, big.hi)
+    rt.sample_masked(coarse_b, dims_big, view.bvh, rt.SamplingParams(rays_per_frame=32), 1)
+    # then a small one with 3x headroom on the same workspace
+    scene, mesh = scene_mesh("sphere")
+    dims = (64, 64, 64)
+    view = scene.view(0)
+    occ = O.voxelize(mesh.vertices, mesh.triangles, dims, scene.bounds)
+    h = (scene.hi - scene.lo) / np.array(dims, dtype=np.float64)
+    coarse = rt.make_field(O.seeds_to_sdf(O.jfa_run(occ, h), h), scene.lo, scene.hi)
+    params = rt.SamplingParams(rays_per_frame=32)
+    g = RS._RsGeom(coarse, dims)
+    dev = coarse.data.device
+    mask = torch.empty(dims, dtype=torch.bool, device=dev)
+    cb = RS.CompactBuffers(g.n, dev)
+    RS.launch_resample(g, params.mask_distance, mask_new=mask, block_counts=cb.block_counts)
+    RS.launch_compact(mask, cb)
+    m = int(cb.count.item())
+    smin = torch.empty(m, dtype=torch.float64, device=dev)
+    sf = torch.empty(m, dtype=torch.int32, device=dev)
+    sb = torch.empty(m, dtype=torch.int32, device=dev)
+    t_max = float(np.linalg.norm(scene.hi - scene.lo))
+    RS.launch_sample_update(view.bvh, g, cb, params, 2, t_max, samp=(smin, sf, sb), m_cap=3 * m)
+    idx = cb.idx[:m].cpu().numpy()
+    b = O.bvh_build(mesh.vertices, mesh.triangles, mesh.normals)
+    wmin, wf, wb = O.sample_masked(b, idx, scene.lo, h, dims, 32, 0, 2, t_max)
+    np.testing.assert_array_equal(sf.cpu().numpy(), wf)
+    np.testing.assert_array_equal(sb.cpu().numpy(), wb)
+    np.testing.assert_array_equal(smin.cpu().numpy(), wmin)
