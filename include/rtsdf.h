@@ -15,9 +15,12 @@
  *   - `stream` is a cudaStream_t passed as void*; every call is asynchronous on
  *     it, deterministic, and free of order-dependent atomics.
  *   - Grids are C-order (nx, ny, nz), z fastest, like the reference arrays.
- *   - Seeds inside the library are PACKED int32: (i << 20) | (j << 10) | k,
- *     EMPTY = -1.  Numeric order == lexicographic (i, j, k) order.  Each dim
- *     must be <= 1024.  rtsdf_seeds_packed_to_linear converts to the
+ *   - Seeds inside the library are PACKED int32: (i << 20) | (j << 10) | k
+ *     when every dim is <= 1024; for larger grids k takes the low bits(nz-1)
+ *     bits, j the next bits(ny-1), i the top bits(nx-1) (their sum must be
+ *     <= 31, and such grids run the per-cell JFA kernel).  EMPTY = -1.
+ *     Numeric order == lexicographic (i, j, k) order.  The layout is a
+ *     function of the dims; rtsdf_seeds_packed_to_linear converts to the
  *     reference's linear index (jfa.py:31,53).
  *   - Return value: 0 on success, else an RTSDF_ERR_* code; no exceptions or
  *     exits cross the ABI.  rtsdf_last_error() gives a message (thread-local).
@@ -36,7 +39,7 @@ enum {
     RTSDF_OK = 0,
     RTSDF_ERR_INVALID = 1,   /* bad argument (maps to ValueError)            */
     RTSDF_ERR_CUDA = 2,      /* CUDA launch / runtime failure (RuntimeError) */
-    RTSDF_ERR_DIMS = 3,      /* unsupported grid dims (> 1024 per axis)      */
+    RTSDF_ERR_DIMS = 3,      /* grid dims beyond packed int32 seeds: bits(nx-1) + bits(ny-1) + bits(nz-1) > 31 */
     RTSDF_ERR_WORKSPACE = 4  /* workspace too small                          */
 };
 

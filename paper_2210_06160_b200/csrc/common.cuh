@@ -39,6 +39,48 @@ __device__ __forceinline__ int unpack_i(int32_t p) { return (int)((uint32_t)p >>
 __device__ __forceinline__ int unpack_j(int32_t p) { return (p >> 10) & 1023; }
 __device__ __forceinline__ int unpack_k(int32_t p) { return p & 1023; }
 
+// Dims-dependent packed seeds.  Grids with every axis <= RTSDF_MAX_DIM use the
+// fixed i<<20 | j<<10 | k layout above (every fast JFA kernel decodes it with
+// immediates); larger grids (any axis beyond 1024, bits(nx-1) + bits(ny-1) +
+// bits(nz-1) <= 31) pack k in the low bz bits, j above it, i on top, and run
+// the per-cell JFA kernel, which decodes with these runtime fields.  In either
+// layout numeric order is lexicographic (i, j, k) order and EMPTY = -1.
+struct SeedFmt {
+    int sx, sy;          // shifts of the i and j fields
+    uint32_t mx, my, mz; // field masks
+};
+__host__ __device__ __forceinline__ SeedFmt seed_fmt_packed() { return SeedFmt{20, 10, 4095u, 1023u, 1023u}; }
+__device__ __forceinline__ int fmt_i(int32_t p, const SeedFmt& f) { return (int)(((uint32_t)p >> f.sx) & f.mx); }
+__device__ __forceinline__ int fmt_j(int32_t p, const SeedFmt& f) { return (int)(((uint32_t)p >> f.sy) & f.my); }
+__device__ __forceinline__ int fmt_k(int32_t p, const SeedFmt& f) { return (int)((uint32_t)p & f.mz); }
+__host__ __device__ __forceinline__ int32_t fmt_pack(int i, int j, int k, const SeedFmt& f) {
+    return (int32_t)(((uint32_t)i << f.sx) | ((uint32_t)j << f.sy) | (uint32_t)k);
+}
+inline int bits_for(int n) {  // bits to hold 0 .. n-1 (>= 1)
+    int b = 1;
+    while (b < 31 && (1 << b) < n) ++b;
+    return b;
+}
+inline bool seed_fmt_legacy(int nx, int ny, int nz) {
+    return nx <= RTSDF_MAX_DIM && ny <= RTSDF_MAX_DIM && nz <= RTSDF_MAX_DIM;
+}
+// false: the grid cannot be packed in 31 bits
+inline bool seed_fmt_for(int nx, int ny, int nz, SeedFmt* f) {
+    if (nx < 1 || ny < 1 || nz < 1) return false;
+    if (seed_fmt_legacy(nx, ny, nz)) {
+        *f = seed_fmt_packed();
+        return true;
+    }
+    const int bx = bits_for(nx), by = bits_for(ny), bz = bits_for(nz);
+    if (bx + by + bz > 31) return false;
+    f->sy = bz;
+    f->sx = by + bz;
+    f->mx = (1u << bx) - 1u;
+    f->my = (1u << by) - 1u;
+    f->mz = (1u << bz) - 1u;
+    return true;
+}
+
 // jfa.py:72-76 _center_d2, fp64, left to right, no contraction
 __device__ __forceinline__ double center_d2(int di, int dj, int dk, double hx, double hy,
                                             double hz) {

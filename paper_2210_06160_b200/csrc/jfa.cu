@@ -35,6 +35,7 @@ struct JfaGeom {
     bool exact;  // fp64 d2 exact for these spacings (fp64_exact): ties resolve in the pass
     int ox0, onx;  // output planes [ox0, ox0 + onx) (a sub-range of the owned planes;
                    // dst points at plane ox0): interior / boundary launches of a slab
+    SeedFmt fmt;   // packed seed layout (seed_fmt_for; the fast kernels assume the fixed one)
 };
 
 // True when every fp64 operation of center_d2 (jfa.py:72-76) is exact for all
@@ -103,7 +104,7 @@ template <int MODE>
 __device__ __forceinline__ void consider(Best<MODE>& b, int32_t c, int i, int j, int k,
                                          const JfaGeom& g) {
     if (c == RTSDF_EMPTY || c == b.p) return;
-    int dx = i - unpack_i(c), dy = j - unpack_j(c), dz = k - unpack_k(c);
+    int dx = i - fmt_i(c, g.fmt), dy = j - fmt_j(c, g.fmt), dz = k - fmt_k(c, g.fmt);
     if (MODE == JFA_INT) {
         int q = g.wx * dx * dx + g.wy * dy * dy + g.wz * dz * dz;
         if (q < b.q) {
@@ -112,7 +113,7 @@ __device__ __forceinline__ void consider(Best<MODE>& b, int32_t c, int i, int j,
         } else if (q == b.q && b.p != RTSDF_EMPTY) {
             // integer tie: decide on the reference's fp64 values
             double dc = center_d2(dx, dy, dz, g.hx, g.hy, g.hz);
-            double db = center_d2(i - unpack_i(b.p), j - unpack_j(b.p), k - unpack_k(b.p), g.hx,
+            double db = center_d2(i - fmt_i(b.p, g.fmt), j - fmt_j(b.p, g.fmt), k - fmt_k(b.p, g.fmt), g.hx,
                                   g.hy, g.hz);
             if (dc < db || (dc == db && c < b.p)) {
                 b.p = c;
@@ -142,7 +143,7 @@ __global__ void __launch_bounds__(256) jfa_step_kernel(PlaneSrc src, int32_t* __
     Best<MODE> b;
     b.p = __ldg(src.local + (int64_t)(i - g.x0) * plane + (int64_t)j * g.nz + k);
     if (b.p != RTSDF_EMPTY) {
-        int dx = i - unpack_i(b.p), dy = j - unpack_j(b.p), dz = k - unpack_k(b.p);
+        int dx = i - fmt_i(b.p, g.fmt), dy = j - fmt_j(b.p, g.fmt), dz = k - fmt_k(b.p, g.fmt);
         if (MODE == JFA_INT) b.q = g.wx * dx * dx + g.wy * dy * dy + g.wz * dz * dz;
         else b.d2 = center_d2(dx, dy, dz, g.hx, g.hy, g.hz);
     } else {
@@ -299,7 +300,7 @@ __global__ void __launch_bounds__(256) jfa_sparse_active_kernel(const int32_t* _
             Best<MODE> b;
             b.p = __ldg(src + cell);
             if (b.p != RTSDF_EMPTY) {
-                int dx = i - unpack_i(b.p), dy = j - unpack_j(b.p), dz = k - unpack_k(b.p);
+                int dx = i - fmt_i(b.p, g.fmt), dy = j - fmt_j(b.p, g.fmt), dz = k - fmt_k(b.p, g.fmt);
                 if (MODE == JFA_INT) b.q = g.wx * dx * dx + g.wy * dy * dy + g.wz * dz * dz;
                 else b.d2 = center_d2(dx, dy, dz, g.hx, g.hy, g.hz);
             } else {
@@ -335,14 +336,14 @@ __global__ void __launch_bounds__(256) jfa_sparse_active_kernel(const int32_t* _
 }
 
 __global__ void jfa_init_kernel(const uint8_t* __restrict__ occ, int ny, int nz, int64_t n,
-                                int32_t* __restrict__ seed, int64_t* __restrict__ count) {
+                                int32_t* __restrict__ seed, int64_t* __restrict__ count, SeedFmt f) {
     int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     bool on = false;
     if (c < n) {
         on = occ[c] != 0;
         int64_t nyz = (int64_t)ny * nz;
         int i = (int)(c / nyz), j = (int)((c / nz) % ny), k = (int)(c % nz);
-        seed[c] = on ? pack_ijk(i, j, k) : RTSDF_EMPTY;
+        seed[c] = on ? fmt_pack(i, j, k, f) : RTSDF_EMPTY;
     }
     if (count) {
         unsigned m = __ballot_sync(0xffffffffu, on);
@@ -353,7 +354,7 @@ __global__ void jfa_init_kernel(const uint8_t* __restrict__ occ, int ny, int nz,
 // jfa.py:148-160: f32(sqrt(d2_fp64) - beta)
 __global__ void seeds_to_sdf_kernel(const int32_t* __restrict__ seed, float* __restrict__ out,
                                     int x0, int ny, int nz, double hx, double hy, double hz,
-                                    double beta, int64_t* __restrict__ empty_count) {
+                                    double beta, int64_t* __restrict__ empty_count, SeedFmt f) {
     const int k = blockIdx.x * 32 + threadIdx.x;
     const int j = blockIdx.y * 8 + threadIdx.y;
     const int i = x0 + blockIdx.z;  // global plane (buffers are global-indexed)
@@ -362,7 +363,7 @@ __global__ void seeds_to_sdf_kernel(const int32_t* __restrict__ seed, float* __r
         int64_t c = ((int64_t)i * ny + j) * nz + k;
         int32_t s = __ldg(seed + c);
         empty = s == RTSDF_EMPTY;
-        double d2 = center_d2(i - unpack_i(s), j - unpack_j(s), k - unpack_k(s), hx, hy, hz);
+        double d2 = center_d2(i - fmt_i(s, f), j - fmt_j(s, f), k - fmt_k(s, f), hx, hy, hz);
         out[c] = (float)__dsub_rn(__dsqrt_rn(d2), beta);
     }
     if (empty_count) {
@@ -373,16 +374,16 @@ __global__ void seeds_to_sdf_kernel(const int32_t* __restrict__ seed, float* __r
 }
 
 __global__ void packed_to_linear_kernel(const int32_t* __restrict__ p, int32_t* __restrict__ l,
-                                        int ny, int nz, int64_t n) {
+                                        int ny, int nz, int64_t n, SeedFmt f) {
     int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (c >= n) return;
     int32_t s = p[c];
     l[c] = s == RTSDF_EMPTY ? RTSDF_EMPTY
-                            : (int32_t)(((int64_t)unpack_i(s) * ny + unpack_j(s)) * nz + unpack_k(s));
+                            : (int32_t)(((int64_t)fmt_i(s, f) * ny + fmt_j(s, f)) * nz + fmt_k(s, f));
 }
 
 __global__ void linear_to_packed_kernel(const int32_t* __restrict__ l, int32_t* __restrict__ p,
-                                        int ny, int nz, int64_t n) {
+                                        int ny, int nz, int64_t n, SeedFmt f) {
     int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (c >= n) return;
     int32_t s = l[c];
@@ -391,7 +392,7 @@ __global__ void linear_to_packed_kernel(const int32_t* __restrict__ l, int32_t* 
         return;
     }
     int64_t nyz = (int64_t)ny * nz;
-    p[c] = pack_ijk((int)(s / nyz), (int)((s / nz) % ny), (int)(s % nz));
+    p[c] = fmt_pack((int)(s / nyz), (int)((s / nz) % ny), (int)(s % nz), f);
 }
 
 }  // namespace rtsdf
@@ -403,11 +404,18 @@ __global__ void linear_to_packed_kernel(const int32_t* __restrict__ l, int32_t* 
 namespace rtsdf {
 
 static bool dims_ok(int nx, int ny, int nz) {
-    if (nx < 1 || ny < 1 || nz < 1 || nx > RTSDF_MAX_DIM || ny > RTSDF_MAX_DIM || nz > RTSDF_MAX_DIM) {
-        set_error("dims (%d, %d, %d) outside 1..%d (packed 10:10:10 seeds)", nx, ny, nz, RTSDF_MAX_DIM);
+    SeedFmt f;
+    if (!seed_fmt_for(nx, ny, nz, &f) || (int64_t)nx * ny * nz >= ((int64_t)1 << 31)) {
+        set_error("dims (%d, %d, %d): packed int32 seeds need bits(nx-1) + bits(ny-1) + bits(nz-1) <= 31",
+                  nx, ny, nz);
         return false;
     }
     return true;
+}
+static SeedFmt fmt_of(int nx, int ny, int nz) {
+    SeedFmt f = seed_fmt_packed();
+    seed_fmt_for(nx, ny, nz, &f);
+    return f;
 }
 
 // jfa2.cuh NAT: min over the grid of the virtual EMPTY seed's weighted d2
@@ -615,7 +623,9 @@ static int launch_step(PlaneSrc s, int32_t* dst, const JfaGeom& g, bool slab, vo
     bool int_mode = g.wx > 0 && g.wy > 0 && g.wz > 0;
     int mdim = g.nx > g.ny ? g.nx : g.ny;
     if (g.nz > mdim) mdim = g.nz;
-    if (int_mode && 2 * g.offset >= mdim) {
+    // grids beyond the fixed packed layout: the per-cell kernel (runtime fields)
+    const bool generic = !seed_fmt_legacy(g.nx, g.ny, g.nz);
+    if (int_mode && (generic || 2 * g.offset >= mdim)) {
         // first pass: every lattice chain has <= 2 cells, v2's register tiles
         // cannot amortise their setup -- the per-cell kernel is faster
         if (slab) jfa_step_kernel<JFA_INT, true><<<grid, block, 0, st>>>(s, dst, g);
@@ -675,7 +685,8 @@ extern "C" int rtsdf_jfa_init(const uint8_t* occ, int nx, int ny, int nz, int32_
     if (!dims_ok(nx, ny, nz)) return RTSDF_ERR_DIMS;
     int64_t n = (int64_t)nx * ny * nz;
     jfa_init_kernel<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(occ, ny, nz, n,
-                                                                                  seed, count);
+                                                                                  seed, count,
+                                                                                  fmt_of(nx, ny, nz));
     count_launch();
     return check_launch("jfa_init");
 }
@@ -691,6 +702,7 @@ extern "C" int rtsdf_jfa_step(const int32_t* src, int32_t* dst, int nx, int ny, 
     if (!ws_ok(ws, ws_bytes, (int64_t)nx * ny * nz)) return RTSDF_ERR_WORKSPACE;
     JfaGeom g{nx, ny, nz, 0, nx, 0, 0, 0, 0, offset, hx, hy, hz, wx, wy, wz,
               wx > 0 && fp64_exact(hx, hy, hz, nx, ny, nz), 0, nx};
+    g.fmt = fmt_of(nx, ny, nz);
     PlaneSrc s{src, nullptr, nullptr};
     return launch_step(s, dst, g, false, ws, (cudaStream_t)stream);
 }
@@ -711,6 +723,7 @@ extern "C" int rtsdf_jfa_step_slab(const int32_t* local, const int32_t* halo_lo,
     if (!ws_ok(ws, ws_bytes, (int64_t)nxl * ny * nz)) return RTSDF_ERR_WORKSPACE;
     JfaGeom g{nx,     ny,    nz, x0, nxl, lo_first, n_lo, hi_first, n_hi, offset, hx, hy, hz,
               wx,     wy,    wz, wx > 0 && fp64_exact(hx, hy, hz, nx, ny, nz), out_first, out_count};
+    g.fmt = fmt_of(nx, ny, nz);
     PlaneSrc s{local, halo_lo, halo_hi};
     return launch_step(s, dst, g, true, ws, (cudaStream_t)stream);
 }
@@ -784,6 +797,26 @@ static int run_schedule(int32_t* a, int32_t* b, float* sdf_out, int nx, int ny, 
     if (nz > m) m = nz;
     int n = 1;
     while (n < m) n *= 2;  // jfa.py:58-68
+    if (!seed_fmt_legacy(nx, ny, nz)) {
+        // grids beyond the fixed packed layout: every pass with the per-cell
+        // kernel (runtime seed fields), then seeds -> SDF
+        int32_t* src = a;
+        int32_t* dst = b;
+        int w = 0;
+        for (int off = n / 2; off >= 1; off /= 2) {
+            JfaGeom g{nx, ny, nz, 0, nx, 0, 0, 0, 0, off, hx, hy, hz, wx, wy, wz, exact, 0, nx};
+            g.fmt = fmt_of(nx, ny, nz);
+            const int rc = launch_step(PlaneSrc{src, nullptr, nullptr}, dst, g, false, ws, st);
+            if (rc != RTSDF_OK) return rc;
+            int32_t* t = src;
+            src = dst;
+            dst = t;
+            w ^= 1;
+        }
+        if (which) *which = w;
+        if (sdf_out) return rtsdf_seeds_to_sdf(src, sdf_out, nx, ny, nz, hx, hy, hz, beta, empty_count, st);
+        return RTSDF_OK;
+    }
     // Sparse passes while the pass input is sparse (< 5 % of its 32-cell
     // segments hold a seed): a sparse pass only pays off while few segments
     // are active, since its active warps run the per-cell rule instead of the
@@ -841,6 +874,7 @@ static int run_schedule(int32_t* a, int32_t* b, float* sdf_out, int nx, int ny, 
     const FastDiv dzb = make_fastdiv((uint32_t)nzb), dny = make_fastdiv((uint32_t)ny);
     for (int off = n / 2; off >= 1; off /= 2) {
         JfaGeom g{nx, ny, nz, 0, nx, 0, 0, 0, 0, off, hx, hy, hz, wx, wy, wz, exact, 0, nx};
+        g.fmt = fmt_of(nx, ny, nz);
         PlaneSrc s{src, nullptr, nullptr};
         if (sdf_out && off == 1 && int_mode) {  // last pass writes the SDF directly
             // v5 leaves the tied winners of the flagged cells in the free buffer
@@ -958,7 +992,8 @@ extern "C" int rtsdf_seeds_to_sdf_range(const int32_t* seed, float* out, int nx,
     dim3 block(32, 8, 1);
     dim3 grid((nz + 31) / 32, (ny + 7) / 8, nxl);
     seeds_to_sdf_kernel<<<grid, block, 0, (cudaStream_t)stream>>>(seed, out, x0, ny, nz, hx, hy,
-                                                                  hz, beta, empty_count);
+                                                                  hz, beta, empty_count,
+                                                                  fmt_of(nx, ny, nz));
     count_launch();
     return check_launch("seeds_to_sdf");
 }
@@ -974,8 +1009,8 @@ extern "C" int rtsdf_seeds_packed_to_linear(const int32_t* p, int32_t* l, int nx
                                             void* stream) {
     if (!dims_ok(nx, ny, nz)) return RTSDF_ERR_DIMS;
     int64_t n = (int64_t)nx * ny * nz;
-    packed_to_linear_kernel<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(p, l, ny,
-                                                                                          nz, n);
+    packed_to_linear_kernel<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+        p, l, ny, nz, n, fmt_of(nx, ny, nz));
     count_launch();
     return check_launch("seeds_packed_to_linear");
 }
@@ -984,8 +1019,8 @@ extern "C" int rtsdf_seeds_linear_to_packed(const int32_t* l, int32_t* p, int nx
                                             void* stream) {
     if (!dims_ok(nx, ny, nz)) return RTSDF_ERR_DIMS;
     int64_t n = (int64_t)nx * ny * nz;
-    linear_to_packed_kernel<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(l, p, ny,
-                                                                                          nz, n);
+    linear_to_packed_kernel<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+        l, p, ny, nz, n, fmt_of(nx, ny, nz));
     count_launch();
     return check_launch("seeds_linear_to_packed");
 }

@@ -67,6 +67,7 @@ __device__ bool tri_box_overlap(const double* a, const double* b, const double* 
 struct VoxParams {
     double lo[3], hi[3], h[3];
     int n[3];
+    SeedFmt fmt;  // packed seed layout for the grid (common.cuh seed_fmt_for)
 };
 
 // Per triangle: gather p0/p1/p2 (voxel.py:168-170), OOB check (:171-175),
@@ -154,7 +155,7 @@ __global__ void __launch_bounds__(256) vox_cells_kernel(
             if (tri_box_overlap(a, b, c, cx, cy, cz, ex, ey, ez)) {
                 int64_t cell = (int64_t)i * nyz + (int64_t)j * P.n[2] + k;
                 if (occ) occ[cell] = 1;  // all writers store the same value
-                if (seed) seed[cell] = pack_ijk(i, j, k);
+                if (seed) seed[cell] = fmt_pack(i, j, k, P.fmt);
                 hit = true;
             }
         }
@@ -192,8 +193,9 @@ extern "C" int rtsdf_voxelize(const double* verts, int64_t n_verts, const int32_
         set_error("voxelize: dims must be >= 2 per axis");
         return RTSDF_ERR_INVALID;
     }
-    if (seed && (nx > RTSDF_MAX_DIM || ny > RTSDF_MAX_DIM || nz > RTSDF_MAX_DIM)) {
-        set_error("voxelize: packed seeds support dims <= %d", RTSDF_MAX_DIM);
+    SeedFmt fmt;
+    if (seed && (!seed_fmt_for(nx, ny, nz, &fmt) || (int64_t)nx * ny * nz >= ((int64_t)1 << 31))) {
+        set_error("voxelize: dims (%d, %d, %d) cannot hold packed int32 seeds", nx, ny, nz);
         return RTSDF_ERR_DIMS;
     }
     if (!counters) {
@@ -205,6 +207,8 @@ extern "C" int rtsdf_voxelize(const double* verts, int64_t n_verts, const int32_
         return RTSDF_ERR_WORKSPACE;
     }
     VoxParams P;
+    P.fmt = seed_fmt_packed();
+    if (seed) P.fmt = fmt;
     int dims[3] = {nx, ny, nz};
     for (int a = 0; a < 3; ++a) {
         P.lo[a] = lo[a];

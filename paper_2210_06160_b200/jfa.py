@@ -2,7 +2,8 @@
 
 SeedGrid keeps the reference's fields and semantics: `seed` is the int32
 LINEAR index of each cell's best seed (EMPTY = -1).  Internally the device
-works on packed coordinates (i<<20 | j<<10 | k); `seed` converts on demand so
+works on packed coordinates (i<<20 | j<<10 | k; a dims-dependent i | j | k
+layout beyond 1024 cells per axis); `seed` converts on demand so
 a drop-in caller sees exactly the reference's array.
 
 `jump_flood(voxels, beta)` is the north-star name for jfa_run + seeds_to_sdf.
@@ -73,9 +74,17 @@ class SeedGrid:
         return cls(packed, np.asarray(lo, np.float64), np.asarray(hi, np.float64))
 
 
+def _bits(n: int) -> int:
+    return max(1, int(n - 1).bit_length())
+
+
 def _check_dims(dims):
-    if max(dims) > MAX_DIM:
-        raise ValueError(f"dims {dims}: packed seeds support at most {MAX_DIM} cells per axis")
+    """Packed int32 seeds: i<<20 | j<<10 | k while every axis is <= MAX_DIM
+    (the fast JFA kernels), else a dims-dependent i | j | k layout that needs
+    bits(nx-1) + bits(ny-1) + bits(nz-1) <= 31 (the per-cell kernel)."""
+    if max(dims) > MAX_DIM and sum(_bits(int(n)) for n in dims) > 31:
+        raise ValueError(f"dims {dims}: packed int32 seeds need bits(nx-1) + bits(ny-1) + "
+                         f"bits(nz-1) <= 31")
 
 
 @lru_cache(maxsize=64)

@@ -139,6 +139,11 @@ def test_jfa_every_pass_matches_oracle(rt, name, dims):
     ((37, 23, 51), (0.37, 0.46, 0.51), 0.02, (1, 4, 1)),
     ((5, 70, 3), (0.05, 1.4, 0.03), 0.05, (1, 4, 1)),
     ((3, 41, 66), (0.096, 1.312, 2.112), 0.03, (1, 1, 1)),
+    # axes beyond 1024 cells: dims-dependent packed seeds, per-cell kernel
+    ((2100, 6, 10), (2.1, 0.012, 0.01), 0.002, (1, 4, 1)),
+    ((20, 1500, 12), (0.02, 3.0, 0.012), 0.002, (1, 4, 1)),
+    ((3, 40, 1100), (0.375, 5.0, 137.5), 0.003, (1, 1, 1)),
+    ((1030, 9, 5), (1.03, 0.0045, 0.0155), 0.004, (0, 0, 0)),
 ])
 def test_jfa_random_occupancy_every_pass_and_schedule(rt, dims, hi, frac, weights):
     """Random seeds, non-dyadic spacings (INT mode with tie marks + fix-ups):
@@ -578,3 +583,21 @@ def test_reference_visibility_matches_reference(rt):
     np.testing.assert_array_equal(vis, want)
     img = _np(rt.reference_render(view, scene.camera, scene.light, spp=4, seed=0))
     assert img.shape == (scene.camera.height, scene.camera.width, 3) and np.isfinite(img).all()
+
+
+def test_frame_on_an_axis_beyond_1024(rt):
+    """A hybrid frame on a grid with one axis past the packed 10:10:10 seed
+    layout (dims-dependent packed seeds, per-cell JFA kernel) == the oracle."""
+    scene = rt.get_scene("sphere")
+    dims = (1040, 14, 12)
+    cfg = rt.PipelineConfig(coarse_dims=dims, fine_dims=dims,
+                            sampling=rt.SamplingParams(rays_per_frame=4, mask_distance=0.3))
+    pipe = rt.FramePipeline(scene, cfg)
+    pipe.direction_fn = lambda idx, frame: O.dir_table(0, idx, frame, 4)
+    rec = pipe.advance(render=False)
+    mesh = scene.view(0).mesh
+    h = O.HybridOracle(mesh.vertices, mesh.triangles, mesh.normals, scene.bounds, dims, dims, x=4, d=0.3)
+    want = h.advance(dirs_fn=lambda idx, frame: O.dir_table(0, idx, frame, 4))
+    assert rec.masked_texels == len(want["idx"])
+    np.testing.assert_array_equal(_np(pipe.coarse.data), want["coarse"])
+    np.testing.assert_array_equal(_np(pipe.fine.data), want["fine"])
