@@ -173,6 +173,7 @@ struct WfBuffers {
     uint32_t* votes;           // [m_cap]
     int32_t* queue;            // [R] rays needing the full search
     int64_t* qcount;
+    unsigned long long* qhead;  // pass 2: next queue chunk to claim
     const int64_t* texels;      // the masked-texel count (device): chunks of rays beyond
     int64_t m_cap;              // min(count, m_cap) * x were not written by this call's pass 1
     int x;
@@ -559,8 +560,25 @@ __global__ void __launch_bounds__(WF_THREADS, WF_MINB) wf_pass2_kernel(SamplePar
     __shared__ int32_t stack_mem[RTSDF_FAST_STACK * WF_THREADS];
     __shared__ __half tstack_mem[WIDE ? RTSDF_FAST_STACK * WF_THREADS : 1];
     const int64_t Q = *B.qcount;
+#ifndef WF2_DYN
+#define WF2_DYN 1
+#endif
+#if WF2_DYN
+    // warps claim 32-ray chunks of the queue dynamically (one atomic per chunk):
+    // a warp that drew short rays takes the next chunk instead of idling at the
+    // end of a static grid-stride share
+    const int lane = threadIdx.x & 31;
+    while (true) {
+        unsigned long long base = 0;
+        if (lane == 0) base = atomicAdd(B.qhead, 32ull);
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if ((int64_t)base >= Q) break;
+        const int64_t q = (int64_t)base + lane;
+        if (q >= Q) continue;
+#else
     for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < Q;
          q += (int64_t)gridDim.x * blockDim.x) {
+#endif
         const int64_t r = B.queue[q];
         double ox, oy, oz, dx, dy, dz;
         wf_ray(P, B, r, ox, oy, oz, dx, dy, dz);
@@ -727,11 +745,12 @@ extern "C" int rtsdf_sample_update(const void* bvh_packed, int64_t n_nodes, int6
         p += (nob * 8 * sizeof(int32_t) + 255) / 256 * 256;
         B.scan_tmp = p;
         B.scan_tmp_bytes = oct_scan_temp_bytes(nob);
+        B.qhead = (unsigned long long*)((char*)B.qcount + 8);
         B.texels = count;
         B.m_cap = m_cap;
         B.x = x;
         B.aligned = 32 % x == 0;
-        cudaMemsetAsync(B.qcount, 0, sizeof(int64_t), st);
+        cudaMemsetAsync(B.qcount, 0, 2 * sizeof(int64_t), st);  // qcount, qhead
         int64_t blocks = (R + WF_THREADS - 1) / WF_THREADS;
         int64_t cap = (int64_t)num_sms() * 24;
         const bool wide = n_nodes4 > 0;
