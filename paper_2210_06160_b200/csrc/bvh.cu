@@ -323,10 +323,10 @@ __global__ void __launch_bounds__(128) ray_query_fast4_kernel(
     if (q >= n) return;
     int32_t id;
     int facing;
-    // the long-ray traversal of the sampler's pass 2 (brute-force-equivalence tested)
-    double t = trace_fast4_ww(b, orig[3 * q], orig[3 * q + 1], orig[3 * q + 2], dirs[3 * q],
-                              dirs[3 * q + 1], dirs[3 * q + 2], t_max, stack_mem + threadIdx.x,
-                              tstack_mem + threadIdx.x, 128, id, facing, tb);
+    // the sampler's BVH4 traversal (brute-force-equivalence tested)
+    double t = trace_fast4(b, orig[3 * q], orig[3 * q + 1], orig[3 * q + 2], dirs[3 * q],
+                           dirs[3 * q + 1], dirs[3 * q + 2], t_max, stack_mem + threadIdx.x,
+                           tstack_mem + threadIdx.x, 128, id, facing, tb);
     out_t[q] = t;
     out_id[q] = id;
     out_facing[q] = facing;

@@ -584,9 +584,10 @@ __global__ void __launch_bounds__(WF_THREADS, WF_MINB) wf_pass2_kernel(SamplePar
         wf_ray(P, B, r, ox, oy, oz, dx, dy, dz);
         int32_t id;
         int facing;
-        // long rays: speculative while-while traversal (BVH4)
-        double t = WIDE ? trace_fast4_ww(P.bvh4, ox, oy, oz, dx, dy, dz, P.t_max, stack_mem + threadIdx.x,
-                                         tstack_mem + threadIdx.x, WF_THREADS, id, facing, P.tb)
+        // long rays: near-first traversal (with dynamic chunks the while-while
+        // form measured slower: 2.30 vs 2.23 ms at C3)
+        double t = WIDE ? trace_fast4(P.bvh4, ox, oy, oz, dx, dy, dz, P.t_max, stack_mem + threadIdx.x,
+                                      tstack_mem + threadIdx.x, WF_THREADS, id, facing, P.tb)
                         : wf_trace<WIDE>(P, ox, oy, oz, dx, dy, dz, stack_mem + threadIdx.x,
                                          tstack_mem + threadIdx.x, id, facing, 0, nullptr);
         if (id >= 0) wf_commit(B, fdiv((unsigned)r, P.div_x), t, facing);

@@ -402,105 +402,4 @@ __device__ __forceinline__ double trace_fast4(const FastBvh4& b, double ox, doub
     return best_id < 0 ? -1.0 : best_t;
 }
 
-// Speculative while-while form of trace_fast4 (no budget), for the long rays
-// of pass 2: a lane that reaches a leaf parks it and keeps descending inner
-// nodes until every active lane of the warp holds a leaf; then the warp runs
-// the leaf phase together.  Inner-node and leaf work no longer alternate
-// lane by lane, so each phase runs with more lanes converged.  Same visited
-// set as trace_fast4 up to order (a parked leaf is tested after inner nodes
-// popped later), so the same brute-force-equivalent result.
-#define T4_DONE ((int32_t)0x80000000)  // no node left (never a valid leaf code)
-__device__ __forceinline__ double trace_fast4_ww(const FastBvh4& b, double ox, double oy,
-                                                 double oz, double dx, double dy, double dz,
-                                                 double t_max, int32_t* stack, __half* tstack,
-                                                 int stride, int32_t& out_id, int& out_facing,
-                                                 float tb0) {
-    RayF r;
-    r.ix = clamp_inv(dx);
-    r.iy = clamp_inv(dy);
-    r.iz = clamp_inv(dz);
-    r.oix = (float)ox * r.ix;
-    r.oiy = (float)oy * r.iy;
-    r.oiz = (float)oz * r.iz;
-    const float fdx = (float)dx, fdy = (float)dy, fdz = (float)dz;
-    double best_t = t_max;
-    int32_t best_id = -1;
-    int best_facing = 0;
-    float tb = tb0;  // tmax_bound(t_max), computed once by the caller
-    int sp = 0;
-    auto pop = [&]() -> int32_t {
-        while (sp > 0) {
-            --sp;
-            if (__half2float(tstack[sp * stride]) <= tb) return stack[sp * stride];
-        }
-        return T4_DONE;
-    };
-    int32_t node = 0;  // >= 0 inner, < 0 leaf, T4_DONE finished
-    int32_t leaf = 0;  // parked leaf (< 0) or 0
-#ifdef RTSDF_TRACE_STATS
-    int visits = 0;
-#endif
-    while (true) {
-        while (node >= 0) {
-            RTSDF_TSTAT(0, 1);
-#ifdef RTSDF_TRACE_STATS
-            ++visits;
-#endif
-            const FastNode4* nd = b.nodes + node;
-            const float4 lx = __ldg((const float4*)nd->lox), ly = __ldg((const float4*)nd->loy),
-                         lz = __ldg((const float4*)nd->loz), hx = __ldg((const float4*)nd->hix),
-                         hy = __ldg((const float4*)nd->hiy), hz = __ldg((const float4*)nd->hiz);
-            const int4 ch = __ldg((const int4*)nd->child);
-            float t[4];
-            t[0] = box_entry(lx.x, ly.x, lz.x, hx.x, hy.x, hz.x, r, tb);
-            t[1] = box_entry(lx.y, ly.y, lz.y, hx.y, hy.y, hz.y, r, tb);
-            t[2] = box_entry(lx.z, ly.z, lz.z, hx.z, hy.z, hz.z, r, tb);
-            t[3] = box_entry(lx.w, ly.w, lz.w, hx.w, hy.w, hz.w, r, tb);
-            const int32_t c[4] = {ch.x, ch.y, ch.z, ch.w};
-            int nearest = -1;
-            float tn = RTSDF_FINF;
-#pragma unroll
-            for (int q = 0; q < 4; ++q)
-                if (t[q] < tn) {
-                    tn = t[q];
-                    nearest = q;
-                }
-#pragma unroll
-            for (int q = 0; q < 4; ++q)
-                if (q != nearest && t[q] != RTSDF_FINF) {
-                    stack[sp * stride] = c[q];
-                    tstack[sp * stride] = __float2half_rd(t[q]);
-                    ++sp;
-                }
-            node = nearest >= 0 ? c[nearest] : pop();
-            if (node < 0 && node != T4_DONE && leaf == 0) {  // park the first leaf
-                leaf = node;
-                node = pop();
-            }
-            if (!__any_sync(__activemask(), leaf == 0)) break;
-        }
-        if (leaf == 0 && node < 0 && node != T4_DONE) {
-            leaf = node;
-            node = pop();
-        }
-        while (leaf != 0) {
-            RTSDF_TSTAT(1, 1);
-            leaf_tris(b.tris, b.exact, leaf, ox, oy, oz, dx, dy, dz, fdx, fdy, fdz, best_t, best_id,
-                      best_facing, tb);
-            leaf = 0;
-            if (node < 0 && node != T4_DONE) {
-                leaf = node;
-                node = pop();
-            }
-        }
-        if (node == T4_DONE) break;
-    }
-#ifdef RTSDF_TRACE_STATS
-    RTSDF_TSTAT(4 + min(7, 31 - __clz(visits | 1)), 1);
-#endif
-    out_id = best_id;
-    out_facing = best_facing;
-    return best_id < 0 ? -1.0 : best_t;
-}
-
 }  // namespace rtsdf
