@@ -259,8 +259,11 @@ typedef struct {
  * warp-per-texel kernel (same results).                                     */
 size_t rtsdf_sample_ws_bytes(int64_t m_cap, int x);
 /* n_nodes4 > 0: the BVH4 collapse of the search tree (rtsdf_bvh4_collapse_host)
- * is appended to bvh_packed at offset rtsdf_bvh_packed_bytes(n_nodes, n_tris). */
+ * is appended to bvh_packed at offset rtsdf_bvh_packed_bytes(n_nodes, n_tris);
+ * stack4: traversal stack entries that BVH4 can need (3 per level; 0 =
+ * unknown): <= 24 lets the long-ray pass run with a smaller shared stack. */
 int rtsdf_sample_update(const void* bvh_packed, int64_t n_nodes, int64_t n_tris, int64_t n_nodes4,
+                        int stack4,
                         const int64_t* idx,
                         const int64_t* count, int64_t m_cap, const rtsdf_resample_desc* rs,
                         int x, uint64_t seed, int64_t frame, const int64_t* frame_dev /*nullable*/,

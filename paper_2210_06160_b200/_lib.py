@@ -77,7 +77,7 @@ SIGNATURES = {
     "rtsdf_ray_query": (I, [P, I64, I64, I, P, P, I64, D, P, P, P, P]),
     "rtsdf_sample_ws_bytes": (SZ, [I64, I]),
     "rtsdf_bvh4_collapse_host": (I64, [P, P, P, P, I64, P, I64]),
-    "rtsdf_sample_update": (I, [P, I64, I64, I64, P, P, I64, C.POINTER(ResampleDesc), I, U64, I64, P, D, P,
+    "rtsdf_sample_update": (I, [P, I64, I64, I64, I, P, P, I64, C.POINTER(ResampleDesc), I, U64, I64, P, D, P,
                                 P, P, P, P, P, P, P, P, D, P, P, SZ, P]),
     "rtsdf_occlusion": (I, [P, I, I, I, DP, DP, P, P, P, I, I, I, I, DP, D, I, D, D, D, D, D, I,
                             U64, F, P, P]),

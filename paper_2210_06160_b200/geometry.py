@@ -179,6 +179,7 @@ class BvhIndex:
     search: torch.Tensor = dc_field(repr=False, compare=False, default=None)
     search_nodes: int = 0
     search_nodes4: int = 0  # > 0: BVH4 collapse appended to `search`
+    search_stack4: int = 0  # > 0: stack entries its traversal can need (3 per level)
 
     @property
     def num_nodes(self):
@@ -241,12 +242,15 @@ def build_bvh(mesh: TriangleMesh) -> BvhIndex:
         nodes4 = np.empty((max(int(ns), 1), 128), dtype=np.uint8)
         n4 = int(L.rtsdf_bvh4_collapse_host(*[_lib.host_ptr(x) for x in (slo_c, shi_c, sl_c, sr_c)],
                                             int(ns), _lib.host_ptr(nodes4), nodes4.shape[0]))
-        if n4 > 0 and 3 * _depth4(nodes4[:n4]) < 40:  # RTSDF_FAST_STACK pushes
+        stack4 = 3 * _depth4(nodes4[:n4]) if n4 > 0 else 0
+        if n4 > 0 and stack4 < 40:  # RTSDF_FAST_STACK pushes
             search = torch.cat([search, to_device(nodes4[:n4].reshape(-1))])
         else:
-            n4 = 0
+            n4, stack4 = 0, 0
+    else:
+        stack4 = 0
     return BvhIndex(mesh, node_lo, node_hi, left, right, order, a, e1, e2, tn, packed,
-                    to_device(mesh.normals), search, int(ns), n4)
+                    to_device(mesh.normals), search, int(ns), n4, stack4)
 
 
 class DeviceBvh:
@@ -263,6 +267,7 @@ class DeviceBvh:
 
     device_built = True
     search_nodes4 = 0
+    search_stack4 = 0
 
     def __init__(self, mesh: TriangleMesh, verts_dev, tris_dev, state: dict | None = None,
                  rebuild_every: int = 8):

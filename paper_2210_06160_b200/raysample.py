@@ -182,7 +182,8 @@ def launch_sample_update(bvh: BvhIndex, g: _RsGeom, cb: CompactBuffers, params: 
         m_cap = max(int(cb.count.item()), 1)
     ws = sample_workspace(m_cap, params.rays_per_frame) if params.rays_per_frame > 0 else None
     _lib.check(_lib.lib().rtsdf_sample_update(
-        _lib.ptr(bvh.search), bvh.search_nodes, bvh.num_tris, bvh.search_nodes4, _lib.ptr(cb.idx),
+        _lib.ptr(bvh.search), bvh.search_nodes, bvh.num_tris, bvh.search_nodes4,
+        getattr(bvh, "search_stack4", 0), _lib.ptr(cb.idx),
         _lib.ptr(cb.count),
         int(m_cap), desc, int(params.rays_per_frame),
         int(params.seed) & 0xFFFFFFFFFFFFFFFF, int(frame), _lib.ptr(frame_dev), float(t_max),

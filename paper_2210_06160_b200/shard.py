@@ -148,7 +148,7 @@ class ShardedFramePipeline:
                                  (_lib.D * 3)(*self.h), nx, ny, nz, (_lib.D * 3)(*self.h))
         _lib.check(L.rtsdf_sample_update(
             _lib.ptr(bvh.search), bvh.search_nodes, bvh.num_tris, bvh.search_nodes4,
-            _lib.ptr(cb.idx), _lib.ptr(cb.count), m_cap, desc, int(s.rays_per_frame),
+            getattr(bvh, "search_stack4", 0), _lib.ptr(cb.idx), _lib.ptr(cb.count), m_cap, desc, int(s.rays_per_frame),
             int(s.seed) & 0xFFFFFFFFFFFFFFFF, int(self.frame), None, float(t_max), None, None, None,
             None,
             fine_b, *acc, float(s.decay_alpha), fine_b, _lib.ptr(ws), 0 if ws is None else ws.numel(),

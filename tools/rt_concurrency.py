@@ -35,7 +35,8 @@ bvh = view.bvh
 def launch(i, stream):
     smin, sf, sb = outs[i]
     _lib.check(L.rtsdf_sample_update(
-        _lib.ptr(bvh.search), bvh.search_nodes, bvh.num_tris, bvh.search_nodes4, _lib.ptr(cb.idx),
+        _lib.ptr(bvh.search), bvh.search_nodes, bvh.num_tris, bvh.search_nodes4, bvh.search_stack4,
+        _lib.ptr(cb.idx),
         _lib.ptr(cb.count), m, desc, 32, 0, 3 + i, None, t_max, None,
         _lib.ptr(smin), _lib.ptr(sf), _lib.ptr(sb), None, None, None, None, None, 0.95, None,
         _lib.ptr(ws[i]), ws[i].numel(), stream.cuda_stream), "sample_update")
