@@ -13,7 +13,7 @@
 #define RS_THREADS 256
 #define RS_PER_THREAD 16
 #define RS_CELLS_PER_BLOCK (RS_THREADS * RS_PER_THREAD)
-#define RS_TAB 1024  // per-axis weight table entries (dims <= 1024)
+#define RS_TAB_MAX 1365  // per-axis table entries: 3 axes x 12 B within the 48 KB default
 
 namespace rtsdf {
 
@@ -24,6 +24,7 @@ struct RsParams {
     double d;
     int64_t c0, n_cells;  // global cells [c0, c0 + n_cells); buffers global-indexed
     FastDiv div_ny, div_nz;
+    int tab;  // per-axis weight table entries in dynamic shared memory (0: no tables)
 };
 
 // raysample.py:97-101: fine centres measured from the COARSE lo, then the
@@ -49,8 +50,10 @@ __global__ void __launch_bounds__(RS_THREADS) resample_mask_kernel(
     const uint8_t* __restrict__ mask_old, float* __restrict__ run_min,
     int32_t* __restrict__ front, int32_t* __restrict__ back) {
     __shared__ int warp_sum[RS_THREADS / 32];
-    __shared__ double tf[3][RS_TAB];
-    __shared__ int ti[3][RS_TAB];
+    extern __shared__ double rs_tab[];  // tf[3][P.tab] doubles, then ti[3][P.tab] ints
+    const int T = P.tab;
+    double* tfb = rs_tab;
+    int* tib = (int*)(rs_tab + 3 * T);
     const int64_t base = P.c0 + (int64_t)blockIdx.x * RS_CELLS_PER_BLOCK;
     const int64_t last = min(base + RS_CELLS_PER_BLOCK, P.c0 + P.n_cells) - 1;
     int i0, j0, k0, i1, j1, k1;
@@ -60,7 +63,7 @@ __global__ void __launch_bounds__(RS_THREADS) resample_mask_kernel(
     const int xs = i0, xn = i1 - i0 + 1;
     const int ys = i0 == i1 ? j0 : 0, yn = i0 == i1 ? j1 - j0 + 1 : P.fny;
     const int zs = (i0 == i1 && j0 == j1) ? k0 : 0, zn = (i0 == i1 && j0 == j1) ? k1 - k0 + 1 : P.fnz;
-    const bool tab = xn <= RS_TAB;  // yn, zn <= 1024 always
+    const bool tab = xn <= T && yn <= T && zn <= T;  // host: T >= fny, fnz when T > 0
     if (tab) {
         const FieldView& f = P.coarse;
         for (int t = threadIdx.x; t < xn + yn + zn; t += RS_THREADS) {
@@ -76,8 +79,8 @@ __global__ void __launch_bounds__(RS_THREADS) resample_mask_kernel(
                 ax = 2, e = t - xn - yn;
                 w = fine_axis(f.loz, P.fhz, f.hz, f.nz, zs + e);
             }
-            tf[ax][e] = w.f;
-            ti[ax][e] = w.i;
+            tfb[ax * T + e] = w.f;
+            tib[ax * T + e] = w.i;
         }
         __syncthreads();
     }
@@ -90,9 +93,9 @@ __global__ void __launch_bounds__(RS_THREADS) resample_mask_kernel(
         cell_ijk(P, (uint32_t)c, i, j, k);
         AxisW wx, wy, wz;
         if (tab) {
-            wx.i = ti[0][i - xs], wx.f = tf[0][i - xs];
-            wy.i = ti[1][j - ys], wy.f = tf[1][j - ys];
-            wz.i = ti[2][k - zs], wz.f = tf[2][k - zs];
+            wx.i = tib[i - xs], wx.f = tfb[i - xs];
+            wy.i = tib[T + j - ys], wy.f = tfb[T + j - ys];
+            wz.i = tib[2 * T + k - zs], wz.f = tfb[2 * T + k - zs];
             wx.j = P.coarse.nx > 1 ? wx.i + 1 : wx.i;
             wy.j = P.coarse.ny > 1 ? wy.i + 1 : wy.i;
             wz.j = P.coarse.nz > 1 ? wz.i + 1 : wz.i;
@@ -137,8 +140,10 @@ __global__ void __launch_bounds__(RS_THREADS) resample_mask4_kernel(
     const uint8_t* __restrict__ mask_old, float* __restrict__ run_min,
     int32_t* __restrict__ front, int32_t* __restrict__ back) {
     __shared__ int warp_sum[RS_THREADS / 32];
-    __shared__ double tf[3][RS_TAB];
-    __shared__ int ti[3][RS_TAB];
+    extern __shared__ double rs_tab[];  // tf[3][P.tab] doubles, then ti[3][P.tab] ints (host: tables fit)
+    const int T = P.tab;
+    double* tfb = rs_tab;
+    int* tib = (int*)(rs_tab + 3 * T);
     const int64_t base = P.c0 + (int64_t)blockIdx.x * RS_CELLS_PER_BLOCK;
     const int64_t last = min(base + RS_CELLS_PER_BLOCK, P.c0 + P.n_cells) - 1;
     int i0, j0, k0, i1, j1, k1;
@@ -148,7 +153,7 @@ __global__ void __launch_bounds__(RS_THREADS) resample_mask4_kernel(
     const int ys = i0 == i1 ? j0 : 0, yn = i0 == i1 ? j1 - j0 + 1 : P.fny;
     const int zs = (i0 == i1 && j0 == j1) ? k0 : 0, zn = (i0 == i1 && j0 == j1) ? k1 - k0 + 1 : P.fnz;
     const FieldView& f = P.coarse;
-    for (int t = threadIdx.x; t < xn + yn + zn; t += RS_THREADS) {  // host: xn <= RS_TAB
+    for (int t = threadIdx.x; t < xn + yn + zn; t += RS_THREADS) {  // host: xn, yn, zn <= T
         AxisW w;
         int ax, e;
         if (t < xn) {
@@ -161,8 +166,8 @@ __global__ void __launch_bounds__(RS_THREADS) resample_mask4_kernel(
             ax = 2, e = t - xn - yn;
             w = fine_axis(f.loz, P.fhz, f.hz, f.nz, zs + e);
         }
-        tf[ax][e] = w.f;
-        ti[ax][e] = w.i;
+        tfb[ax * T + e] = w.f;
+        tib[ax * T + e] = w.i;
     }
     __syncthreads();
     const int64_t sx = (int64_t)f.ny * f.nz, sy = f.nz;
@@ -174,8 +179,8 @@ __global__ void __launch_bounds__(RS_THREADS) resample_mask4_kernel(
         if (c > last) break;
         int i, j, k;
         cell_ijk(P, (uint32_t)c, i, j, k);
-        const int xi = ti[0][i - xs], yi = ti[1][j - ys];
-        const double fx = tf[0][i - xs], fy = tf[1][j - ys];
+        const int xi = tib[i - xs], yi = tib[T + j - ys];
+        const double fx = tfb[i - xs], fy = tfb[T + j - ys];
         const double ofx = __dsub_rn(1.0, fx), ofy = __dsub_rn(1.0, fy);
         const float* r00 = f.data + xi * sx + yi * sy;           // (x.i, y.i)
         const float* r10 = f.data + (xi + dj) * sx + yi * sy;    // (x.j, y.i)
@@ -186,8 +191,8 @@ __global__ void __launch_bounds__(RS_THREADS) resample_mask4_kernel(
         const uint32_t mold = mask_old ? *(const uint32_t*)(mask_old + c) : 0u;
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
-            const int zi = ti[2][k + e - zs], zj = zi + djz;
-            const double fz = tf[2][k + e - zs], ofz = __dsub_rn(1.0, fz);
+            const int zi = tib[2 * T + k + e - zs], zj = zi + djz;
+            const double fz = tfb[2 * T + k + e - zs], ofz = __dsub_rn(1.0, fz);
             // trilinear_w's arithmetic, term for term (field.py:95-128)
             const double c000 = __ldg(r00 + zi), c100 = __ldg(r10 + zi), c010 = __ldg(r01 + zi),
                          c110 = __ldg(r11 + zi), c001 = __ldg(r00 + zj), c101 = __ldg(r10 + zj),
@@ -371,17 +376,25 @@ extern "C" int rtsdf_resample_mask_range(const float* coarse, int cnx, int cny, 
     P.div_ny = make_fastdiv((uint32_t)fny);
     P.div_nz = make_fastdiv((uint32_t)fnz);
     int64_t nb = rtsdf_mask_blocks(n_range);
+    // per-axis weight tables sized for the planes / rows / columns one block of
+    // RS_CELLS_PER_BLOCK consecutive cells can touch (C3: 400 entries, 14 KB
+    // of shared memory instead of a fixed 36 KB -- more L1 for the gathers)
+    const int64_t planes = RS_CELLS_PER_BLOCK / ((int64_t)fny * fnz) + 2;  // >= planes a block spans
+    int64_t T = fnz > fny ? fnz : fny;
+    const int64_t xmax = planes < fnx ? planes : fnx;
+    if (xmax > T) T = xmax;
+    P.tab = T <= RS_TAB_MAX ? (int)T : 0;
+    const size_t smem = (size_t)P.tab * 3 * (sizeof(double) + sizeof(int));
     // vector form: rows split into whole 4-cell groups, 16 / 4-byte aligned
-    // buffers, weight tables for every block (fine planes per block <= RS_TAB)
+    // buffers, weight tables for every block
     auto al = [](const void* q, uintptr_t a) { return ((uintptr_t)q & (a - 1)) == 0; };
-    const bool vec = fnz % 4 == 0 && c0 % 4 == 0 && n_range % 4 == 0 &&
-                     (int64_t)fny * fnz >= RS_CELLS_PER_BLOCK / RS_TAB + 1 && al(c_fine, 16) &&
-                     al(mask_new, 4) && al(mask_old, 4);
+    const bool vec = P.tab > 0 && fnz % 4 == 0 && c0 % 4 == 0 && n_range % 4 == 0 &&
+                     al(c_fine, 16) && al(mask_new, 4) && al(mask_old, 4);
     if (vec)
-        resample_mask4_kernel<<<(unsigned)nb, RS_THREADS, 0, (cudaStream_t)stream>>>(
+        resample_mask4_kernel<<<(unsigned)nb, RS_THREADS, smem, (cudaStream_t)stream>>>(
             P, c_fine, out_unmasked, mask_new, block_counts, mask_old, run_min, front, back);
     else
-        resample_mask_kernel<<<(unsigned)nb, RS_THREADS, 0, (cudaStream_t)stream>>>(
+        resample_mask_kernel<<<(unsigned)nb, RS_THREADS, smem, (cudaStream_t)stream>>>(
             P, c_fine, out_unmasked, mask_new, block_counts, mask_old, run_min, front, back);
     count_launch();
     return check_launch("resample_mask");

@@ -585,11 +585,12 @@ def test_reference_visibility_matches_reference(rt):
     assert img.shape == (scene.camera.height, scene.camera.width, 3) and np.isfinite(img).all()
 
 
-def test_frame_on_an_axis_beyond_1024(rt):
+@pytest.mark.parametrize("dims", [(1040, 14, 12), (12, 10, 1100)])
+def test_frame_on_an_axis_beyond_1024(rt, dims):
     """A hybrid frame on a grid with one axis past the packed 10:10:10 seed
-    layout (dims-dependent packed seeds, per-cell JFA kernel) == the oracle."""
+    layout (dims-dependent packed seeds, per-cell JFA kernel; resample weight
+    tables sized from the dims) == the oracle."""
     scene = rt.get_scene("sphere")
-    dims = (1040, 14, 12)
     cfg = rt.PipelineConfig(coarse_dims=dims, fine_dims=dims,
                             sampling=rt.SamplingParams(rays_per_frame=4, mask_distance=0.3))
     pipe = rt.FramePipeline(scene, cfg)
