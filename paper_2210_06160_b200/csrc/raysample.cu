@@ -277,10 +277,9 @@ __device__ __forceinline__ double wf_trace4_root(const SampleParams& P, double o
     int best_facing = 0;
     float tb = P.tb;
     const FastNode4* nd = P.bvh4.nodes;
-    const float4 lx = __ldg((const float4*)nd->lox), ly = __ldg((const float4*)nd->loy),
-                 lz = __ldg((const float4*)nd->loz), hx = __ldg((const float4*)nd->hix),
-                 hy = __ldg((const float4*)nd->hiy), hz = __ldg((const float4*)nd->hiz);
-    const int4 ch = __ldg((const int4*)nd->child);
+    float4 lx, ly, lz, hx, hy, hz;
+    int4 ch;
+    load_node4(nd, lx, ly, lz, hx, hy, hz, ch);
     float t[4];
     t[0] = box_entry(lx.x, ly.x, lz.x, hx.x, hy.x, hz.x, r, tb);
     t[1] = box_entry(lx.y, ly.y, lz.y, hx.y, hy.y, hz.y, r, tb);
