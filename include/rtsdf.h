@@ -208,7 +208,8 @@ int64_t rtsdf_bvh4_collapse_host(const double* node_lo, const double* node_hi,
                                  const int32_t* node_left, const int32_t* node_right,
                                  int64_t n_nodes, void* out_nodes4, int64_t cap);
 /* Pack the flat BVH (device SoA as in BvhIndex, geometry.py:186-195) into the
- * device traversal layout: nodes (64 B each) and triangles (128 B each).    */
+ * device traversal layout: nodes (64 B each) and triangles (128 B each); the
+ * size is rounded up to 128 B (a BVH4 collapse appended there is aligned). */
 size_t rtsdf_bvh_packed_bytes(int64_t n_nodes, int64_t n_tris);
 int rtsdf_bvh_pack(const double* node_lo, const double* node_hi, const int32_t* node_left,
                    const int32_t* node_right, const int32_t* order, const double* tri_a,

@@ -510,7 +510,7 @@ extern "C" int64_t rtsdf_bvh4_collapse_host(const double* node_lo, const double*
 }
 
 extern "C" size_t rtsdf_bvh_packed_bytes(int64_t n_nodes, int64_t n_tris) {
-    return fast_offset_tris(n_nodes, n_tris) + (size_t)n_tris * sizeof(FastTri);
+    return fast_packed_bytes(n_nodes, n_tris);  // a BVH4 collapse is appended at this offset
 }
 
 extern "C" int rtsdf_bvh_pack(const double* node_lo, const double* node_hi,

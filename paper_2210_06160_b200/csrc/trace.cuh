@@ -280,14 +280,19 @@ struct FastBvh4 {
     const BvhTri* exact;
 };
 
+// End of the packed binary search tree, rounded up to 128 B: the BVH4 nodes
+// appended there are 128-B aligned (load_node4's 256-bit loads need 32 B).
+__host__ __device__ inline size_t fast_packed_bytes(int64_t n_nodes, int64_t n_tris) {
+    return (fast_offset_tris(n_nodes, n_tris) + (size_t)n_tris * sizeof(FastTri) + 127) & ~(size_t)127;
+}
+
 __host__ __device__ inline FastBvh4 fast_bvh4_view(const void* packed, int64_t n_nodes,
                                                    int64_t n_tris) {
     FastBvh4 f;
     const char* p = (const char*)packed;
     f.exact = (const BvhTri*)(p + (size_t)n_nodes * sizeof(BvhNode));
     f.tris = (const FastTri*)(p + fast_offset_tris(n_nodes, n_tris));
-    f.nodes = (const FastNode4*)(p + fast_offset_tris(n_nodes, n_tris) +
-                                 (size_t)n_tris * sizeof(FastTri));
+    f.nodes = (const FastNode4*)(p + fast_packed_bytes(n_nodes, n_tris));
     return f;
 }
 
