@@ -32,6 +32,18 @@ def test_library_exports_every_header_symbol():
     assert lib.rtsdf_version().decode().startswith("rtsdf-b200")
 
 
+def test_bvh4_nodes_are_128_byte_aligned_in_the_packed_layout():
+    """The BVH4 collapse is appended at rtsdf_bvh_packed_bytes: a multiple of
+    128 B, so its nodes (fetched with 256-bit loads) are aligned for any mesh."""
+    from paper_2210_06160_b200 import _lib
+
+    lib = _lib.lib()
+    for n_nodes, n_tris in ((1, 1), (3, 2), (1023, 1282), (2047, 7716), (1048575, 1310720), (7, 5)):
+        nb = int(lib.rtsdf_bvh_packed_bytes(n_nodes, n_tris))
+        assert nb % 128 == 0, (n_nodes, n_tris, nb)
+        assert nb >= n_nodes * 64 + n_tris * (128 + 48)
+
+
 def test_library_is_sm100a():
     import subprocess
 
