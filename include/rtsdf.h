@@ -202,8 +202,11 @@ int64_t rtsdf_bvh_build_sah_host(const double* tri_lo, const double* tri_hi, int
                                  int max_leaf, double* node_lo, double* node_hi,
                                  int32_t* node_left, int32_t* node_right, int32_t* order);
 /* Collapse a flat binary tree into 4-wide nodes (128 B: padded fp32 child
- * boxes + child refs) for the K6 search; host in/out.  Returns node count or
- * < 0 (capacity).                                                           */
+ * boxes + child refs) for the K6 search; host in/out.  Each node is written
+ * as 8 interleaved octant copies (record 8 i + o: the x / y / z lo and hi
+ * planes swapped where bit 0 / 1 / 2 of o is set; inner child refs = 8 i), so
+ * a ray reads its near planes from the lo slots.  cap and the return value
+ * count 128-B records (8 per node); < 0: capacity.                          */
 int64_t rtsdf_bvh4_collapse_host(const double* node_lo, const double* node_hi,
                                  const int32_t* node_left, const int32_t* node_right,
                                  int64_t n_nodes, void* out_nodes4, int64_t cap);

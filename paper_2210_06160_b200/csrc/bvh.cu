@@ -501,12 +501,28 @@ extern "C" int64_t rtsdf_bvh4_collapse_host(const double* node_lo, const double*
     for (int a = 0; a < 3; ++a) m = fmax(m, fmax(fabs(node_lo[a]), fabs(node_hi[a])));
     c.pad = (float)(1e-5 * m);
     c.build(0);
-    if ((int64_t)c.out.size() > cap) {
-        set_error("bvh4_collapse: capacity %lld < %lld nodes", (long long)cap, (long long)c.out.size());
+    // octant copies, interleaved: record 8 i + o is node i with the x / y / z
+    // planes swapped where bit 0 / 1 / 2 of o is set, so a ray whose inverse
+    // direction has those signs finds its near planes in the lo slots; inner
+    // child refs are record indices of copy 0 (8 i)
+    const int64_t n = (int64_t)c.out.size(), total = 8 * n;
+    if (total > cap || total > 0x7ffffff0ll) {
+        set_error("bvh4_collapse: capacity %lld < %lld records", (long long)cap, (long long)total);
         return -1;
     }
-    memcpy(out_nodes4, c.out.data(), c.out.size() * sizeof(FastNode4));
-    return (int64_t)c.out.size();
+    FastNode4* out = (FastNode4*)out_nodes4;
+    for (int64_t i = 0; i < n; ++i)
+        for (int o = 0; o < 8; ++o) {
+            FastNode4 f = c.out[i];
+            for (int q = 0; q < 4; ++q) {
+                if (f.child[q] >= 0 && f.child[q] != 0x7fffffff) f.child[q] *= 8;
+                if (o & 1) std::swap(f.lox[q], f.hix[q]);
+                if (o & 2) std::swap(f.loy[q], f.hiy[q]);
+                if (o & 4) std::swap(f.loz[q], f.hiz[q]);
+            }
+            out[8 * i + o] = f;
+        }
+    return total;
 }
 
 extern "C" size_t rtsdf_bvh_packed_bytes(int64_t n_nodes, int64_t n_tris) {

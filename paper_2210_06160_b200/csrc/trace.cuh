@@ -110,6 +110,29 @@ __host__ __device__ inline float tmax_bound(double t_max) {
 #endif
 }
 
+// Octant of a ray: bit a set when the axis-a inverse direction is negative
+// (its sign bit: clamp_inv keeps the sign of a (near-)zero component).
+__device__ __forceinline__ int ray_octant(float ix, float iy, float iz) {
+    return (int)((__float_as_uint(ix) >> 31) | ((__float_as_uint(iy) >> 31) << 1) |
+                 ((__float_as_uint(iz) >> 31) << 2));
+}
+
+// Slab test on a ray-octant copy of the boxes (rtsdf_bvh4_collapse_host):
+// n* hold the planes nearer along the ray, f* the farther ones.  fmaf is
+// monotonic in the plane for a fixed-sign ix, so these are exactly box_entry's
+// min / max pairs -- the same entry t bit for bit -- without the six pair
+// min / max instructions; t_best folds into the exit side (tmin <= min(tmax,
+// t_best) is box_entry's two tests).
+__device__ __forceinline__ float box_entry_nf(float nx, float ny, float nz, float fx, float fy,
+                                              float fz, const RayF& r, float t_best) {
+    const float tx0 = fmaf(nx, r.ix, -r.oix), tx1 = fmaf(fx, r.ix, -r.oix);
+    const float ty0 = fmaf(ny, r.iy, -r.oiy), ty1 = fmaf(fy, r.iy, -r.oiy);
+    const float tz0 = fmaf(nz, r.iz, -r.oiz), tz1 = fmaf(fz, r.iz, -r.oiz);
+    const float tmin = fmaxf(fmaxf(tx0, ty0), fmaxf(tz0, 0.0f));
+    const float tmax = fminf(fminf(tx1, ty1), fminf(tz1, t_best));
+    return tmin <= tmax ? tmin : RTSDF_FINF;
+}
+
 // Padded child box slab test: entry t (>= 0) or +inf if missed / beyond t_best.
 __device__ __forceinline__ float box_entry(float lx, float ly, float lz, float hx, float hy,
                                            float hz, const RayF& r, float t_best) {
@@ -249,10 +272,13 @@ __device__ __forceinline__ double trace_fast(const FastBvh& b, double ox, double
 // half the depth, four independent slab tests per node fetch (more ILP, fewer
 // divergent loop trips).  Same conservative padding, same pre-test and exact
 // confirm, so the result is the same brute-force closest hit.
+// Stored as 8 interleaved ray-octant copies (record 8 i + o, lo / hi swapped
+// on the axes set in o): traversal starts at record `octant` and adds it to
+// every inner child ref.
 struct __align__(128) FastNode4 {
     float lox[4], loy[4], loz[4];
     float hix[4], hiy[4], hiz[4];
-    int32_t child[4];  // >= 0 node4 index; < 0 leaf -(start * 8 + count) - 1; INT_MAX empty
+    int32_t child[4];  // >= 0 record of copy 0 (8 i); < 0 leaf -(start * 8 + count) - 1; INT_MAX empty
     int32_t pad[4];
 };
 static_assert(sizeof(FastNode4) == 128, "node4 layout");
@@ -364,6 +390,7 @@ __device__ __forceinline__ double trace_fast4(const FastBvh4& b, double ox, doub
     float tb = tb0;  // tmax_bound(t_max), computed once by the caller
     int sp = 0;
     int32_t node = 0;
+    const FastNode4* base = b.nodes + ray_octant(r.ix, r.iy, r.iz);  // this ray's copy
     if (complete) *complete = true;
     while (true) {
         if (node >= 0) {
@@ -371,16 +398,16 @@ __device__ __forceinline__ double trace_fast4(const FastBvh4& b, double ox, doub
                 if (complete) *complete = false;
                 break;
             }
-            const FastNode4* nd = b.nodes + node;
+            const FastNode4* nd = base + node;
             RTSDF_TSTAT(0, 1);
             float4 lx, ly, lz, hx, hy, hz;
             int4 ch;
             load_node4(nd, lx, ly, lz, hx, hy, hz, ch);
             float t[4];
-            t[0] = box_entry(lx.x, ly.x, lz.x, hx.x, hy.x, hz.x, r, tb);
-            t[1] = box_entry(lx.y, ly.y, lz.y, hx.y, hy.y, hz.y, r, tb);
-            t[2] = box_entry(lx.z, ly.z, lz.z, hx.z, hy.z, hz.z, r, tb);
-            t[3] = box_entry(lx.w, ly.w, lz.w, hx.w, hy.w, hz.w, r, tb);
+            t[0] = box_entry_nf(lx.x, ly.x, lz.x, hx.x, hy.x, hz.x, r, tb);
+            t[1] = box_entry_nf(lx.y, ly.y, lz.y, hx.y, hy.y, hz.y, r, tb);
+            t[2] = box_entry_nf(lx.z, ly.z, lz.z, hx.z, hy.z, hz.z, r, tb);
+            t[3] = box_entry_nf(lx.w, ly.w, lz.w, hx.w, hy.w, hz.w, r, tb);
             int32_t c[4] = {ch.x, ch.y, ch.z, ch.w};
             // nearest hit child is visited next; the other hits go on the stack
             int nearest = -1;

@@ -178,7 +178,7 @@ class BvhIndex:
     # K6 search tree (binned SAH) in the packed device layout, and its node count
     search: torch.Tensor = dc_field(repr=False, compare=False, default=None)
     search_nodes: int = 0
-    search_nodes4: int = 0  # > 0: BVH4 collapse appended to `search`
+    search_nodes4: int = 0  # > 0: BVH4 records (8 octant copies per node) appended to `search`
     search_stack4: int = 0  # > 0: stack entries its traversal can need (3 per level)
 
     @property
@@ -239,7 +239,7 @@ def build_bvh(mesh: TriangleMesh) -> BvhIndex:
     if USE_BVH4:
         slo_c, shi_c = np.ascontiguousarray(slo), np.ascontiguousarray(shi)
         sl_c, sr_c = np.ascontiguousarray(sl), np.ascontiguousarray(sr)
-        nodes4 = np.empty((max(int(ns), 1), 128), dtype=np.uint8)
+        nodes4 = np.empty((8 * max(int(ns), 1), 128), dtype=np.uint8)  # 8 octant records per node
         n4 = int(L.rtsdf_bvh4_collapse_host(*[_lib.host_ptr(x) for x in (slo_c, shi_c, sl_c, sr_c)],
                                             int(ns), _lib.host_ptr(nodes4), nodes4.shape[0]))
         stack4 = 3 * _depth4(nodes4[:n4]) if n4 > 0 else 0
