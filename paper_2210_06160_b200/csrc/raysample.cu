@@ -562,7 +562,10 @@ __global__ void __launch_bounds__(WF_OCT_THREADS) wf_oct_scatter_kernel(int64_t 
 // tree and one more resident block: C3 pass 2 2.22 -> 2.10 ms).
 #define WF2_SMALL_STACK 24
 template <bool WIDE, int STK>
-__global__ void __launch_bounds__(WF_THREADS, STK <= WF2_SMALL_STACK ? WF_MINB + 1 : WF_MINB)
+#ifndef WF2_MINB
+#define WF2_MINB (WF_MINB + 1)  // small-stack pass 2: resident blocks per SM
+#endif
+__global__ void __launch_bounds__(WF_THREADS, STK <= WF2_SMALL_STACK ? WF2_MINB : WF_MINB)
     wf_pass2_kernel(SampleParams P, WfBuffers B) {
     __shared__ int32_t stack_mem[STK * WF_THREADS];
     __shared__ __half tstack_mem[WIDE ? STK * WF_THREADS : 1];

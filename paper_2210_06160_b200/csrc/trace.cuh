@@ -426,7 +426,12 @@ __device__ __forceinline__ double trace_fast4(const FastBvh4& b, double ox, doub
                     ++sp;
                 }
             if (nearest >= 0) {
-                node = c[nearest];
+                // select, not c[nearest]: a dynamic index puts c[] in local
+                // memory (a 16-B spill store + reload per visit, measured)
+                int32_t cn = c[0];
+#pragma unroll
+                for (int q = 1; q < 4; ++q) cn = nearest == q ? c[q] : cn;
+                node = cn;
                 continue;
             }
         } else {
