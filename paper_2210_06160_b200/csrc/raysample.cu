@@ -342,7 +342,8 @@ __device__ __forceinline__ double wf_trace(const SampleParams& P, double ox, dou
 // entry, a BVH4 visit <= 3, and at most budget - 1 visits complete, so a small
 // shared stack suffices (measured: no change at 6 / 7 / 8 resident blocks; a
 // two-chunk form that generates both chunks' directions before tracing, for
-// fp64 ILP, measured 2.55 -> 2.69 ms).
+// fp64 ILP, measured 2.55 -> 2.69 ms; loading the next grid-stride step's
+// texel record one step ahead measured 2.47 -> 2.57 ms: 32 B of spills).
 #define WF1_STACK (3 * (WF_BUDGET4 - 1) > WF_BUDGET - 1 ? 3 * (WF_BUDGET4 - 1) : WF_BUDGET - 1)
 static_assert(WF1_STACK >= WF_BUDGET - 1 && WF1_STACK >= 3 * (WF_BUDGET4 - 1), "pass-1 stack");
 template <bool WIDE>
