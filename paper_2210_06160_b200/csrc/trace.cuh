@@ -410,6 +410,8 @@ __device__ __forceinline__ double trace_fast4(const FastBvh4& b, double ox, doub
             t[3] = box_entry_nf(lx.w, ly.w, lz.w, hx.w, hy.w, hz.w, r, tb);
             int32_t c[4] = {ch.x, ch.y, ch.z, ch.w};
             // nearest hit child is visited next; the other hits go on the stack
+            // (a full sort that pushes them farthest first measured 1.93 ->
+            // 2.17 ms in pass 2)
             int nearest = -1;
             float tn = RTSDF_FINF;
 #pragma unroll
