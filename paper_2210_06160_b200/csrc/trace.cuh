@@ -330,6 +330,9 @@ __device__ __forceinline__ bool leaf_tris(const FastTri* __restrict__ tris, cons
     const int32_t code = -ref - 1;
     const int start = code >> 3, count = code & 7;
     bool improved = false;
+    // (all pre-tests of the leaf first, then the exact tests of the candidates
+    // -- fewer divergent exact-path trips, but the pre-tests lose the tighter
+    // tb of an earlier exact hit in the same leaf: pass 2 1.93 -> 2.19 ms)
     for (int k = start; k < start + count; ++k) {
         const FastTri* ft = tris + k;
         float4 f0 = __ldg((const float4*)&ft->a[0]);
