@@ -47,7 +47,7 @@ namespace rtsdf {
 namespace gs {
 
 #ifdef __CUDACC__
-#define RTSDF_GS_TABLE_DECL __device__ const double gs_table_dev[RTSDF_GS_TABLE_N]
+#define RTSDF_GS_TABLE_DECL __device__ __align__(32) const double gs_table_dev[RTSDF_GS_TABLE_N]
 #include "glibc_sincostab.inc"
 #undef RTSDF_GS_TABLE_DECL
 #endif
@@ -55,11 +55,19 @@ namespace gs {
 #include "glibc_sincostab.inc"
 #undef RTSDF_GS_TABLE_DECL
 
-GS_HD double tab(int i) {
+// the four entries {sin hi, sin lo, cos hi, cos lo} of table row k (k % 4 == 0):
+// one 256-bit load of one 32-B sector on the device instead of four 64-bit
+// loads of per-lane random sectors
+GS_HD void tab4(int k, double& sn, double& ssn, double& cs, double& ccs) {
 #if defined(__CUDA_ARCH__)
-    return __ldg(gs_table_dev + i);  // per-lane indices: L1, not the constant cache
+    asm("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];"
+        : "=d"(sn), "=d"(ssn), "=d"(cs), "=d"(ccs)
+        : "l"(gs_table_dev + k));
 #else
-    return gs_table_host[i];
+    sn = gs_table_host[k];
+    ssn = gs_table_host[k + 1];
+    cs = gs_table_host[k + 2];
+    ccs = gs_table_host[k + 3];
 #endif
 }
 
@@ -132,7 +140,8 @@ GS_HD double do_sin(double x, double dx) {
     const double xx = GS_MUL(x, x);
     const double s = GS_ADD(x, GS_FMA(GS_MUL(x, xx), GS_FMA(xx, GS_SN5, GS_SN3), dx));
     const double c = GS_FMA(x, dx, GS_MUL(xx, GS_FMA(xx, GS_FMA(xx, GS_CS6, GS_CS4), GS_CS2)));
-    const double sn = tab(k), ssn = tab(k + 1), cs = tab(k + 2), ccs = tab(k + 3);
+    double sn, ssn, cs, ccs;
+    tab4(k, sn, ssn, cs, ccs);
     // cor = (ssn + s * ccs - sn * c) + cs * s
     const double cor = GS_FMA(s, cs, GS_FMA(gneg(c), sn, GS_FMA(s, ccs, ssn)));
     return gcopysign(GS_ADD(sn, cor), xold);
@@ -147,7 +156,8 @@ GS_HD double do_cos(double x, double dx) {
     const double xx = GS_MUL(x, x);
     const double s = GS_FMA(GS_MUL(x, xx), GS_FMA(xx, GS_SN5, GS_SN3), x);
     const double c = GS_MUL(xx, GS_FMA(xx, GS_FMA(xx, GS_CS6, GS_CS4), GS_CS2));
-    const double sn = tab(k), ssn = tab(k + 1), cs = tab(k + 2), ccs = tab(k + 3);
+    double sn, ssn, cs, ccs;
+    tab4(k, sn, ssn, cs, ccs);
     // cor = (ccs - s * ssn - cs * c) - sn * s
     const double cor = GS_FMA(gneg(s), sn, GS_FMA(gneg(c), cs, GS_FMA(gneg(s), ssn, ccs)));
     return GS_ADD(cs, cor);
@@ -235,7 +245,8 @@ GS_HD double do_sin_nb(double x, double dx) {
     const double s = GS_ADD(xr, GS_FMA(GS_MUL(xr, xx), GS_FMA(xx, GS_SN5, GS_SN3), d2));
     const double c = GS_FMA(xr, d2, GS_MUL(xx, GS_FMA(xx, GS_FMA(xx, GS_CS6, GS_CS4), GS_CS2)));
     const int kk = k < RTSDF_GS_TABLE_N - 3 ? k : 0;
-    const double sn = tab(kk), ssn = tab(kk + 1), cs = tab(kk + 2), ccs = tab(kk + 3);
+    double sn, ssn, cs, ccs;
+    tab4(kk, sn, ssn, cs, ccs);
     const double cor = GS_FMA(s, cs, GS_FMA(gneg(c), sn, GS_FMA(s, ccs, ssn)));
     const double tab_r = gcopysign(GS_ADD(sn, cor), xold);
     return sel(ax < 0.126, tay, tab_r);
