@@ -187,13 +187,14 @@ __device__ __forceinline__ double uniform01(uint64_t key, uint64_t counter) {
     uint64_t bits = mix64(key + counter * RTSDF_GOLDEN);
     return __dmul_rn((double)(bits >> 11), 1.0 / 9007199254740992.0);
 }
+__constant__ double k_two_pi = 6.283185307179586;  // a constant-bank operand, not two UMOVs per ray
 __device__ __forceinline__ void unit_sphere_dir(uint64_t key, uint64_t counter, double& dx,
                                                 double& dy, double& dz) {
     double u = uniform01(key, 2 * counter);
     double v = uniform01(key, 2 * counter + 1);
     double z = __dsub_rn(1.0, __dmul_rn(2.0, u));
     double r = __dsqrt_rn(dmax_(0.0, __dsub_rn(1.0, __dmul_rn(z, z))));
-    double phi = __dmul_rn(6.283185307179586, v);
+    double phi = __dmul_rn(k_two_pi, v);
     // rng.py:53 calls the host libm's cos / sin: its glibc FMA build, restated
     // bit for bit in glibc_sincos.cuh (CUDA's sincos differs in the last ulp);
     // the straight-line pair form keeps a warp's random phis on one path

@@ -96,25 +96,36 @@ GS_HD double gcopysign(double m, double s) {
 }
 
 // constants of s_sin.c / usncs.h (values as stored in the binary)
+// On the device the constants whose low word is non-zero are read from the
+// constant bank (a DFMA / DMUL / DADD operand, c[3][...]): as literals they were
+// re-materialised with two UMOVs per use inside the ray loop (~60 per ray).
+#ifdef __CUDACC__
+__constant__ double gs_kc[16] = {0x1.45f306dc9c883p-1, 0x1.921fb54442d18p+0, 0x1.1a62633145c07p-54, 0x1.921fb58p+0, -0x1.dde973cp-27, -0x1.cb3b398p-55, -0x1.d747f23e32ed7p-83, -0x1.5555555555515p-3, 0x1.11110e829872fp-7, -0x1.5555555555535p-5, 0x1.6c16bedd9e239p-10, -0x1.5555555555555p-3, 0x1.1111111110ecep-7, -0x1.a01a019db08b8p-13, 0x1.71de27b9a7ed9p-19, -0x1.addffc2fcdf59p-26};
+#endif
+#if defined(__CUDA_ARCH__)
+#define GS_K(i, v) (gs_kc[i])
+#else
+#define GS_K(i, v) (v)
+#endif
 #define GS_BIG 0x1.8p+45          // 52776558133248
 #define GS_TOINT 0x1.8p+52        // 6755399441055744
-#define GS_HPINV 0x1.45f306dc9c883p-1
-#define GS_HP0 0x1.921fb54442d18p+0
-#define GS_HP1 0x1.1a62633145c07p-54
-#define GS_MP1 0x1.921fb58p+0
-#define GS_MP2 -0x1.dde973cp-27
-#define GS_PP3 -0x1.cb3b398p-55
-#define GS_PP4 -0x1.d747f23e32ed7p-83
-#define GS_SN3 -0x1.5555555555515p-3
-#define GS_SN5 0x1.11110e829872fp-7
+#define GS_HPINV GS_K(0, 0x1.45f306dc9c883p-1)
+#define GS_HP0 GS_K(1, 0x1.921fb54442d18p+0)
+#define GS_HP1 GS_K(2, 0x1.1a62633145c07p-54)
+#define GS_MP1 GS_K(3, 0x1.921fb58p+0)
+#define GS_MP2 GS_K(4, -0x1.dde973cp-27)
+#define GS_PP3 GS_K(5, -0x1.cb3b398p-55)
+#define GS_PP4 GS_K(6, -0x1.d747f23e32ed7p-83)
+#define GS_SN3 GS_K(7, -0x1.5555555555515p-3)
+#define GS_SN5 GS_K(8, 0x1.11110e829872fp-7)
 #define GS_CS2 0x1p-1
-#define GS_CS4 -0x1.5555555555535p-5
-#define GS_CS6 0x1.6c16bedd9e239p-10
-#define GS_S1 -0x1.5555555555555p-3
-#define GS_S2 0x1.1111111110ecep-7
-#define GS_S3 -0x1.a01a019db08b8p-13
-#define GS_S4 0x1.71de27b9a7ed9p-19
-#define GS_S5 -0x1.addffc2fcdf59p-26
+#define GS_CS4 GS_K(9, -0x1.5555555555535p-5)
+#define GS_CS6 GS_K(10, 0x1.6c16bedd9e239p-10)
+#define GS_S1 GS_K(11, -0x1.5555555555555p-3)
+#define GS_S2 GS_K(12, 0x1.1111111110ecep-7)
+#define GS_S3 GS_K(13, -0x1.a01a019db08b8p-13)
+#define GS_S4 GS_K(14, 0x1.71de27b9a7ed9p-19)
+#define GS_S5 GS_K(15, -0x1.addffc2fcdf59p-26)
 
 // TAYLOR_SIN(xx, a, da) = a + ((POLY(xx) * a - 0.5 * da) * xx + da)
 // (__sin_fma: the chain of 5 vfmadd213sd, vfmsub132sd, vfmadd132sd, vaddsd)
