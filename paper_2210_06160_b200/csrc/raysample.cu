@@ -347,7 +347,10 @@ __device__ __forceinline__ double wf_trace(const SampleParams& P, double ox, dou
 #define WF1_STACK (3 * (WF_BUDGET4 - 1) > WF_BUDGET - 1 ? 3 * (WF_BUDGET4 - 1) : WF_BUDGET - 1)
 static_assert(WF1_STACK >= WF_BUDGET - 1 && WF1_STACK >= 3 * (WF_BUDGET4 - 1), "pass-1 stack");
 template <bool WIDE>
-__global__ void __launch_bounds__(WF_THREADS, WF_MINB) wf_pass1_kernel(SampleParams P, WfBuffers B, int budget) {
+#ifndef WF1_MINB
+#define WF1_MINB WF_MINB  // pass-1 resident blocks per SM (7 / 8 spill: 2.33 -> 2.39 / 2.40 ms)
+#endif
+__global__ void __launch_bounds__(WF_THREADS, WF1_MINB) wf_pass1_kernel(SampleParams P, WfBuffers B, int budget) {
     __shared__ int32_t stack_mem[WF1_STACK * WF_THREADS];
     __shared__ __half tstack_mem[WIDE ? WF1_STACK * WF_THREADS : 1];
     const int lane = threadIdx.x & 31;
