@@ -261,9 +261,13 @@ __device__ __forceinline__ void wf_ray(const SampleParams& P, const WfBuffers& B
 // from the root) -- trace_fast4's order and outcome with node budget 2.  A box
 // entry is a lower bound on every hit inside it, so the unreached children
 // cannot hold a closer hit than the one found.
+#ifndef WF1_SROOT
+#define WF1_SROOT 1
+#endif
+#define WF1_ROOT_STRIDE 36  // floats per staged root copy: 144 B, the 8 copies on disjoint banks
 __device__ __forceinline__ double wf_trace4_root(const SampleParams& P, double ox, double oy, double oz,
                                                  double dx, double dy, double dz, int32_t& out_id,
-                                                 int& out_facing, bool* done) {
+                                                 int& out_facing, bool* done, const float* sroot) {
     RayF r;
     r.ix = clamp_inv(dx);
     r.iy = clamp_inv(dy);
@@ -279,15 +283,35 @@ __device__ __forceinline__ double wf_trace4_root(const SampleParams& P, double o
     // the root's copy 0 (unswapped planes) with box_entry's min / max pairs: one
     // address for the whole warp (pass-1 rays mix all eight octants, and
     // per-lane octant copies measured 2.50 -> 2.72 ms in L1 wavefronts)
-    const FastNode4* nd = P.bvh4.nodes;
     float4 lx, ly, lz, hx, hy, hz;
     int4 ch;
-    load_node4(nd, lx, ly, lz, hx, hy, hz, ch);
     float t[4];
+#if WF1_SROOT
+    // the ray's octant copy of the root, staged in shared memory by the block
+    // (the global copies would cost 8 L1 wavefronts per load: pass-1 warps mix
+    // all octants): near planes in the lo slots, no pair min / max
+    {
+        const float* q = sroot + WF1_ROOT_STRIDE * ray_octant(r.ix, r.iy, r.iz);
+        lx = *(const float4*)(q);
+        ly = *(const float4*)(q + 4);
+        lz = *(const float4*)(q + 8);
+        hx = *(const float4*)(q + 12);
+        hy = *(const float4*)(q + 16);
+        hz = *(const float4*)(q + 20);
+        ch = *(const int4*)(q + 24);
+    }
+    t[0] = box_entry_nf(lx.x, ly.x, lz.x, hx.x, hy.x, hz.x, r, tb);
+    t[1] = box_entry_nf(lx.y, ly.y, lz.y, hx.y, hy.y, hz.y, r, tb);
+    t[2] = box_entry_nf(lx.z, ly.z, lz.z, hx.z, hy.z, hz.z, r, tb);
+    t[3] = box_entry_nf(lx.w, ly.w, lz.w, hx.w, hy.w, hz.w, r, tb);
+#else
+    (void)sroot;
+    load_node4(P.bvh4.nodes, lx, ly, lz, hx, hy, hz, ch);
     t[0] = box_entry(lx.x, ly.x, lz.x, hx.x, hy.x, hz.x, r, tb);
     t[1] = box_entry(lx.y, ly.y, lz.y, hx.y, hy.y, hz.y, r, tb);
     t[2] = box_entry(lx.z, ly.z, lz.z, hx.z, hy.z, hz.z, r, tb);
     t[3] = box_entry(lx.w, ly.w, lz.w, hx.w, hy.w, hz.w, r, tb);
+#endif
     const int32_t c[4] = {ch.x, ch.y, ch.z, ch.w};
     // near-first over the reachable children: an inner child first in line ends
     // pass 1 for this ray (pass 2 traces it from the root); a leaf is tested
@@ -325,12 +349,12 @@ template <bool WIDE>
 __device__ __forceinline__ double wf_trace(const SampleParams& P, double ox, double oy, double oz,
                                            double dx, double dy, double dz, int32_t* stack,
                                            __half* tstack, int32_t& id, int& facing, int budget,
-                                           bool* done) {
+                                           bool* done, const float* sroot = nullptr) {
 #ifndef WF1_ROOT
 #define WF1_ROOT 1
 #endif
     if (WIDE && WF1_ROOT && budget == 2)
-        return wf_trace4_root(P, ox, oy, oz, dx, dy, dz, id, facing, done);
+        return wf_trace4_root(P, ox, oy, oz, dx, dy, dz, id, facing, done, sroot);
     if (WIDE)
         return trace_fast4(P.bvh4, ox, oy, oz, dx, dy, dz, P.t_max, stack, tstack, WF_THREADS, id,
                            facing, P.tb, budget, done);
@@ -353,6 +377,12 @@ template <bool WIDE>
 __global__ void __launch_bounds__(WF_THREADS, WF1_MINB) wf_pass1_kernel(SampleParams P, WfBuffers B, int budget) {
     __shared__ int32_t stack_mem[WF1_STACK * WF_THREADS];
     __shared__ __half tstack_mem[WIDE ? WF1_STACK * WF_THREADS : 1];
+    __shared__ __align__(16) float sroot[WIDE && WF1_SROOT ? 8 * WF1_ROOT_STRIDE : 1];
+    if (WIDE && WF1_SROOT) {  // the root's 8 octant records (boxes + child refs, 112 B each)
+        for (int e = threadIdx.x; e < 8 * 28; e += blockDim.x)
+            sroot[(e / 28) * WF1_ROOT_STRIDE + e % 28] = __ldg((const float*)(P.bvh4.nodes + e / 28) + e % 28);
+        __syncthreads();
+    }
     const int lane = threadIdx.x & 31;
     const int64_t R = min(*P.count, P.m_cap) * P.x;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -374,7 +404,7 @@ __global__ void __launch_bounds__(WF_THREADS, WF1_MINB) wf_pass1_kernel(SamplePa
             int facing;
             bool done;
             double t = wf_trace<WIDE>(P, ox, oy, oz, dx, dy, dz, stack_mem + threadIdx.x,
-                                      tstack_mem + threadIdx.x, id, facing, budget, &done);
+                                      tstack_mem + threadIdx.x, id, facing, budget, &done, sroot);
             if (done && id >= 0) {
                 key = (unsigned long long)__double_as_longlong(t);
                 inc = facing == 1 ? 1u : 0x10000u;
