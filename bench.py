@@ -116,7 +116,7 @@ def peaks():
     return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-PROFILE = ROOT / "profiles" / "r2zi_frame_kernels_summary.csv"  # ncu --set full, one C3 frame
+PROFILE = ROOT / "profiles" / "r2zj_frame_kernels_summary.csv"  # ncu --set full, one C3 frame
 DENSE_KERNEL = "jfa_pass5_kernel<2, 2, 0"  # K2 v5 (jfa5.cuh), the dense passes k <= 16
 DENSE_MAX_K = 16
 
