@@ -610,7 +610,8 @@ __global__ void __launch_bounds__(WF_THREADS, STK <= WF2_SMALL_STACK ? WF2_MINB 
 #if WF2_DYN
     // warps claim 32-ray chunks of the queue dynamically (one atomic per chunk):
     // a warp that drew short rays takes the next chunk instead of idling at the
-    // end of a static grid-stride share
+    // end of a static grid-stride share (claiming the next chunk one step
+    // ahead, to overlap the atomic with the traversal, measured 1.92 -> 1.96 ms)
     const int lane = threadIdx.x & 31;
     while (true) {
         unsigned long long base = 0;
