@@ -83,6 +83,66 @@ def test_host_bvh_build_is_the_reference_tree(case):
     assert digest(order) == g["order"]
 
 
+def test_bvh4_collapse_writes_eight_octant_copies_per_node():
+    """rtsdf_bvh4_collapse_host: record 8 i + o is node i with the x / y / z lo
+    and hi planes swapped where bit 0 / 1 / 2 of o is set, inner child refs are
+    copy-0 records (multiples of 8), and every child box contains its
+    subtree's triangles (the traversal reads a ray's near planes from the lo
+    slots of its octant copy)."""
+    from paper_2210_06160_b200 import _lib
+
+    _, mesh = scene_mesh("sphere_plane")
+    v, t = mesh.vertices, mesh.triangles
+    p0, p1, p2 = v[t[:, 0]], v[t[:, 1]], v[t[:, 2]]
+    lo = np.ascontiguousarray(np.minimum(np.minimum(p0, p1), p2))
+    hi = np.ascontiguousarray(np.maximum(np.maximum(p0, p1), p2))
+    T = len(t)
+    L = _lib.lib()
+    slo, shi = np.empty((2 * T, 3)), np.empty((2 * T, 3))
+    sl, sr = np.empty(2 * T, np.int32), np.empty(2 * T, np.int32)
+    so = np.empty(T, np.int32)
+    ns = L.rtsdf_bvh_build_sah_host(_lib.host_ptr(lo), _lib.host_ptr(hi), T, 4,
+                                    *[_lib.host_ptr(a) for a in (slo, shi, sl, sr, so)])
+    assert ns > 0
+    recs = np.zeros((8 * ns, 128), np.uint8)
+    n4 = L.rtsdf_bvh4_collapse_host(*[_lib.host_ptr(np.ascontiguousarray(a[:ns])) for a in (slo, shi, sl, sr)],
+                                    int(ns), _lib.host_ptr(recs), recs.shape[0])
+    assert n4 > 0 and n4 % 8 == 0
+    assert L.rtsdf_bvh4_collapse_host(*[_lib.host_ptr(np.ascontiguousarray(a[:ns])) for a in (slo, shi, sl, sr)],
+                                      int(ns), _lib.host_ptr(recs), n4 - 1) < 0  # capacity counts records
+    f = recs[:n4].view(np.float32).reshape(-1, 8, 32)
+    c = recs[:n4].view(np.int32).reshape(-1, 8, 32)[:, :, 24:28]
+    base = f[:, 0, :24].reshape(-1, 6, 4)  # lox, loy, loz, hix, hiy, hiz
+    for o in range(8):
+        want = base.copy()
+        for a in range(3):
+            if o >> a & 1:
+                want[:, [a, a + 3]] = want[:, [a + 3, a]]
+        assert np.array_equal(f[:, o, :24].reshape(-1, 6, 4), want), o
+        assert np.array_equal(c[:, o], c[:, 0]), o
+    inner = c[:, 0][(c[:, 0] >= 0) & (c[:, 0] != 0x7FFFFFFF)]
+    assert len(inner) and np.all(inner % 8 == 0) and np.all(inner < n4)
+    # every triangle sits inside the padded box of each BVH4 child on its path
+    order = so[:T]
+    tri_lo, tri_hi = lo[order], hi[order]
+
+    def check(rec, blo, bhi):
+        for q in range(4):
+            ref = int(c[rec // 8, 0, q])
+            if ref == 0x7FFFFFFF:
+                continue
+            qlo = np.array([base[rec // 8, a, q] for a in range(3)], np.float64)
+            qhi = np.array([base[rec // 8, 3 + a, q] for a in range(3)], np.float64)
+            if ref < 0:
+                code = -ref - 1
+                s0, cnt = code >> 3, code & 7
+                assert np.all(tri_lo[s0:s0 + cnt] >= qlo) and np.all(tri_hi[s0:s0 + cnt] <= qhi)
+            else:
+                check(ref, qlo, qhi)
+
+    check(0, None, None)
+
+
 @pytest.mark.parametrize("name,key", [("sphere", "c1"), ("sphere_plane", "c3")])
 def test_scene_meshes_match_reference(name, key):
     _, mesh = scene_mesh(name)
